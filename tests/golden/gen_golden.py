@@ -1,0 +1,148 @@
+"""Generate the committed golden fixtures by running the REAL reference.
+
+Run here (the dev container, where /root/reference exists):
+
+    python tests/golden/gen_golden.py
+
+For every case it runs the reference pipeline
+  parse_program -> bind_dims -> elaborate -> classify_loops
+  (tilecc/pipeline.py:37-43) -> run_autoscheduler (tilecc/autosched/scheduler.py:73)
+  -> lower_seed (tilecc/pipeline.py:46-55)
+and writes
+  <case>.seed<k>.ma.json   MA module (paper_2604_14825_b200.ma_ir JSON)
+  <case>.seed<k>.ma.txt    emit_tile_text(ma, "generic") (tilecc/ma/emit.py:32)
+  <case>.seed<k>.schedule.jsonl  serialize_schedule (tilecc/schedule/steps.py:87)
+  <case>.seed<k>.cost.json cost_model(ma).to_json() (tilecc/ma/cost.py:66)
+and, for cases with `io`, the bf16-representable inputs (as bf16 bits), the
+reference interpret_ma fp32 output (tilecc/ma/interp.py:102) and the fp64
+oracle_eval output (tilecc/frontend/oracle.py:25) plus the dynamic CostReport.
+
+Inputs follow tests/conftest.py:65-67 (`gaussian_inputs`: default_rng(seed)
+standard_normal per input in input order), optionally scaled, then rounded
+to bf16 so the GPU sees identical values (BASELINE.md parity protocol).
+"""
+
+from __future__ import annotations
+
+import json
+import math
+import os
+import sys
+from dataclasses import replace
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, REPO)
+sys.path.insert(0, "/root/reference/pkg/src")
+
+from tilecc.autosched.scheduler import SchedulerOptions, run_autoscheduler  # noqa: E402
+from tilecc.frontend.oracle import oracle_eval  # noqa: E402
+from tilecc.ma.device import DEFAULT_DEVICE  # noqa: E402
+from tilecc.ma.emit import emit_tile_text  # noqa: E402
+from tilecc.ma.interp import interpret_ma  # noqa: E402
+from tilecc.pipeline import frontend, lower_seed  # noqa: E402
+from tilecc.schedule.steps import serialize_schedule  # noqa: E402
+
+from oracle.ma_interp import bf16_bits, causal_mask, round_bf16  # noqa: E402
+from paper_2604_14825_b200 import ma_ir  # noqa: E402
+from paper_2604_14825_b200.programs import PROGRAMS  # noqa: E402
+
+
+def write(path, text):
+    with open(path, "w") as f:
+        f.write(text)
+
+
+def make_inputs(bound, seed, scales, mask):
+    rng = np.random.default_rng(seed)
+    out = {}
+    for name in bound.input_names():
+        shape = bound.shapes[name]
+        if name == "Mask":
+            out[name] = causal_mask(*shape) if mask == "causal" else np.zeros(shape, np.float32)
+            rng.standard_normal(shape)  # keep the stream aligned with conftest
+            continue
+        x = rng.standard_normal(shape) * scales.get(name, 1.0)
+        out[name] = round_bf16(x)
+    return out
+
+
+CASES = [
+    # name, program, binding, seeds exported, io, extra
+    dict(name="attn256", prog="attention", bind=dict(N=256, M=256, D=64), seeds="all", io=True),
+    dict(name="bert512", prog="scaled_0p125", bind=dict(N=512, M=512, D=64), seeds=[0, 1], io=True),
+    dict(name="causal512", prog="llama_causal", bind=dict(N=512, M=512, D=128), seeds=[0, 1], io=True,
+         mask="causal"),
+    dict(name="llama2k", prog="llama", bind=dict(N=2048, M=2048, D=128), seeds=[0], io=False),
+    dict(name="causal2k", prog="llama_causal", bind=dict(N=2048, M=2048, D=128), seeds=[0], io=False),
+    dict(name="causal8k", prog="llama_causal", bind=dict(N=8192, M=8192, D=128), seeds=[0], io=False),
+    dict(name="causal16k", prog="llama_causal", bind=dict(N=16384, M=16384, D=128), seeds=[0], io=False),
+    dict(name="decode4", prog="llama", bind=dict(N=4, M=2048, D=128), seeds=[0], io=True),
+    dict(name="decode1", prog="llama", bind=dict(N=1, M=1024, D=128), seeds=[0], io=True),
+    dict(name="decode4_32k", prog="llama", bind=dict(N=4, M=32768, D=128), seeds=[0], io=False),
+    dict(name="gemm_v6", prog="gemm2", bind=dict(N=256, K=256, F=512, E=128), seeds=[0], io=True,
+         scales={"W1": 1 / 16.0, "W2": 1 / math.sqrt(512)}),
+    dict(name="gemm_v5", prog="gemm2", bind=dict(N=128, K=1024, F=256, E=128), seeds=[0], io=True,
+         scales={"W1": 1 / 32.0, "W2": 1 / math.sqrt(512)}),
+    dict(name="gemm4k_e128", prog="gemm2", bind=dict(N=4096, K=4096, F=4096, E=128), seeds=[0], io=False),
+    dict(name="gemm4k_e4096", prog="gemm2", bind=dict(N=4096, K=4096, F=4096, E=4096), seeds=[0],
+         io=False, device=dict(max_tile_elems=1000000)),
+    # tile-assignment variants of the config-1 kernel (same structure, other tiles)
+    dict(name="attn256_t128x128", prog="attention", bind=dict(N=256, M=256, D=64), seeds=[0], io=True,
+         assign=dict(t0_i=128, t0_j=128)),
+    dict(name="attn256_t32x64", prog="attention", bind=dict(N=256, M=256, D=64), seeds=[0], io=True,
+         assign=dict(t0_i=32, t0_j=64)),
+    dict(name="causal512_t128x64", prog="llama_causal", bind=dict(N=512, M=512, D=128), seeds=[0],
+         io=True, mask="causal", assign=dict(t0_i=128, t0_j=64)),
+]
+
+
+def main():
+    manifest = {}
+    for case in CASES:
+        name = case["name"]
+        src = PROGRAMS[case["prog"]]
+        device = DEFAULT_DEVICE
+        if case.get("device"):
+            device = replace(DEFAULT_DEVICE, **case["device"])
+        bound, base = frontend(src, case["bind"])
+        seeds = run_autoscheduler(base, device, SchedulerOptions())
+        which = range(len(seeds)) if case["seeds"] == "all" else case["seeds"]
+        entry = {"program": case["prog"], "binding": case["bind"], "n_seeds": len(seeds),
+                 "seeds": list(which), "assignment": case.get("assign"),
+                 "device": case.get("device"), "io": case["io"], "mask": case.get("mask")}
+        for k in which:
+            sd = seeds[k]
+            assignment = None
+            if case.get("assign"):
+                assignment = {t.name: t.default for t in sd.schedule.tunables}
+                assignment.update(case["assign"])
+            lw = lower_seed(base, sd.schedule, device, assignment)
+            stem = os.path.join(HERE, f"{name}.seed{k}")
+            mod = ma_ir.from_tilecc(lw.ma)
+            write(stem + ".ma.json", ma_ir.to_json(mod) + "\n")
+            write(stem + ".ma.txt", emit_tile_text(lw.ma))
+            write(stem + ".schedule.jsonl", serialize_schedule(sd.schedule))
+            write(stem + ".cost.json", lw.static_cost.to_json())
+            if case["io"] and k == list(which)[0]:
+                inputs = make_inputs(bound, 0, case.get("scales", {}), case.get("mask"))
+                outs, rep = interpret_ma(lw.ma, inputs, device, "fp32")
+                ref64 = oracle_eval(bound, inputs, "fp64")
+                arrays = {}
+                for n, v in inputs.items():
+                    if n == "Mask":
+                        continue
+                    arrays["in_" + n] = bf16_bits(v)
+                arrays["interp_fp32"] = np.asarray(outs[lw.ma.output], dtype=np.float32)
+                arrays["oracle_fp64"] = np.asarray(ref64[lw.ma.output], dtype=np.float64)
+                np.savez_compressed(stem + ".io.npz", **arrays)
+                write(stem + ".interp_cost.json", rep.to_json())
+        manifest[name] = entry
+        print(name, "seeds", len(seeds), "exported", list(which))
+    write(os.path.join(HERE, "manifest.json"), json.dumps(manifest, indent=1, sort_keys=True) + "\n")
+
+
+if __name__ == "__main__":
+    main()
