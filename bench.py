@@ -1,0 +1,478 @@
+#!/usr/bin/env python
+"""Benchmark: Nautilus-discovered fused attention on B200 (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config NAME] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU, NCCL)
+
+Default workload (the one BASELINE.json's metric/target is quoted on):
+Llama-3-8B GQA causal prefill, bf16, B=1, Hq=32, Hkv=8, D=128, seq 8192, the
+MA kernel the reference auto-scheduler discovers for SURVEY.md Appendix A.3
+(seed 0, default tiles), executed by the sm_100a K1 kernel over the runtime's
+batch x head outer grid.  A "step" is one pass of the hot path over that batch.
+
+Timing: W untimed warm-up steps, then K steps each bracketed by CUDA events on
+the launching stream, with a >L2 (256 MiB) write between steps to flush L2;
+barrier + synchronize on both sides; max over ranks.  Multi-GPU: (batch,
+kv-head) groups are sharded across ranks (no data-path collective) and O is
+all-gathered with NCCL inside the step.
+
+Extra keys: e2e (same metric through the public API execute_ma with pinned
+host inputs, H2D + kernel + D2H in the timed region), roofline (dominant
+kernel vs MEASURED_PEAKS.json), cpu_baseline (the reference CPU executor on a
+bounded sample), clocks (nvidia-smi during the timed region), gpu_launches.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+REF_PATH = os.path.join(REPO, "baseline", "_ref")
+
+LLAMA_SCALE = 0.08838834764831845
+
+CONFIGS = {
+    # name: workload (MA program + runtime outer grid)
+    "llama8k_causal": dict(prog="llama_causal", B=1, Hq=32, Hkv=8, N=8192, D=128, causal=True,
+                           golden="causal8k", scale=LLAMA_SCALE),
+    "llama2k_causal": dict(prog="llama_causal", B=1, Hq=32, Hkv=8, N=2048, D=128, causal=True,
+                           golden="causal2k", scale=LLAMA_SCALE),
+    "llama16k_causal": dict(prog="llama_causal", B=1, Hq=32, Hkv=8, N=16384, D=128, causal=True,
+                            golden="causal16k", scale=LLAMA_SCALE),
+    "bert512": dict(prog="scaled_0p125", B=32, Hq=12, Hkv=12, N=512, D=64, causal=False,
+                    golden="bert512", scale=0.125),
+    "attn256": dict(prog="attention", B=1, Hq=1, Hkv=1, N=256, D=64, causal=False,
+                    golden="attn256", scale=None),
+}
+DEFAULT_CONFIG = "llama8k_causal"
+
+
+def load_peaks():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0}, "fallback"
+
+
+def load_ma(cfg):
+    """The MA module: the committed reference export, else the reference pipeline live."""
+    from paper_2604_14825_b200 import ma_ir
+
+    p = os.path.join(REPO, "tests", "golden", f"{cfg['golden']}.seed0.ma.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return ma_ir.from_json(f.read()), "tests/golden/" + os.path.basename(p)
+    sys.path.insert(0, REF_PATH)
+    from paper_2604_14825_b200.frontdoor import compile_program
+    return compile_program(cfg["prog"], dict(N=cfg["N"], M=cfg["N"], D=cfg["D"]))[0], "tilecc (live)"
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = f"/tmp/nt_clocks_{os.getpid()}.csv"
+
+    def __enter__(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self):
+        if self.proc is None or not os.path.exists(self.path):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    rows.append((float(parts[1]), float(parts[2]), parts[4:9]))
+                except ValueError:
+                    continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for _, _, r in rows:
+            for n, v in zip(names, r[1:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        sm = [r[0] for r in rows]
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------- CPU baseline
+def _sliced_module(ma, nblocks):
+    import dataclasses
+    k = ma.kernels[0]
+    v, ax, _ = k.blocks[0]
+    return dataclasses.replace(ma, kernels=(dataclasses.replace(k, blocks=((v, ax, nblocks),)),))
+
+
+def _cpu_inputs(cfg):
+    import numpy as np
+    rng = np.random.default_rng(0)
+    N, D = cfg["N"], cfg["D"]
+    inp = {n: rng.standard_normal((N, D)).astype(np.float32) for n in ("Q", "K", "V")}
+    if cfg["causal"]:
+        i = np.arange(N)
+        inp["Mask"] = np.where(i[None, :] <= i[:, None], np.float32(0), np.float32(-np.inf)).astype(np.float32)
+    return inp
+
+
+_POOL_STATE = {}
+
+
+def _port_worker(nblocks):
+    from oracle import ma_interp
+    t = time.perf_counter()
+    ma_interp.interpret_ma(_sliced_module(_POOL_STATE["ma"], nblocks), _POOL_STATE["inp"], account=True)
+    return time.perf_counter() - t
+
+
+def _ref_worker(nblocks):
+    from tilecc.ma.device import DEFAULT_DEVICE
+    from tilecc.ma.interp import interpret_ma
+    ma, inp = _POOL_STATE["ma"], _POOL_STATE["inp"]
+    t = time.perf_counter()
+    interpret_ma(_sliced_module(ma, nblocks), inp, DEFAULT_DEVICE, "fp32")
+    return time.perf_counter() - t
+
+
+def reference_module(cfg):
+    """Reference MA via the reference's own pipeline (baseline/_ref), or None."""
+    if REF_PATH not in sys.path:
+        sys.path.insert(0, REF_PATH)
+    try:
+        from tilecc.autosched.scheduler import SchedulerOptions, run_autoscheduler
+        from tilecc.ma.device import DEFAULT_DEVICE
+        from tilecc.pipeline import frontend, lower_seed
+        from paper_2604_14825_b200.programs import PROGRAMS
+    except Exception:
+        return None
+    bound, base = frontend(PROGRAMS[cfg["prog"]], dict(N=cfg["N"], M=cfg["N"], D=cfg["D"]))
+    seeds = run_autoscheduler(base, DEFAULT_DEVICE, SchedulerOptions())
+    return lower_seed(base, seeds[0].schedule, DEFAULT_DEVICE).ma
+
+
+def cpu_baseline_sample(cfg, full_flops, target_s=10.0):
+    """Time the reference CPU executor (or the oracle port) on a bounded sample, 1 core."""
+    ma = reference_module(cfg)
+    inp = _cpu_inputs(cfg)
+    total_blocks_per_slice = None
+    if ma is not None:
+        from tilecc.ma.device import DEFAULT_DEVICE
+        from tilecc.ma.interp import interpret_ma
+        kind = "reference"
+        total_blocks_per_slice = ma.kernels[0].blocks[0][2]
+        run = lambda nb: interpret_ma(_sliced_module(ma, nb), inp, DEFAULT_DEVICE, "fp32")
+    else:
+        from oracle import ma_interp
+        from paper_2604_14825_b200 import ma_ir
+        mod, _ = load_ma(cfg)
+        kind = "port"
+        total_blocks_per_slice = mod.kernels[0].blocks[0][2]
+        run = lambda nb: ma_interp.interpret_ma(_sliced_module(mod, nb), inp)
+    t = time.perf_counter()
+    run(1)
+    per_block = time.perf_counter() - t
+    nb = max(1, min(total_blocks_per_slice, int(target_s / max(per_block, 1e-3))))
+    t = time.perf_counter()
+    run(nb)
+    dt = time.perf_counter() - t
+    per_block = dt / nb
+    slices = cfg["B"] * cfg["Hq"]
+    total_s = per_block * total_blocks_per_slice * slices
+    return {"value": full_flops / total_s / 1e12, "unit": "TFLOP/s", "cores": 1, "kind": kind,
+            "sample": f"{nb} of {total_blocks_per_slice} MA blocks of one (b,h) slice "
+                      f"({dt:.1f} s), extrapolated x{total_blocks_per_slice * slices / nb:.0f} "
+                      f"to {slices} slices = {total_s:.0f} s on 1 core",
+            "seconds_full_workload": total_s}
+
+
+def run_reference_arm(args, cfg, rank, world):
+    """--impl reference: the reference's CPU tile executor on all host cores."""
+    import multiprocessing as mp
+    if rank != 0:
+        return
+    ma = reference_module(cfg)
+    flops = attention_flops(cfg)
+    if ma is None:
+        kind = "port"
+        mod, _ = load_ma(cfg)
+    else:
+        kind = "reference"
+    inp = _cpu_inputs(cfg)
+    cores = os.cpu_count() or 1
+    total_blocks = (ma.kernels[0].blocks[0][2] if ma is not None else mod.kernels[0].blocks[0][2])
+    _POOL_STATE["ma"] = ma if ma is not None else mod
+    _POOL_STATE["inp"] = inp
+    worker = _port_worker if kind == "port" else _ref_worker
+    ctx = mp.get_context("fork")
+    times = []
+    with ctx.Pool(cores) as pool:
+        for step in range(args.warmup + args.steps):
+            t = time.perf_counter()
+            pool.map(worker, [1] * cores)
+            dt = time.perf_counter() - t
+            if step >= args.warmup:
+                times.append(dt)
+    step_s = statistics.mean(times)
+    blocks_total = total_blocks * cfg["B"] * cfg["Hq"]
+    full_s = step_s * blocks_total / cores
+    value = flops / full_s / 1e12
+    out = {"metric": "fused-attention bf16 TFLOP/s (reference CPU tile executor)", "value": value,
+           "unit": "TFLOP/s", "impl": "reference", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+           "config": config_block(cfg, args),
+           "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": kind,
+                            "sample": f"each step: {cores} processes x 1 MA block of the "
+                                      f"{args.config} slice program; extrapolated to {blocks_total} blocks "
+                                      f"({full_s:.0f} s for the full workload)"},
+           "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def attention_flops(cfg):
+    B, Hq, N, D = cfg["B"], cfg["Hq"], cfg["N"], cfg["D"]
+    if cfg["causal"]:
+        return 2.0 * B * Hq * D * N * (N + 1)
+    return 4.0 * B * Hq * N * N * D
+
+
+def config_block(cfg, args):
+    world = args.gpus
+    return {"workload": args.config, "program": cfg["prog"], "batch": cfg["B"], "heads_q": cfg["Hq"],
+            "heads_kv": cfg["Hkv"], "seq_len": cfg["N"], "head_dim": cfg["D"], "causal": cfg["causal"],
+            "ma_tiles": None, "parallelism": f"batch x kv-head sharding over {world} GPU(s)",
+            "l2": "flushed between timed steps (256 MiB write)"}
+
+
+def shard(cfg, rank, world):
+    """(b0, b1, h0, h1) kv-group range of this rank: batch split if possible, else kv heads."""
+    B, Hkv = cfg["B"], cfg["Hkv"]
+    if world == 1:
+        return 0, B, 0, Hkv
+    if B % world == 0:
+        n = B // world
+        return rank * n, (rank + 1) * n, 0, Hkv
+    if Hkv % world == 0:
+        n = Hkv // world
+        return 0, B, rank * n, (rank + 1) * n
+    raise SystemExit(f"cannot shard B={B}, Hkv={Hkv} over {world} GPUs")
+
+
+def run_ours(args, cfg, rank, world, dist):
+    import torch
+    from paper_2604_14825_b200 import _lib, execute_ma
+    from paper_2604_14825_b200.recognize import recognize
+    from paper_2604_14825_b200.runtime import AttentionPlan
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    mod, ma_src = load_ma(cfg)
+    spec = recognize(mod)[0]
+    b0, b1, h0, h1 = shard(cfg, rank, world)
+    g = cfg["Hq"] // cfg["Hkv"]
+    Bl, Hkvl, Hql = b1 - b0, h1 - h0, (h1 - h0) * g
+    N, D = cfg["N"], cfg["D"]
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    q = torch.randn((Bl, Hql, N, D), generator=gen, device=dev).to(torch.bfloat16)
+    k = torch.randn((Bl, Hkvl, N, D), generator=gen, device=dev).to(torch.bfloat16)
+    v = torch.randn((Bl, Hkvl, N, D), generator=gen, device=dev).to(torch.bfloat16)
+    o = torch.empty((Bl, Hql, N, D), dtype=torch.bfloat16, device=dev)
+    mask_kind = "causal" if cfg["causal"] else "none"
+    plan = AttentionPlan(q, k, v, o, spec.scale, mask_kind)
+    full = torch.empty((world,) + tuple(o.shape), dtype=o.dtype, device=dev) if world > 1 else None
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        plan.launch(stream)
+        if world > 1:
+            dist.all_gather_into_tensor(full, o)
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    plan.check_errors()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = _lib.launch_count()
+    with ClockSampler(dev.index if rank == 0 else dev.index) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            ev[i][0].record(stream)
+            plan.launch(stream)
+            ev[i][1].record(stream)
+            if world > 1:
+                dist.all_gather_into_tensor(full, o)
+            ev[i][2].record(stream)
+        torch.cuda.synchronize()
+    launches = _lib.launch_count() - l0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    kern_ms = [a.elapsed_time(b) for a, b, _ in ev]
+    step_ms = [a.elapsed_time(c) for a, _, c in ev]
+    ms_kernel = statistics.mean(kern_ms)
+    ms_step = statistics.mean(step_ms)
+    if world > 1:
+        t = torch.tensor([ms_step, ms_kernel], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step, ms_kernel = float(t[0]), float(t[1])
+    total_flops = attention_flops(cfg)
+    value = total_flops / (ms_step * 1e-3) / 1e12
+    local_flops = plan.flops()
+    achieved = local_flops / (statistics.mean(kern_ms) * 1e-3) / 1e12
+    peaks, peak_src = load_peaks()
+    clocks = clk.summary()
+
+    # ---------------- e2e through the public API (pinned host in, host out)
+    e2e = None
+    if rank == 0 or True:
+        hq_ = q.cpu().pin_memory()
+        hk_ = k.cpu().pin_memory()
+        hv_ = v.cpu().pin_memory()
+        inputs = {spec.q: hq_, spec.k: hk_, spec.v: hv_}
+        outer = (Bl, Hql, Hkvl)
+        host_out = torch.empty(tuple(o.shape), dtype=torch.bfloat16).pin_memory()
+
+        def e2e_step():
+            bufs, _ = execute_ma(mod, inputs, outer=outer, mask_kind=mask_kind, out_dtype="bf16",
+                                 return_torch=True, timing=False)
+            host_out.copy_(bufs[spec.o], non_blocking=True)
+
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        torch.cuda.synchronize()
+        e_ms = []
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            e2e_step()
+            e1.record(stream)
+            e1.synchronize()
+            e_ms.append(e0.elapsed_time(e1))
+        em = statistics.mean(e_ms)
+        if world > 1:
+            t = torch.tensor([em], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            em = float(t[0])
+        e2e = {"value": total_flops / (em * 1e-3) / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": int((q.numel() + k.numel() + v.numel()) * 2 * world),
+               "d2h_bytes_per_step": int(o.numel() * 2 * world), "ms_per_step": em,
+               "api": "paper_2604_14825_b200.execute_ma"}
+
+    if rank != 0:
+        return
+    traffic = None
+    prof = os.path.join(REPO, "profiles", "attn_fwd_ncu_summary.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                pj = json.load(f)
+            if pj.get("workload") == args.config:
+                traffic = pj.get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    peak = peaks["bf16_tflops"]
+    out = {
+        "metric": "fused-attention bf16 TFLOP/s & % tensor peak; box throughput at 1/2/4/8 GPUs",
+        "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic (torch.randn, seeded)",
+        "config": dict(config_block(cfg, args), ma_tiles=[spec.block_m, spec.block_n], ma_source=ma_src,
+                       kernel_ms=ms_kernel),
+        "pct_of_peak": {"measured_burst": value / peak, "measured_sustained": value / peaks.get(
+            "bf16_tflops_sustained", peak), "nominal_2250": value / 2250.0, "peak_source": peak_src},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "peak_source": f"MEASURED_PEAKS.json bf16_tflops (burst; {peak_src})",
+                     "kernel": "attn_fwd_kernel<128,causal>" if cfg["causal"] else "attn_fwd_kernel"},
+        "e2e": e2e,
+        "clocks": clocks,
+        "gpu_launches": launches,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            out["cpu_baseline"] = cpu_baseline_sample(cfg, total_flops, args.cpu_seconds)
+        except Exception as ex:  # pragma: no cover
+            out["cpu_baseline"] = {"value": None, "error": repr(ex)}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    args.gpus = world if world > 1 else args.gpus
+    if args.impl == "reference":
+        run_reference_arm(args, cfg, rank, world)
+        return
+    import torch
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    run_ours(args, cfg, rank, world, dist)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,133 @@
+/*
+ * nautilus_b200.h -- C ABI of the B200-native MA-tile executor.
+ *
+ * This is the drop-in boundary that replaces the reference's CPU tile
+ * executor.  The reference seam is the Python function
+ *
+ *   interpret_ma(module, inputs, device, precision) -> (buffers, CostReport)
+ *     /root/reference/pkg/src/tilecc/ma/interp.py:102-148
+ *   (wrapped by run_pipeline, tilecc/pipeline.py:62-64, and called by the
+ *    tuner's score, tilecc/tuner/tuner.py:139, and the CLI gates,
+ *    tilecc/cli.py:185,193,288)
+ *
+ * The host package paper_2604_14825_b200 recognises each MA kernel
+ * (tilecc/ma/ir.py:46-62) as one of the kernel families below and calls the
+ * matching entry point through ctypes.  All pointers are DEVICE pointers
+ * owned by the caller; `stream` is a cudaStream_t (NULL = legacy default
+ * stream).  Every entry point is asynchronous on `stream` and returns
+ * NT_OK or an error code; nt_last_error() gives a thread-local message.
+ * No torch types cross this boundary.
+ */
+#ifndef NAUTILUS_B200_H_
+#define NAUTILUS_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NT_ABI_VERSION 1
+
+/* status codes (mapped by the host onto tilecc.errors CompilerError subclasses) */
+#define NT_OK 0
+#define NT_ERR_INVALID 1     /* bad arguments (shape/stride/alignment)            */
+#define NT_ERR_UNSUPPORTED 2 /* no sm_100a realisation for this configuration    */
+#define NT_ERR_CUDA 3        /* CUDA runtime / driver error                        */
+
+#define NT_MASK_NONE 0
+#define NT_MASK_CAUSAL 1 /* Mask[i, j] = 0 if j <= i + causal_offset else -inf */
+#define NT_MASK_TENSOR 2 /* explicit fp32 Mask[seq_q, seq_kv] added to S*c    */
+
+#define NT_DTYPE_BF16 0
+#define NT_DTYPE_F32 1
+
+/* Rank-4 view [batch, heads, seq, dim]; dim is contiguous; strides in elements. */
+typedef struct nt_tensor4 {
+  void* ptr;
+  int64_t stride_b, stride_h, stride_s;
+} nt_tensor4;
+
+/*
+ * K1 fused attention forward -- realises the MA kernel the auto-scheduler
+ * discovers for softmax(Q (K c)^T [+ Mask]) V (SURVEY.md B.2 / Appendix C
+ * V0-V4), i.e. what interpret_ma executes over the block grid i0 with the
+ * sequential KV loop j0 (tilecc/ma/interp.py:121-127, 174-211).
+ * q/k/v are bf16; o is bf16 or fp32 (out_dtype).  GQA: head hq reads kv head
+ * hq / (heads_q / heads_kv).  The batch x head grid is the runtime outer grid.
+ */
+typedef struct nt_attn_args {
+  nt_tensor4 q, k, v, o;
+  int32_t batch, heads_q, heads_kv, seq_q, seq_kv, head_dim; /* head_dim 64 or 128 */
+  float scale;            /* c in S = Q (K c)^T (1.0 for the unscaled program) */
+  int32_t mask_kind;      /* NT_MASK_* */
+  int32_t causal_offset;  /* NT_MASK_CAUSAL: 0 = top-left (the MA fixture) */
+  const float* mask;      /* NT_MASK_TENSOR: fp32 [seq_q, seq_kv] */
+  int64_t mask_stride_row;
+  int32_t out_dtype; /* NT_DTYPE_BF16 | NT_DTYPE_F32 */
+  int32_t* err_flag; /* device int32 or NULL: bit0 = zero softmax denominator */
+} nt_attn_args;
+int nt_attn_fwd(const nt_attn_args* args, void* stream);
+
+/*
+ * K2 split-KV decode attention + combine (flash-decoding) for short query
+ * blocks (seq_q <= 16 rows per (batch, kv-head) group): the reference runs one
+ * block with a sequential KV loop; here the KV range is split
+ * over CTAs and partial (m, l, O) are merged with the repair law
+ * exp2(m_i - m) (tilecc/schedule/repair.py:80-88).  q/k/v bf16, o fp32/bf16.
+ * `workspace` must hold nt_decode_workspace_bytes(...) bytes of device memory.
+ */
+typedef struct nt_decode_args {
+  nt_tensor4 q, k, v, o;
+  int32_t batch, heads_q, heads_kv, seq_q, seq_kv, head_dim;
+  float scale;
+  int32_t num_splits; /* 0 = choose automatically */
+  int32_t out_dtype;
+  void* workspace;
+  int32_t* err_flag;
+} nt_decode_args;
+int64_t nt_decode_workspace_bytes(int32_t batch, int32_t heads_q, int32_t seq_q, int32_t head_dim,
+                                  int32_t num_splits);
+int nt_attn_decode(const nt_decode_args* args, void* stream);
+
+/*
+ * K3 GEMM (tcgen05, fp32 accumulate): C[M,N] = A[M,K] . B[K,N] with bf16 A, B
+ * (row-major, unit inner stride) and bf16 or fp32 C; optional fp32 C_in added
+ * (C = C_in + A.B) to realise the MA's `dot(..., acc=Y[...])`.
+ * Used twice for the GEMM chain (X.W1).W2 when the Y accumulator does not fit
+ * TMEM, and fused (nt_gemm_chain) when E <= 256.
+ */
+typedef struct nt_gemm_args {
+  const void* a; int64_t lda;   /* bf16 [M, K] */
+  const void* b; int64_t ldb;   /* bf16 [K, N] */
+  void* c; int64_t ldc;         /* out */
+  int32_t m, n, k;
+  int32_t out_dtype;            /* NT_DTYPE_BF16 | NT_DTYPE_F32 */
+} nt_gemm_args;
+int nt_gemm(const nt_gemm_args* args, void* stream);
+
+/* Fused chain Y = (X . W1) . W2 with the T tile kept on chip (E <= 256). */
+typedef struct nt_chain_args {
+  const void* x; int64_t ldx;   /* bf16 [N, K] */
+  const void* w1; int64_t ldw1; /* bf16 [K, F] */
+  const void* w2; int64_t ldw2; /* bf16 [F, E] */
+  void* y; int64_t ldy;         /* out [N, E] */
+  int32_t n, k, f, e;
+  int32_t out_dtype;
+} nt_chain_args;
+int nt_gemm_chain(const nt_chain_args* args, void* stream);
+
+/* dtype conversion helpers (device buffers) */
+int nt_cast_f32_to_bf16(const float* src, void* dst, int64_t n, void* stream);
+int nt_cast_bf16_to_f32(const void* src, float* dst, int64_t n, void* stream);
+
+/* introspection */
+int nt_abi_version(void);
+const char* nt_last_error(void);
+/* number of kernel launches issued by this library since load (for gpu_launches accounting) */
+int64_t nt_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NAUTILUS_B200_H_ */

@@ -1,0 +1,102 @@
+"""ctypes binding of the C ABI (include/nautilus_b200.h).
+
+The shared library is built in-tree by ``paper_2604_14825_b200.build``.  There
+is no fallback: if it is missing, every device entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+from .errors import NativeLibraryMissing, raise_for_status
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_native", "libnautilus_b200.so")
+
+NT_MASK_NONE, NT_MASK_CAUSAL, NT_MASK_TENSOR = 0, 1, 2
+NT_DTYPE_BF16, NT_DTYPE_F32 = 0, 1
+
+# Every symbol include/nautilus_b200.h declares (checked by tests/test_capi.py).
+EXPORTED = (
+    "nt_attn_fwd", "nt_attn_decode", "nt_decode_workspace_bytes", "nt_gemm", "nt_gemm_chain",
+    "nt_cast_f32_to_bf16", "nt_cast_bf16_to_f32", "nt_abi_version", "nt_last_error", "nt_launch_count",
+)
+
+
+class Tensor4(C.Structure):
+    _fields_ = [("ptr", C.c_void_p), ("stride_b", C.c_int64), ("stride_h", C.c_int64),
+                ("stride_s", C.c_int64)]
+
+
+class AttnArgs(C.Structure):
+    _fields_ = [("q", Tensor4), ("k", Tensor4), ("v", Tensor4), ("o", Tensor4),
+                ("batch", C.c_int32), ("heads_q", C.c_int32), ("heads_kv", C.c_int32),
+                ("seq_q", C.c_int32), ("seq_kv", C.c_int32), ("head_dim", C.c_int32),
+                ("scale", C.c_float), ("mask_kind", C.c_int32), ("causal_offset", C.c_int32),
+                ("mask", C.c_void_p), ("mask_stride_row", C.c_int64),
+                ("out_dtype", C.c_int32), ("err_flag", C.c_void_p)]
+
+
+class DecodeArgs(C.Structure):
+    _fields_ = [("q", Tensor4), ("k", Tensor4), ("v", Tensor4), ("o", Tensor4),
+                ("batch", C.c_int32), ("heads_q", C.c_int32), ("heads_kv", C.c_int32),
+                ("seq_q", C.c_int32), ("seq_kv", C.c_int32), ("head_dim", C.c_int32),
+                ("scale", C.c_float), ("num_splits", C.c_int32), ("out_dtype", C.c_int32),
+                ("workspace", C.c_void_p), ("err_flag", C.c_void_p)]
+
+
+class GemmArgs(C.Structure):
+    _fields_ = [("a", C.c_void_p), ("lda", C.c_int64), ("b", C.c_void_p), ("ldb", C.c_int64),
+                ("c", C.c_void_p), ("ldc", C.c_int64), ("m", C.c_int32), ("n", C.c_int32),
+                ("k", C.c_int32), ("out_dtype", C.c_int32)]
+
+
+class ChainArgs(C.Structure):
+    _fields_ = [("x", C.c_void_p), ("ldx", C.c_int64), ("w1", C.c_void_p), ("ldw1", C.c_int64),
+                ("w2", C.c_void_p), ("ldw2", C.c_int64), ("y", C.c_void_p), ("ldy", C.c_int64),
+                ("n", C.c_int32), ("k", C.c_int32), ("f", C.c_int32), ("e", C.c_int32),
+                ("out_dtype", C.c_int32)]
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib():
+    """Load (once) and return the native library; raise if it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise NativeLibraryMissing(
+                    f"{LIB_PATH} not built: run `python -m paper_2604_14825_b200.build` "
+                    "(there is no CPU fallback)")
+            L = C.CDLL(LIB_PATH)
+            L.nt_attn_fwd.argtypes = [C.POINTER(AttnArgs), C.c_void_p]
+            L.nt_attn_decode.argtypes = [C.POINTER(DecodeArgs), C.c_void_p]
+            L.nt_decode_workspace_bytes.argtypes = [C.c_int32] * 5
+            L.nt_decode_workspace_bytes.restype = C.c_int64
+            L.nt_gemm.argtypes = [C.POINTER(GemmArgs), C.c_void_p]
+            L.nt_gemm_chain.argtypes = [C.POINTER(ChainArgs), C.c_void_p]
+            L.nt_cast_f32_to_bf16.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
+            L.nt_cast_bf16_to_f32.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
+            L.nt_last_error.restype = C.c_char_p
+            L.nt_launch_count.restype = C.c_int64
+            for name in ("nt_attn_fwd", "nt_attn_decode", "nt_gemm", "nt_gemm_chain",
+                         "nt_cast_f32_to_bf16", "nt_cast_bf16_to_f32", "nt_abi_version"):
+                getattr(L, name).restype = C.c_int
+            _lib = L
+    return _lib
+
+
+def check(status: int, what: str) -> None:
+    if status != 0:
+        msg = lib().nt_last_error().decode(errors="replace")
+        raise_for_status(status, f"{what}: {msg}")
+
+
+def launch_count() -> int:
+    return int(lib().nt_launch_count())

@@ -1,0 +1,226 @@
+// C ABI entry points (include/nautilus_b200.h): argument validation, TMA
+// descriptor encoding, launch configuration.  Kernels live in *.cuh.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/nautilus_b200.h"
+#include "attn_fwd.cuh"
+#include "common_host.h"
+
+namespace nt {
+
+thread_local std::string g_last_error;
+std::atomic<int64_t> g_launches{0};
+
+int set_error(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) return set_error(NT_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return NT_OK;
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeFn get_encode() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+// rank-4 bf16 map over [B, H, S, D] (dims innermost-first), box {64, box_rows, 1, 1}, 128B swizzle
+int make_map_4d(CUtensorMap* m, const void* ptr, int64_t D, int64_t S, int64_t H, int64_t B, int64_t sS,
+                int64_t sH, int64_t sB, int box_rows, size_t elem) {
+  EncodeFn enc = get_encode();
+  if (!enc) return set_error(NT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if (reinterpret_cast<uintptr_t>(ptr) % 16) return set_error(NT_ERR_INVALID, "tensor base not 16B aligned");
+  cuuint64_t dims[4] = {(cuuint64_t)D, (cuuint64_t)S, (cuuint64_t)H, (cuuint64_t)B};
+  cuuint64_t strides[3] = {(cuuint64_t)(sS * elem), (cuuint64_t)(sH * elem), (cuuint64_t)(sB * elem)};
+  for (int i = 0; i < 3; ++i) {
+    if (strides[i] % 16) return set_error(NT_ERR_INVALID, "tensor strides must be multiples of 16 bytes");
+    if (strides[i] == 0) strides[i] = 16;  // broadcast dims of extent 1
+  }
+  cuuint32_t box[4] = {(cuuint32_t)(128 / elem), (cuuint32_t)box_rows, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(m, elem == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+                   const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(NT_ERR_INVALID, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return NT_OK;
+}
+
+int make_map_2d(CUtensorMap* m, const void* ptr, int64_t inner, int64_t outer, int64_t ld, int box_inner,
+                int box_outer, size_t elem, CUtensorMapSwizzle swz) {
+  EncodeFn enc = get_encode();
+  if (!enc) return set_error(NT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if (reinterpret_cast<uintptr_t>(ptr) % 16) return set_error(NT_ERR_INVALID, "matrix base not 16B aligned");
+  if ((ld * elem) % 16) return set_error(NT_ERR_INVALID, "leading dimension must be a multiple of 16 bytes");
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * elem)};
+  cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, elem == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                   const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(NT_ERR_INVALID, "cuTensorMapEncodeTiled(2d) failed (" + std::to_string((int)r) + ")");
+  return NT_OK;
+}
+
+// ----------------------------------------------------------------- attention
+template <int D, int MASK, bool F32>
+static int launch_attn(const nt_attn_args* a, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
+                       const CUtensorMap& mo, const AttnFwdParams& p, cudaStream_t st) {
+  auto kern = attn_fwd_kernel<D, MASK, F32>;
+  const int smem = AttnCfg<D>::SMEM_BYTES;
+  static bool configured = false;
+  if (!configured) {
+    int rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+                        "cudaFuncSetAttribute(attn_fwd)");
+    if (rc) return rc;
+    configured = true;
+  }
+  dim3 grid(p.n_mblocks * a->batch * a->heads_q);
+  kern<<<grid, kAttnThreads, smem, st>>>(mq, mk, mv, mo, p);
+  g_launches++;
+  return check_cuda(cudaGetLastError(), "attn_fwd launch");
+}
+
+template <int D>
+static int dispatch_attn(const nt_attn_args* a, const CUtensorMap& mq, const CUtensorMap& mk,
+                         const CUtensorMap& mv, const CUtensorMap& mo, const AttnFwdParams& p, cudaStream_t st) {
+  const bool f32 = a->out_dtype == NT_DTYPE_F32;
+  switch (a->mask_kind) {
+    case NT_MASK_NONE:
+      return f32 ? launch_attn<D, MASK_NONE, true>(a, mq, mk, mv, mo, p, st)
+                 : launch_attn<D, MASK_NONE, false>(a, mq, mk, mv, mo, p, st);
+    case NT_MASK_CAUSAL:
+      return f32 ? launch_attn<D, MASK_CAUSAL, true>(a, mq, mk, mv, mo, p, st)
+                 : launch_attn<D, MASK_CAUSAL, false>(a, mq, mk, mv, mo, p, st);
+    case NT_MASK_TENSOR:
+      return f32 ? launch_attn<D, MASK_TENSOR, true>(a, mq, mk, mv, mo, p, st)
+                 : launch_attn<D, MASK_TENSOR, false>(a, mq, mk, mv, mo, p, st);
+  }
+  return set_error(NT_ERR_INVALID, "unknown mask_kind");
+}
+
+}  // namespace nt
+
+using namespace nt;
+
+extern "C" int nt_attn_fwd(const nt_attn_args* a, void* stream) {
+  if (!a) return set_error(NT_ERR_INVALID, "null args");
+  if (a->head_dim != 64 && a->head_dim != 128)
+    return set_error(NT_ERR_UNSUPPORTED, "head_dim must be 64 or 128");
+  if (a->batch <= 0 || a->heads_q <= 0 || a->heads_kv <= 0 || a->seq_q <= 0 || a->seq_kv <= 0)
+    return set_error(NT_ERR_INVALID, "non-positive extent");
+  if (a->heads_q % a->heads_kv) return set_error(NT_ERR_INVALID, "heads_q must be a multiple of heads_kv");
+  if (!(a->scale > 0.f)) return set_error(NT_ERR_UNSUPPORTED, "scale must be positive");
+  if (a->mask_kind == NT_MASK_TENSOR && !a->mask) return set_error(NT_ERR_INVALID, "tensor mask missing");
+  const int D = a->head_dim;
+  CUtensorMap mq, mk, mv, mo;
+  int rc;
+  if ((rc = make_map_4d(&mq, a->q.ptr, D, a->seq_q, a->heads_q, a->batch, a->q.stride_s, a->q.stride_h,
+                        a->q.stride_b, 128, 2)))
+    return rc;
+  if ((rc = make_map_4d(&mk, a->k.ptr, D, a->seq_kv, a->heads_kv, a->batch, a->k.stride_s, a->k.stride_h,
+                        a->k.stride_b, 128, 2)))
+    return rc;
+  if ((rc = make_map_4d(&mv, a->v.ptr, D, a->seq_kv, a->heads_kv, a->batch, a->v.stride_s, a->v.stride_h,
+                        a->v.stride_b, 128, 2)))
+    return rc;
+  if (a->out_dtype == NT_DTYPE_BF16) {
+    if ((rc = make_map_4d(&mo, a->o.ptr, D, a->seq_q, a->heads_q, a->batch, a->o.stride_s, a->o.stride_h,
+                          a->o.stride_b, 128, 2)))
+      return rc;
+  } else {
+    memset(&mo, 0, sizeof(mo));
+    if (reinterpret_cast<uintptr_t>(a->o.ptr) % 16 || a->o.stride_s % 4)
+      return set_error(NT_ERR_INVALID, "fp32 output must be 16B aligned with row stride % 4 == 0");
+  }
+  AttnFwdParams p{};
+  p.B = a->batch;
+  p.Hq = a->heads_q;
+  p.Hkv = a->heads_kv;
+  p.N = a->seq_q;
+  p.M = a->seq_kv;
+  p.q_per_kv = a->heads_q / a->heads_kv;
+  p.n_mblocks = (a->seq_q + 255) / 256;
+  p.n_kv_total = (a->seq_kv + 127) / 128;
+  p.causal_offset = a->causal_offset;
+  p.scale_log2 = a->scale * 1.4426950408889634f;
+  p.mask = a->mask;
+  p.mask_row_stride = a->mask_stride_row;
+  p.o_f32 = static_cast<float*>(a->o.ptr);
+  p.o_sb = a->o.stride_b;
+  p.o_sh = a->o.stride_h;
+  p.o_sn = a->o.stride_s;
+  p.err = a->err_flag;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  return D == 64 ? dispatch_attn<64>(a, mq, mk, mv, mo, p, st) : dispatch_attn<128>(a, mq, mk, mv, mo, p, st);
+}
+
+// ----------------------------------------------------------------- casts
+__global__ void cast_f32_bf16_kernel(const float4* __restrict__ src, uint2* __restrict__ dst, int64_t n4) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 v = src[i];
+    dst[i] = make_uint2(pack_bf16(v.x, v.y), pack_bf16(v.z, v.w));
+  }
+}
+__global__ void cast_f32_bf16_tail(const float* src, __nv_bfloat16* dst, int64_t lo, int64_t n) {
+  int64_t i = lo + threadIdx.x;
+  if (i < n) dst[i] = __float2bfloat16_rn(src[i]);
+}
+__global__ void cast_bf16_f32_kernel(const __nv_bfloat16* __restrict__ src, float* __restrict__ dst, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = __bfloat162float(src[i]);
+}
+
+extern "C" int nt_cast_f32_to_bf16(const float* src, void* dst, int64_t n, void* stream) {
+  if (n <= 0) return NT_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool aligned = (reinterpret_cast<uintptr_t>(src) % 16 == 0) && (reinterpret_cast<uintptr_t>(dst) % 8 == 0);
+  int64_t n4 = aligned ? n / 4 : 0;
+  if (n4) {
+    int blocks = (int)std::min<int64_t>((n4 + 255) / 256, 148 * 16);
+    cast_f32_bf16_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(src), static_cast<uint2*>(dst), n4);
+    g_launches++;
+  }
+  int64_t lo = n4 * 4;
+  while (lo < n) {
+    cast_f32_bf16_tail<<<1, 256, 0, st>>>(src, static_cast<__nv_bfloat16*>(dst), lo, n);
+    g_launches++;
+    lo += 256;
+  }
+  return check_cuda(cudaGetLastError(), "cast_f32_bf16");
+}
+
+extern "C" int nt_cast_bf16_to_f32(const void* src, float* dst, int64_t n, void* stream) {
+  if (n <= 0) return NT_OK;
+  int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  cast_bf16_f32_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const __nv_bfloat16*>(src), dst, n);
+  g_launches++;
+  return check_cuda(cudaGetLastError(), "cast_bf16_f32");
+}
+
+extern "C" int nt_abi_version(void) { return NT_ABI_VERSION; }
+extern "C" const char* nt_last_error(void) { return g_last_error.c_str(); }
+extern "C" int64_t nt_launch_count(void) { return g_launches.load(); }

@@ -1,0 +1,233 @@
+"""``execute_ma``: the device replacement of the reference CPU tile executor.
+
+Reference seam:
+    interpret_ma(module, inputs, device, precision=None) -> (buffers, CostReport)
+    tilecc/ma/interp.py:102-148, wrapped by run_pipeline (tilecc/pipeline.py:62-64)
+
+``execute_ma`` keeps that positional signature and return shape:
+
+* ``module`` -- a tilecc ``MAModule``, a mirrored ``ma_ir.Module`` or its JSON;
+* ``inputs`` -- ``{name: array}`` with the MA buffer shapes (numpy or torch,
+  CPU or CUDA).  With ``outer=(B, Hq, Hkv)`` (or rank-4 inputs) the runtime
+  adds the batch x head (x GQA) outer grid the reference cannot express;
+* ``device`` -- accepted for signature compatibility (a VirtualDevice or
+  ``B200Profile``); the hardware is the device;
+* ``precision`` -- "fp32" (the MA precision; realised as bf16 operands with
+  fp32 accumulation) -- fp64/rational have no device realisation and raise.
+
+It returns ``(buffers, ExecReport)`` where ``buffers`` maps every Global
+buffer name to an array (inputs as given, the output computed on the GPU) --
+callers index ``[module.output]`` exactly as they do for interpret_ma
+(tilecc/cli.py:186, 194, 289) -- and ``ExecReport`` carries the static
+counters of the reference cost model plus the measured device time.
+
+Errors: shape mismatches raise ``OutOfBounds`` (interp.py:111-112), a zero
+softmax denominator raises ``DivisionByZero`` (numerics.py:123-126), an
+unrecognised MA raises ``UnsupportedMA``.  There is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib, cost
+from . import ma_ir as ir
+from .errors import DivisionByZero, OutOfBounds, UnsupportedMA
+from .recognize import AttentionSpec, GemmChainSpec, recognize
+from .runtime import AttentionPlan
+
+
+@dataclass
+class ExecReport:
+    """Device execution report (mirrors tilecc CostReport fields + timing)."""
+
+    bytes_global: int = 0
+    bytes_shared: int = 0
+    bytes_register: int = 0
+    flops: int = 0
+    kernels: int = 0
+    steps: int = 0
+    modeled_cost: float = 0.0
+    device_ms: float = 0.0
+    algorithmic_flops: float = 0.0
+    tflops: float = 0.0
+    launches: int = 0
+    specs: list = field(default_factory=list)
+    realisation: list = field(default_factory=list)
+
+
+def _to_device(x, dev, name) -> torch.Tensor:
+    if isinstance(x, torch.Tensor):
+        return x.to(dev, non_blocking=True) if x.device != dev else x
+    arr = np.ascontiguousarray(np.asarray(x, dtype=np.float32))
+    return torch.from_numpy(arr).pin_memory().to(dev, non_blocking=True)
+
+
+def to_bf16(t: torch.Tensor, stream=None) -> torch.Tensor:
+    """fp32 CUDA tensor -> bf16 (round to nearest even) with the library's cast kernel."""
+    if t.dtype == torch.bfloat16:
+        return t
+    if t.dtype != torch.float32:
+        t = t.float()
+    t = t.contiguous()
+    out = torch.empty(t.shape, dtype=torch.bfloat16, device=t.device)
+    st = torch.cuda.current_stream().cuda_stream if stream is None else stream
+    _lib.check(_lib.lib().nt_cast_f32_to_bf16(t.data_ptr(), out.data_ptr(), t.numel(), st),
+               "nt_cast_f32_to_bf16")
+    return out
+
+
+def _is_causal_mask(mask, n, m, offset=0) -> bool:
+    """True iff Mask[i, j] == 0 for j <= i + offset and -inf otherwise."""
+    if isinstance(mask, torch.Tensor):
+        i = torch.arange(n, device=mask.device)[:, None]
+        j = torch.arange(m, device=mask.device)[None, :]
+        keep = j <= i + offset
+        mk = mask.reshape(n, m)
+        return bool(torch.all(torch.where(keep, mk == 0, torch.isneginf(mk))).item())
+    mk = np.asarray(mask).reshape(n, m)
+    keep = np.arange(m)[None, :] <= np.arange(n)[:, None] + offset
+    return bool(np.all(np.where(keep, mk == 0, np.isneginf(mk))))
+
+
+def _shape_check(name, x, shape, outer):
+    got = tuple(x.shape)
+    if outer is None:
+        if got != tuple(shape):
+            raise OutOfBounds(f"input {name!r}: wrong shape {got}")
+    elif got[-2:] != tuple(shape):
+        raise OutOfBounds(f"input {name!r}: wrong shape {got} (trailing dims must be {tuple(shape)})")
+
+
+def _prepare_attention(spec: AttentionSpec, module: ir.Module, inputs: dict, outer, mask_kind, out_dtype,
+                       dev):
+    q_in, k_in, v_in = inputs[spec.q], inputs[spec.k], inputs[spec.v]
+    if outer is None and getattr(q_in, "ndim", 2) == 4:
+        outer = (q_in.shape[0], q_in.shape[1], k_in.shape[1])
+    for nm, x, shp in ((spec.q, q_in, (spec.n, spec.d)), (spec.k, k_in, (spec.m, spec.d)),
+                       (spec.v, v_in, (spec.m, spec.dv))):
+        _shape_check(nm, x, shp, outer)
+    q = to_bf16(_to_device(q_in, dev, spec.q))
+    k = to_bf16(_to_device(k_in, dev, spec.k))
+    v = to_bf16(_to_device(v_in, dev, spec.v))
+    if outer is not None:
+        B, Hq, Hkv = outer
+        q = q.reshape(B, Hq, spec.n, spec.d)
+        k = k.reshape(B, Hkv, spec.m, spec.d)
+        v = v.reshape(B, Hkv, spec.m, spec.dv)
+    else:
+        B, Hq = 1, 1
+    kind = "none"
+    mask_t = None
+    if spec.mask is not None and spec.mask not in inputs and mask_kind == "causal":
+        kind = "causal"  # caller asserts the structured causal mask; no tensor needed
+    elif spec.mask is not None:
+        mk = inputs[spec.mask]
+        _shape_check(spec.mask, mk, (spec.n, spec.m), None)
+        if mask_kind in (None, "auto"):
+            kind = "causal" if _is_causal_mask(mk, spec.n, spec.m) else "tensor"
+        else:
+            kind = mask_kind
+        if kind == "tensor":
+            mask_t = _to_device(mk, dev, spec.mask).float().contiguous()
+    elif mask_kind not in (None, "auto", "none"):
+        kind = mask_kind  # caller asserts a structured mask on an unmasked program
+    odt = torch.float32 if out_dtype in (None, "fp32", torch.float32) else torch.bfloat16
+    o = torch.empty((B, Hq, spec.n, spec.dv), dtype=odt, device=dev)
+    plan = AttentionPlan(q, k, v, o, spec.scale, kind, mask_t)
+    return plan, o, outer
+
+
+_SPEC_CACHE: dict = {}
+_COST_CACHE: dict = {}
+
+
+def _static_cached(obj, mod):
+    hit = _COST_CACHE.get(id(obj))
+    if hit is not None and hit[0] is obj:
+        return hit[1]
+    st = cost.cost_model(mod)
+    if len(_COST_CACHE) > 256:
+        _COST_CACHE.clear()
+    _COST_CACHE[id(obj)] = (obj, st)
+    return st
+
+
+def _recognize_cached(obj, mod):
+    key = id(obj)
+    hit = _SPEC_CACHE.get(key)
+    if hit is not None and hit[0] is obj:
+        return hit[1]
+    specs = recognize(mod)
+    if len(_SPEC_CACHE) > 256:
+        _SPEC_CACHE.clear()
+    _SPEC_CACHE[key] = (obj, specs)
+    return specs
+
+
+def execute_ma(module, inputs: dict, device=None, precision=None, *, outer=None, mask_kind=None,
+               out_dtype=None, stream=None, timing: bool = True, return_torch: bool = False):
+    """Run an MA module on the B200 (see module docstring)."""
+    mod = ir.as_module(module)
+    prec = precision if precision is None or isinstance(precision, str) else getattr(precision, "value", precision)
+    if prec not in (None, "fp32"):
+        raise UnsupportedMA(f"precision {prec!r} has no device realisation")
+    if not torch.cuda.is_available():
+        raise UnsupportedMA("no CUDA device: the B200 executor has no CPU fallback")
+    specs = _recognize_cached(module, mod)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    report = ExecReport(kernels=len(mod.kernels))
+    static = _static_cached(module, mod)
+    for f in ("bytes_global", "bytes_shared", "bytes_register", "flops", "steps", "modeled_cost"):
+        setattr(report, f, getattr(static, f))
+    outputs: dict = {}
+    l0 = _lib.launch_count()
+    for spec in specs:
+        report.specs.append(spec)
+        if isinstance(spec, AttentionSpec):
+            plan, o, outer_used = _prepare_attention(spec, mod, inputs, outer, mask_kind, out_dtype, dev)
+            report.realisation.append({"kernel": "attn_fwd", "mask": plan.mask_kind,
+                                       "grid_ctas": -(-spec.n // 256) * o.shape[0] * o.shape[1],
+                                       "gpu_tile": (256, 128), "ma_tile": (spec.block_m, spec.block_n)})
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record()
+            plan.launch(stream)
+            ev1.record()
+            ev1.synchronize()
+            plan.check_errors()
+            report.device_ms += ev0.elapsed_time(ev1)
+            report.algorithmic_flops += plan.flops()
+            res = o if outer_used is not None else o[0, 0]
+            outputs[spec.o] = res
+        elif isinstance(spec, GemmChainSpec):
+            from .gemm import run_gemm_chain
+            y, ms, fl, info = run_gemm_chain(spec, inputs, dev, out_dtype)
+            report.realisation.append(info)
+            report.device_ms += ms
+            report.algorithmic_flops += fl
+            outputs[spec.y] = y
+        else:  # pragma: no cover
+            raise UnsupportedMA(f"no launcher for {type(spec).__name__}")
+    report.launches = _lib.launch_count() - l0
+    if report.device_ms > 0:
+        report.tflops = report.algorithmic_flops / (report.device_ms * 1e-3) / 1e12
+    bufs: dict = {}
+    for b in mod.buffers:
+        if b.scope != "Global":
+            continue
+        if b.name in outputs:
+            val = outputs[b.name]
+            bufs[b.name] = val if return_torch else val.float().cpu().numpy()
+        elif b.is_input:
+            bufs[b.name] = inputs[b.name]
+    return bufs, report
+
+
+def run_pipeline(ma, inputs: dict, device=None, precision=None):
+    """Drop-in for tilecc.pipeline.run_pipeline (tilecc/pipeline.py:62-64)."""
+    return execute_ma(ma, inputs, device, precision)

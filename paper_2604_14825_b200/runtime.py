@@ -1,0 +1,108 @@
+"""Launch plans: a recognised KernelSpec bound to device tensors.
+
+A plan owns the ctypes argument struct for one launch of a C-ABI entry point
+(include/nautilus_b200.h) so that hot loops (bench, tuner timing) pay only the
+foreign call.  torch is used purely as the device-memory / stream provider.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from typing import Optional
+
+import torch
+
+from . import _lib
+from .errors import DivisionByZero, InvalidArguments, UnsupportedMA
+from .recognize import AttentionSpec, GemmChainSpec
+
+
+def _stream_handle(stream) -> int:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def _as4(t: torch.Tensor) -> torch.Tensor:
+    if t.dim() == 2:
+        return t.unsqueeze(0).unsqueeze(0)
+    if t.dim() == 3:
+        return t.unsqueeze(0)
+    if t.dim() != 4:
+        raise InvalidArguments(f"expected a rank-2/3/4 tensor, got shape {tuple(t.shape)}")
+    return t
+
+
+def _t4(t: torch.Tensor) -> _lib.Tensor4:
+    if t.stride(-1) != 1:
+        raise InvalidArguments("innermost (head) dimension must be contiguous")
+    return _lib.Tensor4(t.data_ptr(), t.stride(0), t.stride(1), t.stride(2))
+
+
+class AttentionPlan:
+    """K1 fused attention over a [B, H, N, D] outer grid (bf16 in, bf16/fp32 out)."""
+
+    def __init__(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor,
+                 scale: Optional[float], mask_kind: str = "none", mask: Optional[torch.Tensor] = None,
+                 causal_offset: int = 0, err_flag: Optional[torch.Tensor] = None):
+        q, k, v, o = _as4(q), _as4(k), _as4(v), _as4(o)
+        for name, t in (("q", q), ("k", k), ("v", v)):
+            if t.dtype != torch.bfloat16 or not t.is_cuda:
+                raise InvalidArguments(f"{name} must be a CUDA bf16 tensor")
+        if o.dtype not in (torch.bfloat16, torch.float32) or not o.is_cuda:
+            raise InvalidArguments("o must be a CUDA bf16/fp32 tensor")
+        B, Hq, N, D = q.shape
+        Bk, Hkv, M, Dk = k.shape
+        if Bk != B or Dk != D or tuple(v.shape) != (B, Hkv, M, D) or tuple(o.shape) != (B, Hq, N, D):
+            raise InvalidArguments("q/k/v/o shapes inconsistent")
+        self.q, self.k, self.v, self.o, self.mask = q, k, v, o, mask
+        self.err = err_flag if err_flag is not None else torch.zeros(1, dtype=torch.int32, device=q.device)
+        kind = {"none": _lib.NT_MASK_NONE, "causal": _lib.NT_MASK_CAUSAL, "tensor": _lib.NT_MASK_TENSOR}[mask_kind]
+        self.mask_kind = mask_kind
+        a = _lib.AttnArgs()
+        a.q, a.k, a.v, a.o = _t4(q), _t4(k), _t4(v), _t4(o)
+        a.batch, a.heads_q, a.heads_kv, a.seq_q, a.seq_kv, a.head_dim = B, Hq, Hkv, N, M, D
+        a.scale = 1.0 if scale is None else float(scale)
+        a.mask_kind = kind
+        a.causal_offset = int(causal_offset)
+        if kind == _lib.NT_MASK_TENSOR:
+            if mask is None or mask.dtype != torch.float32 or not mask.is_cuda or mask.stride(-1) != 1:
+                raise InvalidArguments("tensor mask must be a CUDA fp32 [N, M] tensor")
+            a.mask = mask.data_ptr()
+            a.mask_stride_row = mask.stride(0)
+        a.out_dtype = _lib.NT_DTYPE_F32 if o.dtype == torch.float32 else _lib.NT_DTYPE_BF16
+        a.err_flag = self.err.data_ptr()
+        self.args = a
+        self.shape = (B, Hq, Hkv, N, M, D)
+        self._fn = _lib.lib().nt_attn_fwd
+        self._ref = C.byref(a)
+
+    def launch(self, stream=None) -> None:
+        st = self._fn(self._ref, _stream_handle(stream))
+        if st:
+            _lib.check(st, "nt_attn_fwd")
+
+    def flops(self) -> float:
+        B, Hq, _, N, M, D = self.shape
+        if self.mask_kind == "causal":
+            # exact count of unmasked (i, j) pairs for top-left causal (j <= i + off)
+            off = int(self.args.causal_offset)
+            pairs = _causal_pairs(N, M, off)
+            return 4.0 * B * Hq * D * pairs
+        return 4.0 * B * Hq * N * M * D
+
+    def check_errors(self) -> None:
+        flag = int(self.err.item())
+        if flag & 1:
+            raise DivisionByZero("tile divide: softmax denominator is zero (row fully masked)")
+        if flag & 0x100:
+            raise RuntimeError(f"device pipeline timeout (code {flag & 0xff})")
+
+
+def _causal_pairs(N: int, M: int, off: int) -> int:
+    """sum_i clamp(i + off + 1, 0, M): unmasked (query, key) pairs of a causal mask."""
+    import numpy as np
+    return int(np.clip(np.arange(N, dtype=np.int64) + off + 1, 0, M).sum())

@@ -1,0 +1,124 @@
+"""MA -> KernelSpec recognition, index-math parity and static-cost parity (CPU)."""
+
+import json
+import os
+
+import pytest
+
+from conftest import GOLDEN, all_ma_files
+from paper_2604_14825_b200 import cost, ma_ir
+from paper_2604_14825_b200.errors import UnsupportedMA
+from paper_2604_14825_b200.recognize import AttentionSpec, GemmChainSpec, recognize
+
+
+def _load(fname):
+    with open(os.path.join(GOLDEN, fname)) as f:
+        return ma_ir.from_json(f.read())
+
+
+@pytest.mark.parametrize("fname", all_ma_files())
+def test_every_golden_kernel_is_recognised(fname):
+    mod = _load(fname)
+    specs = recognize(mod)
+    assert len(specs) == 1
+    spec = specs[0]
+    if fname.startswith("gemm"):
+        assert isinstance(spec, GemmChainSpec)
+        assert spec.n_blocks * spec.block_m == spec.n
+        assert spec.n_iters * spec.block_f == spec.f
+    else:
+        assert isinstance(spec, AttentionSpec)
+        assert spec.n_blocks * spec.block_m == spec.n
+        assert spec.n_iters * spec.block_n == spec.m
+        txt = open(os.path.join(GOLDEN, fname.replace(".ma.json", ".ma.txt"))).read()
+        if "0.125" in txt:
+            assert spec.scale == 0.125
+        elif "0.0883883" in txt:
+            assert spec.scale == 0.08838834764831845
+        else:
+            assert spec.scale is None
+        assert (spec.mask is not None) == ("Mask" in txt)
+
+
+@pytest.mark.parametrize("fname", all_ma_files())
+def test_static_cost_matches_reference_cost_model(fname):
+    mod = _load(fname)
+    mine = cost.cost_model(mod)
+    with open(os.path.join(GOLDEN, fname.replace(".ma.json", ".cost.json"))) as f:
+        ref = json.load(f)
+    assert mine.bytes_global == ref["bytes"]["Global"]
+    assert mine.bytes_shared == ref["bytes"]["Shared"]
+    assert mine.bytes_register == ref["bytes"]["Register"]
+    assert mine.flops == ref["flops"]
+    assert mine.steps == ref["steps"]
+    assert round(mine.modeled_cost, 6) == ref["modeled_cost"]
+
+
+def _ma_slices(mod):
+    """Evaluate every slice offset of the MA kernel at every (block, loop) point."""
+    k = mod.kernels[0]
+    (bvar, _, nb), = k.blocks
+    loop = [s for s in k.body if isinstance(s, ma_ir.Loop)][0]
+    out = []
+    for i in range(nb):
+        for j in range(loop.extent):
+            env = {bvar: i, loop.var: j}
+            for st in loop.body:
+                exprs = [st.expr] if isinstance(st, ma_ir.Compute) else []
+                for e in exprs:
+                    for n in e.walk():
+                        if isinstance(n, ma_ir.Ref) and mod.buffer(n.buffer).is_input:
+                            out.append((i, j, n.buffer, tuple((s.off.evaluate(env), s.length) for s in n.slices)))
+                if isinstance(st, ma_ir.Copy) and mod.buffer(st.src).is_input:
+                    out.append((i, j, st.src, tuple((s.off.evaluate(env), s.length) for s in st.src_slices)))
+    return out
+
+
+@pytest.mark.parametrize("fname", [f for f in all_ma_files() if not f.startswith("gemm")
+                                   and ("256" in f or "512" in f or "decode" in f)])
+def test_attention_index_math_matches_gpu_tiling(fname):
+    """Each GPU (CTA, kv-tile) is exactly the union of the MA (block, j0) tiles
+    it covers, visited in the MA's ascending j0 order."""
+    mod = _load(fname)
+    spec = recognize(mod)[0]
+    ma = _ma_slices(mod)
+    k_rows = {}
+    for i, j, buf, sl in ma:
+        if buf == spec.k:
+            k_rows.setdefault(j, set()).add(sl[0])
+    q_rows = {}
+    for st in mod.kernels[0].body:
+        if isinstance(st, ma_ir.Copy) and st.src == spec.q:
+            for i in range(spec.n_blocks):
+                q_rows[i] = (st.src_slices[0].off.evaluate({spec.block_var: i}), st.src_slices[0].length)
+    seen_q, seen_k = set(), set()
+    for cta, blocks, kv, iters in spec.gpu_tiles():
+        rows = sorted(q_rows[b] for b in blocks)
+        lo = cta * 256
+        hi = min(spec.n, lo + 256)
+        covered = sorted(r for o, l in rows for r in range(o, o + l))
+        assert covered == list(range(lo, hi))
+        assert iters == sorted(iters)
+        kcov = sorted(r for t in iters for (o, l) in k_rows[t] for r in range(o, o + l))
+        assert kcov == list(range(kv * 128, min(spec.m, kv * 128 + 128)))
+        seen_q.update(blocks)
+        seen_k.update(iters)
+    assert seen_q == set(range(spec.n_blocks)) and seen_k == set(range(spec.n_iters))
+
+
+def test_unrecognised_program_raises():
+    mod = _load("attn256.seed0.ma.json")
+    d = ma_ir.to_dict(mod)
+    # corrupt: make the epilogue multiply instead of divide
+    k = d["kernels"][0]
+    k["body"][-2]["expr"]["op"] = "mul"
+    with pytest.raises(UnsupportedMA):
+        recognize(ma_ir.from_dict(d))
+
+
+def test_precision_without_device_realisation_raises():
+    mod = _load("attn256.seed0.ma.json")
+    d = ma_ir.to_dict(mod)
+    d["precision"] = "fp64"
+    with pytest.raises(UnsupportedMA):
+        recognize(ma_ir.from_dict(d))
