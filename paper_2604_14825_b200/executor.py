@@ -223,7 +223,7 @@ def execute_ma(module, inputs: dict, device=None, precision=None, *, outer=None,
         if b.name in outputs:
             val = outputs[b.name]
             bufs[b.name] = val if return_torch else val.float().cpu().numpy()
-        elif b.is_input:
+        elif b.is_input and b.name in inputs:
             bufs[b.name] = inputs[b.name]
     return bufs, report
 

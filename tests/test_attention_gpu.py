@@ -148,3 +148,15 @@ def test_causal_mask_tensor_is_recognised_as_structured():
     inputs["Mask"][3, 0] = -1.0  # no longer the causal pattern -> general tensor path
     bufs, rep = execute_ma(mod, inputs)
     assert rep.realisation[0]["mask"] == "tensor"
+
+
+def test_llama_8k_causal_two_heads_vs_fp64():
+    """Full-length parity at the headline shape (2 q-heads sharing one kv-head)."""
+    B, Hq, Hkv, N, D = 1, 2, 1, 8192, 128
+    scale = 0.08838834764831845
+    q = _rand((B, Hq, N, D), 21)
+    k = _rand((B, Hkv, N, D), 22)
+    v = _rand((B, Hkv, N, D), 23)
+    got = _run_batched(q, k, v, scale, True)
+    ref = reference_math.attention_batched_fp64(q, k, v, scale, True)
+    _check(got, ref)
