@@ -51,8 +51,17 @@ CONFIGS = {
                     golden="bert512", scale=0.125),
     "attn256": dict(prog="attention", B=1, Hq=1, Hkv=1, N=256, D=64, causal=False,
                     golden="attn256", scale=None),
+    # config 5: decode, the 4 q-heads of a GQA group packed as the MA's 4 rows
+    "decode32k": dict(kind="decode", prog="llama", B=64, Hq=32, Hkv=8, N=1, M=32768, D=128, causal=False,
+                      golden="decode4_32k", scale=LLAMA_SCALE),
+    # config 2: (X.W1).W2 at 4096^3 x E=4096 (schedulable with max_tile_elems >= 262144)
+    "gemm_chain_e4096": dict(kind="gemm_chain", prog="gemm2", N=4096, K=4096, F=4096, E=4096,
+                             golden="gemm4k_e4096", causal=False, B=1, Hq=1, Hkv=1, D=0),
+    "gemm_chain_e128": dict(kind="gemm_chain", prog="gemm2", N=4096, K=4096, F=4096, E=128,
+                            golden="gemm4k_e128", causal=False, B=1, Hq=1, Hkv=1, D=0),
 }
 DEFAULT_CONFIG = "llama8k_causal"
+METRIC = "fused-attention bf16 TFLOP/s & % tensor peak; box throughput at 1/2/4/8 GPUs"
 
 
 def load_peaks():
@@ -142,14 +151,22 @@ def _sliced_module(ma, nblocks):
     return dataclasses.replace(ma, kernels=(dataclasses.replace(k, blocks=((v, ax, nblocks),)),))
 
 
-def _cpu_inputs(cfg):
+def _cpu_inputs(module):
+    """Seeded inputs for every input buffer of the MA module (causal pattern for Mask)."""
     import numpy as np
     rng = np.random.default_rng(0)
-    N, D = cfg["N"], cfg["D"]
-    inp = {n: rng.standard_normal((N, D)).astype(np.float32) for n in ("Q", "K", "V")}
-    if cfg["causal"]:
-        i = np.arange(N)
-        inp["Mask"] = np.where(i[None, :] <= i[:, None], np.float32(0), np.float32(-np.inf)).astype(np.float32)
+    inp = {}
+    for b in module.buffers:
+        if not b.is_input:
+            continue
+        shape = tuple(b.shape)
+        if b.name == "Mask":
+            n, m = shape
+            inp[b.name] = np.where(np.arange(m)[None, :] <= np.arange(n)[:, None], np.float32(0),
+                                   np.float32(-np.inf)).astype(np.float32)
+        else:
+            inp[b.name] = (rng.standard_normal(shape) / (np.sqrt(shape[0]) if b.name.startswith("W") else 1.0)
+                           ).astype(np.float32)
     return inp
 
 
@@ -177,23 +194,26 @@ def reference_module(cfg):
     if REF_PATH not in sys.path:
         sys.path.insert(0, REF_PATH)
     try:
+        import dataclasses
         from tilecc.autosched.scheduler import SchedulerOptions, run_autoscheduler
         from tilecc.ma.device import DEFAULT_DEVICE
         from tilecc.pipeline import frontend, lower_seed
         from paper_2604_14825_b200.programs import PROGRAMS
     except Exception:
         return None
-    bound, base = frontend(PROGRAMS[cfg["prog"]], dict(N=cfg["N"], M=cfg["N"], D=cfg["D"]))
-    seeds = run_autoscheduler(base, DEFAULT_DEVICE, SchedulerOptions())
-    return lower_seed(base, seeds[0].schedule, DEFAULT_DEVICE).ma
+    binding, devo, _ = cpu_binding(cfg)
+    device = dataclasses.replace(DEFAULT_DEVICE, **devo) if devo else DEFAULT_DEVICE
+    bound, base = frontend(PROGRAMS[cfg["prog"]], binding)
+    seeds = run_autoscheduler(base, device, SchedulerOptions())
+    return lower_seed(base, seeds[0].schedule, device).ma
 
 
 def cpu_baseline_sample(cfg, full_flops, target_s=10.0):
     """Time the reference CPU executor (or the oracle port) on a bounded sample, 1 core."""
     ma = reference_module(cfg)
-    inp = _cpu_inputs(cfg)
     total_blocks_per_slice = None
     if ma is not None:
+        inp = _cpu_inputs(ma)
         from tilecc.ma.device import DEFAULT_DEVICE
         from tilecc.ma.interp import interpret_ma
         kind = "reference"
@@ -203,6 +223,7 @@ def cpu_baseline_sample(cfg, full_flops, target_s=10.0):
         from oracle import ma_interp
         from paper_2604_14825_b200 import ma_ir
         mod, _ = load_ma(cfg)
+        inp = _cpu_inputs(mod)
         kind = "port"
         total_blocks_per_slice = mod.kernels[0].blocks[0][2]
         run = lambda nb: ma_interp.interpret_ma(_sliced_module(mod, nb), inp)
@@ -214,7 +235,7 @@ def cpu_baseline_sample(cfg, full_flops, target_s=10.0):
     run(nb)
     dt = time.perf_counter() - t
     per_block = dt / nb
-    slices = cfg["B"] * cfg["Hq"]
+    slices = cpu_binding(cfg)[2]
     total_s = per_block * total_blocks_per_slice * slices
     return {"value": full_flops / total_s / 1e12, "unit": "TFLOP/s", "cores": 1, "kind": kind,
             "sample": f"{nb} of {total_blocks_per_slice} MA blocks of one (b,h) slice "
@@ -235,7 +256,7 @@ def run_reference_arm(args, cfg, rank, world):
         mod, _ = load_ma(cfg)
     else:
         kind = "reference"
-    inp = _cpu_inputs(cfg)
+    inp = _cpu_inputs(ma if ma is not None else mod)
     cores = os.cpu_count() or 1
     total_blocks = (ma.kernels[0].blocks[0][2] if ma is not None else mod.kernels[0].blocks[0][2])
     _POOL_STATE["ma"] = ma if ma is not None else mod
@@ -251,10 +272,10 @@ def run_reference_arm(args, cfg, rank, world):
             if step >= args.warmup:
                 times.append(dt)
     step_s = statistics.mean(times)
-    blocks_total = total_blocks * cfg["B"] * cfg["Hq"]
+    blocks_total = total_blocks * cpu_binding(cfg)[2]
     full_s = step_s * blocks_total / cores
     value = flops / full_s / 1e12
-    out = {"metric": "fused-attention bf16 TFLOP/s (reference CPU tile executor)", "value": value,
+    out = {"metric": METRIC, "value": value,
            "unit": "TFLOP/s", "impl": "reference", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
@@ -270,17 +291,34 @@ def run_reference_arm(args, cfg, rank, world):
 # ----------------------------------------------------------------------------- GPU arm
 def attention_flops(cfg):
     B, Hq, N, D = cfg["B"], cfg["Hq"], cfg["N"], cfg["D"]
+    M = cfg.get("M", N)
+    if cfg.get("kind") == "gemm_chain":
+        return 2.0 * cfg["N"] * cfg["F"] * (cfg["K"] + cfg["E"])
     if cfg["causal"]:
         return 2.0 * B * Hq * D * N * (N + 1)
-    return 4.0 * B * Hq * N * N * D
+    return 4.0 * B * Hq * N * M * D
 
 
 def config_block(cfg, args):
     world = args.gpus
-    return {"workload": args.config, "program": cfg["prog"], "batch": cfg["B"], "heads_q": cfg["Hq"],
-            "heads_kv": cfg["Hkv"], "seq_len": cfg["N"], "head_dim": cfg["D"], "causal": cfg["causal"],
-            "ma_tiles": None, "parallelism": f"batch x kv-head sharding over {world} GPU(s)",
-            "l2": "flushed between timed steps (256 MiB write)"}
+    blk = {"workload": args.config}
+    blk.update({k: v for k, v in cfg.items() if k not in ("golden",)})
+    blk["parallelism"] = (f"row-block sharding over {world} GPU(s)" if cfg.get("kind") == "gemm_chain"
+                          else f"(batch, kv-head) group sharding over {world} GPU(s)")
+    blk["l2"] = "flushed between timed steps (256 MiB write)"
+    return blk
+
+
+def cpu_binding(cfg):
+    """(binding, device overrides, number of MA slices in the full workload) of the CPU baseline."""
+    kind = cfg.get("kind", "prefill")
+    if kind == "gemm_chain":
+        dev = {"max_tile_elems": 1000000} if cfg["E"] > 128 else {}
+        return dict(N=cfg["N"], K=cfg["K"], F=cfg["F"], E=cfg["E"]), dev, 1
+    if kind == "decode":
+        g = cfg["Hq"] // cfg["Hkv"]
+        return dict(N=g * cfg["N"], M=cfg["M"], D=cfg["D"]), {}, cfg["B"] * cfg["Hkv"]
+    return dict(N=cfg["N"], M=cfg.get("M", cfg["N"]), D=cfg["D"]), {}, cfg["B"] * cfg["Hq"]
 
 
 def shard(cfg, rank, world):
@@ -297,48 +335,89 @@ def shard(cfg, rank, world):
     raise SystemExit(f"cannot shard B={B}, Hkv={Hkv} over {world} GPUs")
 
 
+def build_workload(cfg, spec, rank, world, dev):
+    """Device tensors + launch plan for this rank's shard of the configured workload."""
+    import torch
+    from paper_2604_14825_b200.gemm import ChainPlan
+    from paper_2604_14825_b200.runtime import AttentionPlan, DecodePlan
+
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    kind = cfg.get("kind", "prefill")
+    w = {"kind": kind}
+    if kind == "gemm_chain":
+        N, K, F, E = cfg["N"], cfg["K"], cfg["F"], cfg["E"]
+        rows = N // world
+        x = torch.randn((rows, K), generator=gen, device=dev).to(torch.bfloat16)
+        w1 = (torch.randn((K, F), generator=gen, device=dev) / K ** 0.5).to(torch.bfloat16)
+        w2 = (torch.randn((F, E), generator=gen, device=dev) / F ** 0.5).to(torch.bfloat16)
+        y = torch.empty((rows, E), dtype=torch.bfloat16, device=dev)
+        w.update(plan=ChainPlan(x, w1, w2, y), out=y, local_flops=2.0 * rows * F * (K + E),
+                 total_flops=2.0 * N * F * (K + E), bound="tensor",
+                 host_inputs={spec.x: x, spec.w1: w1, spec.w2: w2}, outer=None, mask_kind=None,
+                 in_bytes=(x.numel() + w1.numel() + w2.numel()) * 2)
+        return w
+    b0, b1, h0, h1 = shard(cfg, rank, world)
+    g = cfg["Hq"] // cfg["Hkv"]
+    Bl, Hkvl = b1 - b0, h1 - h0
+    N, D = cfg["N"], cfg["D"]
+    M = cfg.get("M", N)
+    if kind == "decode":
+        # the MA's rows are the g q-heads of one kv group (SURVEY.md 8(d) config 5): Q [B, Hkv, g, D]
+        q = torch.randn((Bl, Hkvl, g * N, D), generator=gen, device=dev).to(torch.bfloat16)
+        k = torch.randn((Bl, Hkvl, M, D), generator=gen, device=dev).to(torch.bfloat16)
+        v = torch.randn((Bl, Hkvl, M, D), generator=gen, device=dev).to(torch.bfloat16)
+        o = torch.empty((Bl, Hkvl, g * N, D), dtype=torch.bfloat16, device=dev)
+        plan = DecodePlan(q, k, v, o, spec.scale)
+        kv_bytes = 2 * Bl * Hkvl * M * D * 2
+        w.update(plan=plan, out=o, local_flops=4.0 * Bl * Hkvl * g * N * M * D,
+                 total_flops=4.0 * cfg["B"] * cfg["Hq"] * N * M * D, bound="hbm",
+                 local_bytes=kv_bytes + 2 * q.numel() * 2, host_inputs={spec.q: q, spec.k: k, spec.v: v},
+                 outer=(Bl, Hkvl, Hkvl), mask_kind="none",
+                 in_bytes=(q.numel() + k.numel() + v.numel()) * 2)
+        return w
+    Hql = Hkvl * g
+    q = torch.randn((Bl, Hql, N, D), generator=gen, device=dev).to(torch.bfloat16)
+    k = torch.randn((Bl, Hkvl, M, D), generator=gen, device=dev).to(torch.bfloat16)
+    v = torch.randn((Bl, Hkvl, M, D), generator=gen, device=dev).to(torch.bfloat16)
+    o = torch.empty((Bl, Hql, N, D), dtype=torch.bfloat16, device=dev)
+    mask_kind = "causal" if cfg["causal"] else "none"
+    plan = AttentionPlan(q, k, v, o, spec.scale, mask_kind)
+    w.update(plan=plan, out=o, local_flops=plan.flops(), total_flops=attention_flops(cfg), bound="tensor",
+             host_inputs={spec.q: q, spec.k: k, spec.v: v}, outer=(Bl, Hql, Hkvl), mask_kind=mask_kind,
+             in_bytes=(q.numel() + k.numel() + v.numel()) * 2)
+    return w
+
+
 def run_ours(args, cfg, rank, world, dist):
     import torch
     from paper_2604_14825_b200 import _lib, execute_ma
     from paper_2604_14825_b200.recognize import recognize
-    from paper_2604_14825_b200.runtime import AttentionPlan
 
     dev = torch.device("cuda", torch.cuda.current_device())
     mod, ma_src = load_ma(cfg)
     spec = recognize(mod)[0]
-    b0, b1, h0, h1 = shard(cfg, rank, world)
-    g = cfg["Hq"] // cfg["Hkv"]
-    Bl, Hkvl, Hql = b1 - b0, h1 - h0, (h1 - h0) * g
-    N, D = cfg["N"], cfg["D"]
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(1234 + rank)
-    q = torch.randn((Bl, Hql, N, D), generator=gen, device=dev).to(torch.bfloat16)
-    k = torch.randn((Bl, Hkvl, N, D), generator=gen, device=dev).to(torch.bfloat16)
-    v = torch.randn((Bl, Hkvl, N, D), generator=gen, device=dev).to(torch.bfloat16)
-    o = torch.empty((Bl, Hql, N, D), dtype=torch.bfloat16, device=dev)
-    mask_kind = "causal" if cfg["causal"] else "none"
-    plan = AttentionPlan(q, k, v, o, spec.scale, mask_kind)
+    w = build_workload(cfg, spec, rank, world, dev)
+    plan, o = w["plan"], w["out"]
     full = torch.empty((world,) + tuple(o.shape), dtype=o.dtype, device=dev) if world > 1 else None
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
 
-    def step():
+    for _ in range(args.warmup):
+        flush.zero_()
         plan.launch(stream)
         if world > 1:
             dist.all_gather_into_tensor(full, o)
-
-    for _ in range(args.warmup):
-        flush.zero_()
-        step()
     torch.cuda.synchronize()
-    plan.check_errors()
+    if hasattr(plan, "check_errors"):
+        plan.check_errors()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     l0 = _lib.launch_count()
-    with ClockSampler(dev.index if rank == 0 else dev.index) as clk:
+    with ClockSampler(dev.index) as clk:
         for i in range(args.steps):
             flush.zero_()
             ev[i][0].record(stream)
@@ -354,84 +433,84 @@ def run_ours(args, cfg, rank, world, dist):
     torch.cuda.synchronize()
     kern_ms = [a.elapsed_time(b) for a, b, _ in ev]
     step_ms = [a.elapsed_time(c) for a, _, c in ev]
-    ms_kernel = statistics.mean(kern_ms)
-    ms_step = statistics.mean(step_ms)
+    ms_kernel_local = statistics.mean(kern_ms)
+    ms_kernel, ms_step = ms_kernel_local, statistics.mean(step_ms)
     if world > 1:
         t = torch.tensor([ms_step, ms_kernel], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_step, ms_kernel = float(t[0]), float(t[1])
-    total_flops = attention_flops(cfg)
+    total_flops = w["total_flops"]
     value = total_flops / (ms_step * 1e-3) / 1e12
-    local_flops = plan.flops()
-    achieved = local_flops / (statistics.mean(kern_ms) * 1e-3) / 1e12
     peaks, peak_src = load_peaks()
     clocks = clk.summary()
 
     # ---------------- e2e through the public API (pinned host in, host out)
-    e2e = None
-    if rank == 0 or True:
-        hq_ = q.cpu().pin_memory()
-        hk_ = k.cpu().pin_memory()
-        hv_ = v.cpu().pin_memory()
-        inputs = {spec.q: hq_, spec.k: hk_, spec.v: hv_}
-        outer = (Bl, Hql, Hkvl)
-        host_out = torch.empty(tuple(o.shape), dtype=torch.bfloat16).pin_memory()
+    host_in = {n: t.cpu().pin_memory() for n, t in w["host_inputs"].items()}
+    host_out = torch.empty(tuple(o.shape), dtype=o.dtype).pin_memory()
 
-        def e2e_step():
-            bufs, _ = execute_ma(mod, inputs, outer=outer, mask_kind=mask_kind, out_dtype="bf16",
-                                 return_torch=True, timing=False)
-            host_out.copy_(bufs[spec.o], non_blocking=True)
+    def e2e_step():
+        bufs, _ = execute_ma(mod, host_in, outer=w["outer"], mask_kind=w["mask_kind"], out_dtype="bf16",
+                             return_torch=True, timing=False)
+        out = bufs[mod.output]
+        host_out.copy_(out.reshape(host_out.shape), non_blocking=True)
 
-        for _ in range(max(1, args.warmup)):
-            e2e_step()
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    torch.cuda.synchronize()
+    e_ms = []
+    for _ in range(args.steps):
+        flush.zero_()
         torch.cuda.synchronize()
-        e_ms = []
-        for _ in range(args.steps):
-            flush.zero_()
-            torch.cuda.synchronize()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            e2e_step()
-            e1.record(stream)
-            e1.synchronize()
-            e_ms.append(e0.elapsed_time(e1))
-        em = statistics.mean(e_ms)
-        if world > 1:
-            t = torch.tensor([em], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            em = float(t[0])
-        e2e = {"value": total_flops / (em * 1e-3) / 1e12, "unit": "TFLOP/s",
-               "h2d_bytes_per_step": int((q.numel() + k.numel() + v.numel()) * 2 * world),
-               "d2h_bytes_per_step": int(o.numel() * 2 * world), "ms_per_step": em,
-               "api": "paper_2604_14825_b200.execute_ma"}
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        e2e_step()
+        e1.record(stream)
+        e1.synchronize()
+        e_ms.append(e0.elapsed_time(e1))
+    em = statistics.mean(e_ms)
+    if world > 1:
+        t = torch.tensor([em], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        em = float(t[0])
+    e2e = {"value": total_flops / (em * 1e-3) / 1e12, "unit": "TFLOP/s",
+           "h2d_bytes_per_step": int(w["in_bytes"] * world), "d2h_bytes_per_step": int(o.numel() * 2 * world),
+           "ms_per_step": em, "api": "paper_2604_14825_b200.execute_ma (pinned host tensors)"}
 
     if rank != 0:
         return
     traffic = None
-    prof = os.path.join(REPO, "profiles", "attn_fwd_ncu_summary.json")
+    prof = os.path.join(REPO, "profiles", f"latest_{args.config}_ncu.json")
     if os.path.exists(prof):
         try:
             with open(prof) as f:
-                pj = json.load(f)
-            if pj.get("workload") == args.config:
-                traffic = pj.get("dram_bytes_per_launch")
+                traffic = json.load(f).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    peak = peaks["bf16_tflops"]
+    if w["bound"] == "hbm":
+        achieved = w["local_bytes"] / (ms_kernel_local * 1e-3) / 1e9
+        peak = peaks["hbm_gbs"]
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})",
+                "algorithmic_bytes_per_launch": w["local_bytes"], "kernel": "decode_split_kernel + combine"}
+    else:
+        achieved = w["local_flops"] / (ms_kernel_local * 1e-3) / 1e12
+        peak = peaks["bf16_tflops"]
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": traffic, "peak_source": f"MEASURED_PEAKS.json bf16_tflops (burst; {peak_src})",
+                "algorithmic_flops_per_launch": w["local_flops"],
+                "kernel": {"prefill": "attn_fwd_kernel", "gemm_chain": getattr(plan, "realisation", "gemm")}[w["kind"]]}
+    peak_t = peaks["bf16_tflops"]
     out = {
-        "metric": "fused-attention bf16 TFLOP/s & % tensor peak; box throughput at 1/2/4/8 GPUs",
+        "metric": METRIC,
         "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (torch.randn, seeded)",
-        "config": dict(config_block(cfg, args), ma_tiles=[spec.block_m, spec.block_n], ma_source=ma_src,
-                       kernel_ms=ms_kernel),
-        "pct_of_peak": {"measured_burst": value / peak, "measured_sustained": value / peaks.get(
-            "bf16_tflops_sustained", peak), "nominal_2250": value / 2250.0, "peak_source": peak_src},
-        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": traffic,
-                     "peak_source": f"MEASURED_PEAKS.json bf16_tflops (burst; {peak_src})",
-                     "kernel": "attn_fwd_kernel<128,causal>" if cfg["causal"] else "attn_fwd_kernel"},
+        "config": dict(config_block(cfg, args), ma_source=ma_src, kernel_ms=ms_kernel),
+        "pct_of_peak": {"measured_burst": value / peak_t,
+                        "measured_sustained": value / peaks.get("bf16_tflops_sustained", peak_t),
+                        "nominal_2250": value / 2250.0, "peak_source": peak_src},
+        "roofline": roof,
         "e2e": e2e,
         "clocks": clocks,
         "gpu_launches": launches,

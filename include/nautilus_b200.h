@@ -81,19 +81,22 @@ typedef struct nt_decode_args {
   nt_tensor4 q, k, v, o;
   int32_t batch, heads_q, heads_kv, seq_q, seq_kv, head_dim;
   float scale;
-  int32_t num_splits; /* 0 = choose automatically */
+  int32_t num_splits; /* >= 1 (see nt_decode_num_splits) */
   int32_t out_dtype;
   void* workspace;
   int32_t* err_flag;
 } nt_decode_args;
-int64_t nt_decode_workspace_bytes(int32_t batch, int32_t heads_q, int32_t seq_q, int32_t head_dim,
+/* rows_per_group = (heads_q / heads_kv) * seq_q; workspace = fp32 (O, m, l) per split */
+int64_t nt_decode_workspace_bytes(int32_t batch, int32_t heads_kv, int32_t rows_per_group, int32_t head_dim,
                                   int32_t num_splits);
+/* split count the library would choose (requested > 0 is clamped to the key count) */
+int nt_decode_num_splits(int32_t batch, int32_t heads_kv, int32_t seq_kv, int32_t requested);
 int nt_attn_decode(const nt_decode_args* args, void* stream);
 
 /*
  * K3 GEMM (tcgen05, fp32 accumulate): C[M,N] = A[M,K] . B[K,N] with bf16 A, B
- * (row-major, unit inner stride) and bf16 or fp32 C; optional fp32 C_in added
- * (C = C_in + A.B) to realise the MA's `dot(..., acc=Y[...])`.
+ * (row-major, unit inner stride) and bf16 or fp32 C
+ * (the MA's zero-initialised `acc=Y[...]` accumulation is the GEMM's own K loop).
  * Used twice for the GEMM chain (X.W1).W2 when the Y accumulator does not fit
  * TMEM, and fused (nt_gemm_chain) when E <= 256.
  */

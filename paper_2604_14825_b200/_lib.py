@@ -19,7 +19,8 @@ NT_DTYPE_BF16, NT_DTYPE_F32 = 0, 1
 
 # Every symbol include/nautilus_b200.h declares (checked by tests/test_capi.py).
 EXPORTED = (
-    "nt_attn_fwd", "nt_attn_decode", "nt_decode_workspace_bytes", "nt_gemm", "nt_gemm_chain",
+    "nt_attn_fwd", "nt_attn_decode", "nt_decode_workspace_bytes", "nt_decode_num_splits", "nt_gemm",
+    "nt_gemm_chain",
     "nt_cast_f32_to_bf16", "nt_cast_bf16_to_f32", "nt_abi_version", "nt_last_error", "nt_launch_count",
 )
 
@@ -79,6 +80,8 @@ def lib():
             L.nt_attn_decode.argtypes = [C.POINTER(DecodeArgs), C.c_void_p]
             L.nt_decode_workspace_bytes.argtypes = [C.c_int32] * 5
             L.nt_decode_workspace_bytes.restype = C.c_int64
+            L.nt_decode_num_splits.argtypes = [C.c_int32] * 4
+            L.nt_decode_num_splits.restype = C.c_int
             L.nt_gemm.argtypes = [C.POINTER(GemmArgs), C.c_void_p]
             L.nt_gemm_chain.argtypes = [C.POINTER(ChainArgs), C.c_void_p]
             L.nt_cast_f32_to_bf16.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]

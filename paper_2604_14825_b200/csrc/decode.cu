@@ -1,0 +1,89 @@
+// C ABI: nt_attn_decode (K2 split-KV decode + combine).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "../../include/nautilus_b200.h"
+#include "common_host.h"
+#include "decode.cuh"
+
+using namespace nt;
+
+namespace {
+int sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+int choose_splits(int groups, int M, int requested) {
+  if (requested > 0) return std::min(requested, std::max(1, (M + 63) / 64));
+  const int by_occupancy = (16 * sms() + groups - 1) / groups;
+  const int by_length = std::max(1, (M + 1023) / 1024);
+  return std::max(1, std::min(by_occupancy, by_length));
+}
+
+template <int R>
+int launch(DecodeParams& p, cudaStream_t st) {
+  dim3 grid(p.splits, p.B * p.Hkv);
+  decode_split_kernel<R><<<grid, kDecodeThreads, 0, st>>>(p);
+  g_launches++;
+  int rc = check_cuda(cudaGetLastError(), "decode_split launch");
+  if (rc) return rc;
+  const int rows = p.B * p.Hkv * R;
+  decode_combine_kernel<<<(rows + 3) / 4, 128, 0, st>>>(p, R);
+  g_launches++;
+  return check_cuda(cudaGetLastError(), "decode_combine launch");
+}
+}  // namespace
+
+extern "C" int64_t nt_decode_workspace_bytes(int32_t batch, int32_t heads_kv, int32_t rows_per_group,
+                                             int32_t head_dim, int32_t num_splits) {
+  return (int64_t)batch * heads_kv * num_splits * rows_per_group * (head_dim + 2) * (int64_t)sizeof(float);
+}
+
+extern "C" int nt_attn_decode(const nt_decode_args* a, void* stream) {
+  if (!a) return set_error(NT_ERR_INVALID, "null args");
+  if (a->head_dim != kDecodeD) return set_error(NT_ERR_UNSUPPORTED, "decode kernel is built for head_dim 128");
+  if (a->heads_q % a->heads_kv) return set_error(NT_ERR_INVALID, "heads_q must be a multiple of heads_kv");
+  const int g = a->heads_q / a->heads_kv;
+  const int R = g * a->seq_q;
+  if (R != 1 && R != 2 && R != 4 && R != 8)
+    return set_error(NT_ERR_UNSUPPORTED, "decode kernel packs 1, 2, 4 or 8 query rows per kv group");
+  if (!a->workspace) return set_error(NT_ERR_INVALID, "workspace required");
+  for (const nt_tensor4* t : {&a->q, &a->k, &a->v})
+    if (reinterpret_cast<uintptr_t>(t->ptr) % 16 || t->stride_s % 8 || t->stride_h % 8 || t->stride_b % 8)
+      return set_error(NT_ERR_INVALID, "q/k/v must be 16-byte aligned with strides % 8 == 0");
+  DecodeParams p{};
+  p.q = static_cast<const __nv_bfloat16*>(a->q.ptr);
+  p.q_sb = a->q.stride_b; p.q_sh = a->q.stride_h; p.q_sn = a->q.stride_s;
+  p.k = static_cast<const __nv_bfloat16*>(a->k.ptr);
+  p.k_sb = a->k.stride_b; p.k_sh = a->k.stride_h; p.k_sn = a->k.stride_s;
+  p.v = static_cast<const __nv_bfloat16*>(a->v.ptr);
+  p.v_sb = a->v.stride_b; p.v_sh = a->v.stride_h; p.v_sn = a->v.stride_s;
+  p.o = a->o.ptr;
+  p.o_sb = a->o.stride_b; p.o_sh = a->o.stride_h; p.o_sn = a->o.stride_s;
+  p.out_f32 = a->out_dtype == NT_DTYPE_F32;
+  p.B = a->batch; p.Hq = a->heads_q; p.Hkv = a->heads_kv; p.Nq = a->seq_q; p.M = a->seq_kv; p.g = g;
+  p.scale_log2 = a->scale * 1.4426950408889634f;
+  p.splits = a->num_splits;
+  p.keys_per_split = (a->seq_kv + p.splits - 1) / p.splits;
+  p.ws = static_cast<float*>(a->workspace);
+  p.err = a->err_flag;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  switch (R) {
+    case 1: return launch<1>(p, st);
+    case 2: return launch<2>(p, st);
+    case 4: return launch<4>(p, st);
+    default: return launch<8>(p, st);
+  }
+}
+
+extern "C" int nt_decode_num_splits(int32_t batch, int32_t heads_kv, int32_t seq_kv, int32_t requested) {
+  return choose_splits(batch * heads_kv, seq_kv, requested);
+}

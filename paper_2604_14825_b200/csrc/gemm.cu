@@ -1,0 +1,133 @@
+// C ABI: nt_gemm (K3) and nt_gemm_chain (K3b).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+
+#include "../../include/nautilus_b200.h"
+#include "chain.cuh"
+#include "common_host.h"
+#include "gemm.cuh"
+
+using namespace nt;
+
+namespace {
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int BN, bool F32>
+int launch_gemm(const nt_gemm_args* a, cudaStream_t st) {
+  CUtensorMap ma, mb;
+  int rc;
+  if ((rc = make_map_2d(&ma, a->a, a->k, a->m, a->lda, 64, 128, 2, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+  if ((rc = make_map_2d(&mb, a->b, a->n, a->k, a->ldb, 64, 64, 2, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+  GemmParams p{};
+  p.M = a->m;
+  p.N = a->n;
+  p.K = a->k;
+  p.tiles_m = (a->m + 127) / 128;
+  p.tiles_n = (a->n + BN - 1) / BN;
+  p.c = a->c;
+  p.ldc = a->ldc;
+  auto kern = gemm_kernel<BN, F32>;
+  const int smem = GemmCfg<BN>::SMEM_BYTES;
+  static bool configured = false;
+  if (!configured) {
+    if ((rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+                         "cudaFuncSetAttribute(gemm)")))
+      return rc;
+    configured = true;
+  }
+  const int tiles = p.tiles_m * p.tiles_n;
+  const int grid = std::min(tiles, sm_count());
+  kern<<<grid, kGemmThreads, smem, st>>>(ma, mb, p);
+  g_launches++;
+  return check_cuda(cudaGetLastError(), "gemm launch");
+}
+
+template <int E>
+int launch_chain(const nt_chain_args* a, cudaStream_t st) {
+  CUtensorMap mx, mw1, mw2;
+  int rc;
+  if ((rc = make_map_2d(&mx, a->x, a->k, a->n, a->ldx, 64, 128, 2, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+  if ((rc = make_map_2d(&mw1, a->w1, a->f, a->k, a->ldw1, 64, 64, 2, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+  if ((rc = make_map_2d(&mw2, a->w2, a->e, a->f, a->ldw2, 64, 128, 2, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+  ChainParams p{};
+  p.N = a->n;
+  p.K = a->k;
+  p.F = a->f;
+  p.E = a->e;
+  p.row_blocks = (a->n + 127) / 128;
+  const int f_tiles = (a->f + 127) / 128;
+  int splits = std::max(1, std::min(f_tiles, sm_count() / std::max(1, p.row_blocks)));
+  p.f_tiles_per_split = (f_tiles + splits - 1) / splits;
+  splits = (f_tiles + p.f_tiles_per_split - 1) / p.f_tiles_per_split;
+  p.splits = splits;
+  p.y = a->y;
+  p.ldy = a->ldy;
+  p.out_f32 = a->out_dtype == NT_DTYPE_F32;
+  float* partial = nullptr;
+  if (splits > 1) {
+    if ((rc = check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&partial),
+                                         sizeof(float) * (size_t)splits * a->n * a->e, st),
+                         "cudaMallocAsync(chain partials)")))
+      return rc;
+  }
+  p.partial = partial;
+  auto kern = chain_kernel<E>;
+  const int smem = ChainCfg<E>::SMEM_BYTES;
+  static bool configured = false;
+  if (!configured) {
+    if ((rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+                         "cudaFuncSetAttribute(chain)")))
+      return rc;
+    configured = true;
+  }
+  kern<<<p.row_blocks * splits, kChainThreads, smem, st>>>(mx, mw1, mw2, p);
+  g_launches++;
+  if ((rc = check_cuda(cudaGetLastError(), "chain launch"))) return rc;
+  if (splits > 1) {
+    const long long total = (long long)a->n * a->e;
+    const int blocks = (int)std::min<long long>((total + 255) / 256, 4 * sm_count());
+    chain_reduce_kernel<<<blocks, 256, 0, st>>>(partial, splits, a->n, a->e, a->y, a->ldy, p.out_f32);
+    g_launches++;
+    if ((rc = check_cuda(cudaGetLastError(), "chain reduce launch"))) return rc;
+    if ((rc = check_cuda(cudaFreeAsync(partial, st), "cudaFreeAsync"))) return rc;
+  }
+  return NT_OK;
+}
+}  // namespace
+
+extern "C" int nt_gemm(const nt_gemm_args* a, void* stream) {
+  if (!a) return set_error(NT_ERR_INVALID, "null args");
+  if (a->m <= 0 || a->n <= 0 || a->k <= 0) return set_error(NT_ERR_INVALID, "non-positive extent");
+  if (a->k % 8 || a->n % 8) return set_error(NT_ERR_UNSUPPORTED, "K and N must be multiples of 8");
+  if (a->ldc % 8) return set_error(NT_ERR_INVALID, "ldc must be a multiple of 8");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool f32 = a->out_dtype == NT_DTYPE_F32;
+  if (a->n <= 128) return f32 ? launch_gemm<128, true>(a, st) : launch_gemm<128, false>(a, st);
+  return f32 ? launch_gemm<256, true>(a, st) : launch_gemm<256, false>(a, st);
+}
+
+extern "C" int nt_gemm_chain(const nt_chain_args* a, void* stream) {
+  if (!a) return set_error(NT_ERR_INVALID, "null args");
+  if (a->n <= 0 || a->k <= 0 || a->f <= 0 || a->e <= 0) return set_error(NT_ERR_INVALID, "non-positive extent");
+  if (a->k % 8 || a->f % 8 || a->e % 8) return set_error(NT_ERR_UNSUPPORTED, "K, F, E must be multiples of 8");
+  if (a->e > 256) return set_error(NT_ERR_UNSUPPORTED, "fused chain keeps Y in TMEM: E must be <= 256");
+  if (a->ldy % 8) return set_error(NT_ERR_INVALID, "ldy must be a multiple of 8");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (a->e <= 64) return launch_chain<64>(a, st);
+  if (a->e <= 128) return launch_chain<128>(a, st);
+  return launch_chain<256>(a, st);
+}
+
+// K2 decode entry points live in decode.cu

@@ -1,0 +1,180 @@
+// K3: tcgen05 GEMM C[M,N] = A[M,K] . B[K,N] (bf16 in, fp32 accumulate in TMEM).
+//
+// Realises the MA dots of the GEMM-chain kernel (SURVEY.md B.4, Appendix C
+// V5/V6): `xT = dot(X[64*i0:+64, 0:K], W1[0:K, 128*j0:+128])` and
+// `xY = dot(xT, W2[128*j0:+128, 0:E], acc=Y[...])`, which interpret_ma runs as
+// sequential rank-1 updates (tilecc/ma/interp.py:241-251).
+//
+// Persistent, warp-specialised:
+//   warp 0      TMA producer (A K-major panels, B MN-major panels, SWIZZLE_128B)
+//   warp 1      MMA issuer: tcgen05.mma.cta_group::1.kind::f16 M=128 N=BN K=16
+//   warps 2-5   epilogue: TMEM -> registers -> global (fp32 or bf16)
+// TMEM holds two BN-column accumulators so the epilogue of tile i overlaps
+// the main loop of tile i+1.
+#pragma once
+#include "sm100.cuh"
+
+namespace nt {
+
+struct GemmParams {
+  int M, N, K;
+  int tiles_m, tiles_n;
+  void* c;
+  long long ldc;
+};
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int BM = 128, BK = 64;
+  static constexpr int A_BYTES = BM * BK * 2;   // 16 KB
+  static constexpr int B_BYTES = BK * BN * 2;   // 32 KB at BN=256
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (BN == 256) ? 4 : 6;
+  static constexpr int SMEM_BAR = STAGES * STAGE;
+  static constexpr int NBAR = 2 * STAGES + 4;
+  static constexpr int SMEM_BYTES = SMEM_BAR + NBAR * 8 + 16 + 1024;
+  static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
+};
+
+constexpr int kGemmThreads = 192;
+
+template <int BN, bool OUT_F32>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const GemmParams p) {
+  using C = GemmCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_u32 = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw_u32 + 1023u) & ~1023u) - raw_u32);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::SMEM_BAR);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + C::STAGES;
+  uint64_t* tfull = bars + 2 * C::STAGES;      // [2]
+  uint64_t* tempty = bars + 2 * C::STAGES + 2; // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBAR);
+
+  const int warp = __shfl_sync(0xffffffffu, threadIdx.x / 32, 0);
+  const int lane = threadIdx.x & 31;
+  const int num_tiles = p.tiles_m * p.tiles_n;
+  const int k_blocks = (p.K + C::BK - 1) / C::BK;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int it = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int mb = tile % p.tiles_m, nb = tile / p.tiles_m;
+        for (int kb = 0; kb < k_blocks; ++kb, ++it) {
+          const int s = it % C::STAGES;
+          mbar_wait(&empty[s], ((it / C::STAGES) & 1) ^ 1);
+          mbar_arrive_expect_tx(&full[s], C::STAGE);
+          uint8_t* sa = smem + s * C::STAGE;
+          uint8_t* sb = sa + C::A_BYTES;
+          tma_load_2d(sa, &tmA, &full[s], kb * C::BK, mb * C::BM);
+#pragma unroll
+          for (int c = 0; c < BN / 64; ++c)
+            tma_load_2d(sb + c * (C::BK * 128), &tmB, &full[s], nb * BN + c * 64, kb * C::BK);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16(128, BN, 0, 1);
+      const uint32_t sbase = smem_u32(smem);
+      int it = 0, tcount = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tcount) {
+        const int acc = tcount & 1;
+        mbar_wait(&tempty[acc], ((tcount >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * BN;
+        for (int kb = 0; kb < k_blocks; ++kb, ++it) {
+          const int s = it % C::STAGES;
+          mbar_wait(&full[s], (it / C::STAGES) & 1);
+          tc_fence_after();
+          const uint32_t sa = sbase + s * C::STAGE;
+          const uint32_t sb = sa + C::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < C::BK / 16; ++k) {
+            const uint64_t ad = sdesc_sw128(sa + k * 32, 16, 1024);
+            const uint64_t bd = sdesc_sw128(sb + k * 2048, C::BK * 128, 1024);
+            umma_ss(d, ad, bd, idesc, (kb | k) ? 1u : 0u);
+          }
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&tfull[acc]);
+      }
+    }
+  } else {
+    // epilogue warps 2..5 -> TMEM sub-partitions 2,3,0,1
+    const int wq = warp & 3;
+    const int r = wq * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
+    int tcount = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tcount) {
+      const int acc = tcount & 1;
+      const int mb = tile % p.tiles_m, nb = tile / p.tiles_m;
+      mbar_wait(&tfull[acc], (tcount >> 1) & 1);
+      tc_fence_after();
+      const int row = mb * 128 + r;
+      const bool rv = row < p.M;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tmem + acc * BN + lane_off + c * 32, v);
+        tmem_wait_ld();
+        const int col0 = nb * BN + c * 32;
+        if (rv && col0 < p.N) {
+          if (OUT_F32) {
+            float* cp = static_cast<float*>(p.c) + (long long)row * p.ldc + col0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if (col0 + 4 * i < p.N)
+                *reinterpret_cast<float4*>(cp + 4 * i) =
+                    make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                                __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+          } else {
+            __nv_bfloat16* cp = static_cast<__nv_bfloat16*>(p.c) + (long long)row * p.ldc + col0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              if (col0 + 8 * i < p.N)
+                *reinterpret_cast<uint4*>(cp + 8 * i) = make_uint4(
+                    pack_bf16(__uint_as_float(v[8 * i]), __uint_as_float(v[8 * i + 1])),
+                    pack_bf16(__uint_as_float(v[8 * i + 2]), __uint_as_float(v[8 * i + 3])),
+                    pack_bf16(__uint_as_float(v[8 * i + 4]), __uint_as_float(v[8 * i + 5])),
+                    pack_bf16(__uint_as_float(v[8 * i + 6]), __uint_as_float(v[8 * i + 7])));
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+  }
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+}  // namespace nt

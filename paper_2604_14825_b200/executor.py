@@ -39,7 +39,7 @@ from . import _lib, cost
 from . import ma_ir as ir
 from .errors import DivisionByZero, OutOfBounds, UnsupportedMA
 from .recognize import AttentionSpec, GemmChainSpec, recognize
-from .runtime import AttentionPlan
+from .runtime import AttentionPlan, DecodePlan, decode_eligible
 
 
 @dataclass
@@ -139,7 +139,13 @@ def _prepare_attention(spec: AttentionSpec, module: ir.Module, inputs: dict, out
         kind = mask_kind  # caller asserts a structured mask on an unmasked program
     odt = torch.float32 if out_dtype in (None, "fp32", torch.float32) else torch.bfloat16
     o = torch.empty((B, Hq, spec.n, spec.dv), dtype=odt, device=dev)
-    plan = AttentionPlan(q, k, v, o, spec.scale, kind, mask_t)
+    Hkv = k.shape[1] if outer is not None else 1
+    rows = (Hq // Hkv) * spec.n
+    if decode_eligible(rows, spec.d, kind) and spec.m >= 1024:
+        # short query block over a long KV range: K2 split-KV decode
+        plan = DecodePlan(q, k, v, o, spec.scale)
+    else:
+        plan = AttentionPlan(q, k, v, o, spec.scale, kind, mask_t)
     return plan, o, outer
 
 
@@ -191,9 +197,13 @@ def execute_ma(module, inputs: dict, device=None, precision=None, *, outer=None,
         report.specs.append(spec)
         if isinstance(spec, AttentionSpec):
             plan, o, outer_used = _prepare_attention(spec, mod, inputs, outer, mask_kind, out_dtype, dev)
-            report.realisation.append({"kernel": "attn_fwd", "mask": plan.mask_kind,
-                                       "grid_ctas": -(-spec.n // 256) * o.shape[0] * o.shape[1],
-                                       "gpu_tile": (256, 128), "ma_tile": (spec.block_m, spec.block_n)})
+            if isinstance(plan, DecodePlan):
+                report.realisation.append({"kernel": "attn_decode_splitkv", "mask": "none",
+                                           "splits": plan.splits, "ma_tile": (spec.block_m, spec.block_n)})
+            else:
+                report.realisation.append({"kernel": "attn_fwd", "mask": plan.mask_kind,
+                                           "grid_ctas": -(-spec.n // 256) * o.shape[0] * o.shape[1],
+                                           "gpu_tile": (256, 128), "ma_tile": (spec.block_m, spec.block_n)})
             ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             ev0.record()
             plan.launch(stream)

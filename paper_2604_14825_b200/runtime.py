@@ -106,3 +106,59 @@ def _causal_pairs(N: int, M: int, off: int) -> int:
     """sum_i clamp(i + off + 1, 0, M): unmasked (query, key) pairs of a causal mask."""
     import numpy as np
     return int(np.clip(np.arange(N, dtype=np.int64) + off + 1, 0, M).sum())
+
+
+class DecodePlan:
+    """K2 split-KV decode over [B, Hq, Nq, 128] queries ((Hq/Hkv) * Nq in {1, 2, 4, 8} rows per kv group)."""
+
+    def __init__(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor,
+                 scale: Optional[float], num_splits: int = 0, err_flag: Optional[torch.Tensor] = None):
+        q, k, v, o = _as4(q), _as4(k), _as4(v), _as4(o)
+        for name, t in (("q", q), ("k", k), ("v", v)):
+            if t.dtype != torch.bfloat16 or not t.is_cuda:
+                raise InvalidArguments(f"{name} must be a CUDA bf16 tensor")
+        B, Hq, Nq, D = q.shape
+        _, Hkv, M, _ = k.shape
+        if tuple(v.shape) != (B, Hkv, M, D) or tuple(o.shape) != (B, Hq, Nq, D) or Hq % Hkv:
+            raise InvalidArguments("q/k/v/o shapes inconsistent")
+        L = _lib.lib()
+        splits = int(L.nt_decode_num_splits(B, Hkv, M, int(num_splits)))
+        rows = (Hq // Hkv) * Nq
+        ws_bytes = int(L.nt_decode_workspace_bytes(B, Hkv, rows, D, splits))
+        self.ws = torch.empty(max(ws_bytes // 4, 1), dtype=torch.float32, device=q.device)
+        self.err = err_flag if err_flag is not None else torch.zeros(1, dtype=torch.int32, device=q.device)
+        a = _lib.DecodeArgs()
+        a.q, a.k, a.v, a.o = _t4(q), _t4(k), _t4(v), _t4(o)
+        a.batch, a.heads_q, a.heads_kv, a.seq_q, a.seq_kv, a.head_dim = B, Hq, Hkv, Nq, M, D
+        a.scale = 1.0 if scale is None else float(scale)
+        a.num_splits = splits
+        a.out_dtype = _lib.NT_DTYPE_F32 if o.dtype == torch.float32 else _lib.NT_DTYPE_BF16
+        a.workspace = self.ws.data_ptr()
+        a.err_flag = self.err.data_ptr()
+        self.args, self.splits = a, splits
+        self.tensors = (q, k, v, o)
+        self.shape = (B, Hq, Hkv, Nq, M, D)
+        self._fn = L.nt_attn_decode
+        self._ref = C.byref(a)
+        self.mask_kind = "none"
+
+    def launch(self, stream=None) -> None:
+        st = self._fn(self._ref, _stream_handle(stream))
+        if st:
+            _lib.check(st, "nt_attn_decode")
+
+    def flops(self) -> float:
+        B, Hq, _, Nq, M, D = self.shape
+        return 4.0 * B * Hq * Nq * M * D
+
+    def kv_bytes(self) -> int:
+        B, _, Hkv, _, M, D = self.shape
+        return 2 * B * Hkv * M * D * 2
+
+    def check_errors(self) -> None:
+        if int(self.err.item()) & 1:
+            raise DivisionByZero("tile divide: softmax denominator is zero")
+
+
+def decode_eligible(n_rows_per_group: int, d: int, mask_kind: str) -> bool:
+    return mask_kind == "none" and d == 128 and n_rows_per_group in (1, 2, 4, 8)

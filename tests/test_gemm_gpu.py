@@ -1,0 +1,83 @@
+"""K3 GEMM / K3b fused chain on the B200 vs the CPU oracle (need a GPU)."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import load_golden
+from oracle import reference_math
+from oracle.ma_interp import round_bf16
+
+pytestmark = pytest.mark.gpu
+
+
+def _check(got, ref, max_abs=2e-2, rel=1e-2):
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    assert np.all(np.isfinite(got))
+    mx = float(np.max(np.abs(got - ref)))
+    rl = float(np.linalg.norm(got - ref) / np.linalg.norm(ref))
+    assert mx <= max_abs and rl <= rel, (mx, rl)
+
+
+@pytest.mark.parametrize("case", ["gemm_v6", "gemm_v5"])
+def test_execute_ma_gemm_chain_matches_reference(case):
+    from paper_2604_14825_b200 import execute_ma
+
+    mod, inputs, interp32, ref64 = load_golden(case)
+    bufs, rep = execute_ma(mod, inputs)
+    _check(bufs[mod.output], interp32)
+    _check(bufs[mod.output], ref64)
+    assert rep.realisation[0]["kernel"] == "chain_fused"
+
+
+@pytest.mark.parametrize("M,N,K,f32", [(128, 128, 64, True), (256, 512, 512, True), (300, 264, 136, True),
+                                       (1024, 768, 1024, False), (4096, 4096, 4096, False)])
+def test_gemm_vs_fp64(M, N, K, f32):
+    from paper_2604_14825_b200.gemm import GemmPlan
+
+    g = np.random.default_rng(M + N + K)
+    a = round_bf16(g.standard_normal((M, K)))
+    b = round_bf16(g.standard_normal((K, N)) / np.sqrt(K))
+    ta = torch.from_numpy(a).cuda().bfloat16()
+    tb = torch.from_numpy(b).cuda().bfloat16()
+    c = torch.empty((M, N), dtype=torch.float32 if f32 else torch.bfloat16, device="cuda")
+    GemmPlan(ta, tb, c).launch()
+    torch.cuda.synchronize()
+    ref = a.astype(np.float64) @ b.astype(np.float64)
+    _check(c.float().cpu().numpy(), ref, max_abs=3e-2 if not f32 else 2e-2)
+
+
+@pytest.mark.parametrize("N,K,F,E", [(256, 256, 512, 128), (512, 1024, 1024, 64), (384, 512, 768, 256),
+                                     (130, 136, 200, 72)])
+def test_fused_chain_vs_fp64(N, K, F, E):
+    from paper_2604_14825_b200.gemm import ChainPlan
+
+    g = np.random.default_rng(N + K + F + E)
+    x = round_bf16(g.standard_normal((N, K)))
+    w1 = round_bf16(g.standard_normal((K, F)) / np.sqrt(K))
+    w2 = round_bf16(g.standard_normal((F, E)) / np.sqrt(F))
+    tx, t1, t2 = (torch.from_numpy(v).cuda().bfloat16() for v in (x, w1, w2))
+    y = torch.empty((N, E), dtype=torch.float32, device="cuda")
+    plan = ChainPlan(tx, t1, t2, y)
+    assert plan.fused
+    plan.launch()
+    torch.cuda.synchronize()
+    _check(y.cpu().numpy(), reference_math.gemm_chain_fp64(x, w1, w2))
+
+
+def test_two_gemm_chain_realisation_e4096_shape():
+    from paper_2604_14825_b200.gemm import ChainPlan
+
+    N, K, F, E = 512, 1024, 1024, 4096
+    g = np.random.default_rng(5)
+    x = round_bf16(g.standard_normal((N, K)))
+    w1 = round_bf16(g.standard_normal((K, F)) / np.sqrt(K))
+    w2 = round_bf16(g.standard_normal((F, E)) / np.sqrt(F))
+    tx, t1, t2 = (torch.from_numpy(v).cuda().bfloat16() for v in (x, w1, w2))
+    y = torch.empty((N, E), dtype=torch.float32, device="cuda")
+    plan = ChainPlan(tx, t1, t2, y)
+    assert not plan.fused
+    plan.launch()
+    torch.cuda.synchronize()
+    _check(y.cpu().numpy(), reference_math.gemm_chain_fp64(x, w1, w2))
