@@ -101,25 +101,30 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_split_kernel(const D
   const __nv_bfloat16* kbase = p.k + b * p.k_sb + hkv * p.k_sh + d0;
   const __nv_bfloat16* vbase = p.v + b * p.v_sb + hkv * p.v_sh + d0;
 
-  int j = j0 + kg;
+  // warp-uniform trip count: every lane runs every step (the TPK-lane shuffles
+  // below need all lanes of the warp); out-of-range keys contribute nothing.
+  const int nsteps = (j1 > j0) ? (j1 - j0 + KPS - 1) / KPS : 0;
   uint4 kc[NV], vc[NV];
-  if (j < j1) {
+  {
+    const int j = j0 + kg;
+    const bool ok = j < j1;
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
-      kc[i] = ldg_nc_v4(kbase + (long long)j * p.k_sn + 8 * i);
-      vc[i] = ldg_nc_v4(vbase + (long long)j * p.v_sn + 8 * i);
+      kc[i] = ok ? ldg_nc_v4(kbase + (long long)j * p.k_sn + 8 * i) : make_uint4(0, 0, 0, 0);
+      vc[i] = ok ? ldg_nc_v4(vbase + (long long)j * p.v_sn + 8 * i) : make_uint4(0, 0, 0, 0);
     }
   }
-  for (; j < j1; j += KPS) {
+  for (int st = 0; st < nsteps; ++st) {
+    const int j = j0 + st * KPS + kg;
+    const bool valid = j < j1;
     // prefetch the next key of this group (one step ahead)
     uint4 kn[NV], vn[NV];
     const int jn = j + KPS;
-    if (jn < j1) {
+    const bool okn = jn < j1;
 #pragma unroll
-      for (int i = 0; i < NV; ++i) {
-        kn[i] = ldg_nc_v4(kbase + (long long)jn * p.k_sn + 8 * i);
-        vn[i] = ldg_nc_v4(vbase + (long long)jn * p.v_sn + 8 * i);
-      }
+    for (int i = 0; i < NV; ++i) {
+      kn[i] = okn ? ldg_nc_v4(kbase + (long long)jn * p.k_sn + 8 * i) : make_uint4(0, 0, 0, 0);
+      vn[i] = okn ? ldg_nc_v4(vbase + (long long)jn * p.v_sn + 8 * i) : make_uint4(0, 0, 0, 0);
     }
     float kf[DPT], vf[DPT];
 #pragma unroll
@@ -142,19 +147,21 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) decode_split_kernel(const D
     for (int off = 1; off < TPK; off <<= 1)
 #pragma unroll
       for (int r = 0; r < R; ++r) sc[r] += __shfl_xor_sync(0xffffffffu, sc[r], off);
+    if (valid) {
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      if (sc[r] > m[r] + 8.0f) {  // lazy rescale (exact identity; keeps p <= 2^8)
-        const float alpha = ex2(m[r] - sc[r]);
-        l[r] *= alpha;
+      for (int r = 0; r < R; ++r) {
+        if (sc[r] > m[r] + 8.0f) {  // lazy rescale (exact identity; keeps p <= 2^8)
+          const float alpha = ex2(m[r] - sc[r]);
+          l[r] *= alpha;
 #pragma unroll
-        for (int i = 0; i < DPT; ++i) o[r][i] *= alpha;
-        m[r] = sc[r];
+          for (int i = 0; i < DPT; ++i) o[r][i] *= alpha;
+          m[r] = sc[r];
+        }
+        const float pr = ex2(sc[r] - m[r]);
+        l[r] += pr;
+#pragma unroll
+        for (int i = 0; i < DPT; ++i) o[r][i] = fmaf(pr, vf[i], o[r][i]);
       }
-      const float pr = ex2(sc[r] - m[r]);
-      l[r] += pr;
-#pragma unroll
-      for (int i = 0; i < DPT; ++i) o[r][i] = fmaf(pr, vf[i], o[r][i]);
     }
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
