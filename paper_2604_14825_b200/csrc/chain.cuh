@@ -205,39 +205,33 @@ __global__ void __launch_bounds__(kChainThreads, 1)
     mbar_wait(y_full, 0);
     tc_fence_after();
     const int row = rb * 128 + r;
-    if (row < p.N) {
+    const bool rv = row < p.N;
+    // tcgen05.ld is .sync.aligned: every lane loads, only valid rows store
 #pragma unroll 1
-      for (int c = 0; c < E / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(tY + lane_off + c * 32, v);
-        tmem_wait_ld();
-        const int col0 = c * 32;
-        if (col0 >= p.E) continue;
-        if (p.splits > 1 || p.out_f32) {
-          float* dst = (p.splits > 1) ? p.partial + ((long long)split * p.N + row) * p.E + col0
-                                      : static_cast<float*>(p.y) + (long long)row * p.ldy + col0;
+    for (int c = 0; c < E / 32; ++c) {
+      uint32_t v[32];
+      tmem_ld32(tY + lane_off + c * 32, v);
+      tmem_wait_ld();
+      const int col0 = c * 32;
+      if (!rv || col0 >= p.E) continue;
+      if (p.splits > 1 || p.out_f32) {
+        float* dst = (p.splits > 1) ? p.partial + ((long long)split * p.N + row) * p.E + col0
+                                    : static_cast<float*>(p.y) + (long long)row * p.ldy + col0;
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            if (col0 + 4 * j < p.E)
-              *reinterpret_cast<float4*>(dst + 4 * j) = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
-                                                                    __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
-        } else {
-          __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.y) + (long long)row * p.ldy + col0;
+        for (int j = 0; j < 8; ++j)
+          if (col0 + 4 * j < p.E)
+            *reinterpret_cast<float4*>(dst + 4 * j) = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                                                  __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+      } else {
+        __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.y) + (long long)row * p.ldy + col0;
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (col0 + 8 * j < p.E)
-              *reinterpret_cast<uint4*>(dst + 8 * j) = make_uint4(
-                  pack_bf16(__uint_as_float(v[8 * j]), __uint_as_float(v[8 * j + 1])),
-                  pack_bf16(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3])),
-                  pack_bf16(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5])),
-                  pack_bf16(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7])));
-        }
-      }
-    } else {
-      for (int c = 0; c < E / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(tY + lane_off + c * 32, v);  // keep the warp converged for .sync.aligned
-        tmem_wait_ld();
+        for (int j = 0; j < 4; ++j)
+          if (col0 + 8 * j < p.E)
+            *reinterpret_cast<uint4*>(dst + 8 * j) = make_uint4(
+                pack_bf16(__uint_as_float(v[8 * j]), __uint_as_float(v[8 * j + 1])),
+                pack_bf16(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3])),
+                pack_bf16(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5])),
+                pack_bf16(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7])));
       }
     }
   }

@@ -24,17 +24,32 @@ int sms() {
 int choose_splits(int groups, int M, int requested) {
   if (requested > 0) return std::min(requested, std::max(1, (M + 63) / 64));
   const int by_occupancy = (16 * sms() + groups - 1) / groups;
-  const int by_length = std::max(1, (M + 1023) / 1024);
+  const int by_length = std::max(1, (M + 1023) / 1024);  // >= 16 tiles per split
   return std::max(1, std::min(by_occupancy, by_length));
 }
 
 template <int R>
-int launch(DecodeParams& p, cudaStream_t st) {
+int launch(const nt_decode_args* a, DecodeParams& p, cudaStream_t st) {
+  CUtensorMap mk, mv;
+  int rc;
+  if ((rc = make_map_4d(&mk, a->k.ptr, kDecodeD, a->seq_kv, a->heads_kv, a->batch, a->k.stride_s, a->k.stride_h,
+                        a->k.stride_b, kDecodeTile, 2)))
+    return rc;
+  if ((rc = make_map_4d(&mv, a->v.ptr, kDecodeD, a->seq_kv, a->heads_kv, a->batch, a->v.stride_s, a->v.stride_h,
+                        a->v.stride_b, kDecodeTile, 2)))
+    return rc;
+  auto kern = decode_split_kernel<R>;
+  static bool configured = false;
+  if (!configured) {
+    if ((rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kDecodeSmem),
+                         "cudaFuncSetAttribute(decode)")))
+      return rc;
+    configured = true;
+  }
   dim3 grid(p.splits, p.B * p.Hkv);
-  decode_split_kernel<R><<<grid, kDecodeThreads, 0, st>>>(p);
+  kern<<<grid, kDecodeThreads + 32, kDecodeSmem, st>>>(mk, mv, p);
   g_launches++;
-  int rc = check_cuda(cudaGetLastError(), "decode_split launch");
-  if (rc) return rc;
+  if ((rc = check_cuda(cudaGetLastError(), "decode_split launch"))) return rc;
   const int rows = p.B * p.Hkv * R;
   decode_combine_kernel<<<(rows + 3) / 4, 128, 0, st>>>(p, R);
   g_launches++;
@@ -71,16 +86,17 @@ extern "C" int nt_attn_decode(const nt_decode_args* a, void* stream) {
   p.out_f32 = a->out_dtype == NT_DTYPE_F32;
   p.B = a->batch; p.Hq = a->heads_q; p.Hkv = a->heads_kv; p.Nq = a->seq_q; p.M = a->seq_kv; p.g = g;
   p.scale_log2 = a->scale * 1.4426950408889634f;
-  p.splits = a->num_splits;
-  p.keys_per_split = (a->seq_kv + p.splits - 1) / p.splits;
+  p.splits = std::max(1, a->num_splits);
+  // key ranges are whole 64-key TMA tiles
+  p.keys_per_split = ((a->seq_kv + p.splits - 1) / p.splits + kDecodeTile - 1) / kDecodeTile * kDecodeTile;
   p.ws = static_cast<float*>(a->workspace);
   p.err = a->err_flag;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   switch (R) {
-    case 1: return launch<1>(p, st);
-    case 2: return launch<2>(p, st);
-    case 4: return launch<4>(p, st);
-    default: return launch<8>(p, st);
+    case 1: return launch<1>(a, p, st);
+    case 2: return launch<2>(a, p, st);
+    case 4: return launch<4>(a, p, st);
+    default: return launch<8>(a, p, st);
   }
 }
 

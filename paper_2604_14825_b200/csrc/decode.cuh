@@ -9,10 +9,11 @@
 // O = sum_s O_s 2^(m_s - m) / sum_s l_s 2^(m_s - m)   (tilecc/schedule/repair.py:80-88).
 //
 // The work is 4 flop/byte (GQA ratio 4), far below the tensor-core ridge, so
-// the kernel streams K/V with coalesced 16-byte loads straight into
-// registers (software-pipelined one key step ahead) and does the dots on the
-// FMA pipe: TPK = max(8, 2R) threads share a key (DPT = 128/TPK dims each), the R rows of
-// the group live in registers, partial dots are reduced with shuffles.
+// the kernel is built to stream: a producer warp keeps kDecodeStages K/V tile
+// pairs (64 keys each, swizzle-128B) in flight with TMA, and 128 consumer
+// threads do the dots on the FMA pipe from shared memory -- 16 threads share a
+// key (8 dims = one 16-byte chunk each), the R rows of the group live in
+// registers, partial dots are reduced with shuffles.
 #pragma once
 #include "sm100.cuh"
 
@@ -57,151 +58,177 @@ __device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
   return r;
 }
 
+constexpr int kDecodeTile = 64;    // keys per TMA tile
+constexpr int kDecodeStages = 3;   // K+V tile pairs in flight per CTA
+constexpr int kDecodeTPK = 16;     // threads per key (8 dims = one 16-byte chunk each)
+constexpr int kDecodeKPS = kDecodeThreads / kDecodeTPK;  // keys per consumer step
+constexpr int kDecodePanel = kDecodeTile * 128;          // one 64-dim swizzle-128B panel (8 KB)
+constexpr int kDecodeTileBytes = 2 * kDecodePanel;       // 64 keys x 128 dims bf16 (16 KB)
+constexpr int kDecodeSmem = kDecodeStages * 2 * kDecodeTileBytes + 1024 + 2 * kDecodeStages * 8 + 64;
+
+// One CTA = (split, batch x kv-head group).  Warp 0 streams K/V tiles with TMA into a
+// kDecodeStages-deep ring; warps 1-4 (128 threads) consume them from shared memory.
 template <int R>
-__global__ void __launch_bounds__(kDecodeThreads, 2) decode_split_kernel(const DecodeParams p) {
+__global__ void __launch_bounds__(kDecodeThreads + 32, 2)
+    decode_split_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                        const DecodeParams p) {
   constexpr int D = kDecodeD;
-  constexpr int TPK = (2 * R > 8) ? 2 * R : 8;  // threads per key
-  constexpr int DPT = D / TPK;                  // dims per thread
-  constexpr int KPS = kDecodeThreads / TPK;  // keys per step
-  constexpr int NV = DPT / 8;            // 16-byte vectors per thread per row
-  static_assert(DPT % 8 == 0, "DPT must be a multiple of 8");
-  __shared__ float sm_m[KPS][R];
-  __shared__ float sm_l[KPS][R];
-  __shared__ float sm_o[KPS][R][D];
+  constexpr int TPK = kDecodeTPK, DPT = D / TPK, KPS = kDecodeKPS;
+  static_assert(DPT == 8, "one 16-byte chunk per thread");
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_u32 = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw_u32 + 1023u) & ~1023u) - raw_u32);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kDecodeStages * 2 * kDecodeTileBytes);
+  uint64_t* empty = full + kDecodeStages;
 
   const int s = blockIdx.x;
   const int grp = blockIdx.y;  // b * Hkv + hkv
   const int b = grp / p.Hkv, hkv = grp % p.Hkv;
-  const int t = threadIdx.x;
-  const int kg = t / TPK, ds = t % TPK;
-  const int d0 = ds * DPT;
-
-  float q[R][DPT];
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int h = hkv * p.g + r / p.Nq, n = r % p.Nq;
-    const __nv_bfloat16* qp = p.q + b * p.q_sb + h * p.q_sh + n * p.q_sn + d0;
-#pragma unroll
-    for (int i = 0; i < NV; ++i) bf16x8_to_f32(*reinterpret_cast<const uint4*>(qp + 8 * i), &q[r][8 * i]);
-#pragma unroll
-    for (int i = 0; i < DPT; ++i) q[r][i] *= p.scale_log2;  // fold c*log2e into q
-  }
-  float o[R][DPT];
-  float m[R], l[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    m[r] = __int_as_float(0xff800000);
-    l[r] = 0.f;
-#pragma unroll
-    for (int i = 0; i < DPT; ++i) o[r][i] = 0.f;
-  }
-
-  const int j0 = s * p.keys_per_split;
+  const int warp = __shfl_sync(0xffffffffu, threadIdx.x / 32, 0);
+  const int lane = threadIdx.x & 31;
+  const int j0 = s * p.keys_per_split;  // multiple of kDecodeTile
   const int j1 = min(p.M, j0 + p.keys_per_split);
-  const __nv_bfloat16* kbase = p.k + b * p.k_sb + hkv * p.k_sh + d0;
-  const __nv_bfloat16* vbase = p.v + b * p.v_sb + hkv * p.v_sh + d0;
+  const int ntiles = (j1 > j0) ? (j1 - j0 + kDecodeTile - 1) / kDecodeTile : 0;
 
-  // warp-uniform trip count: every lane runs every step (the TPK-lane shuffles
-  // below need all lanes of the warp); out-of-range keys contribute nothing.
-  const int nsteps = (j1 > j0) ? (j1 - j0 + KPS - 1) / KPS : 0;
-  uint4 kc[NV], vc[NV];
-  {
-    const int j = j0 + kg;
-    const bool ok = j < j1;
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      kc[i] = ok ? ldg_nc_v4(kbase + (long long)j * p.k_sn + 8 * i) : make_uint4(0, 0, 0, 0);
-      vc[i] = ok ? ldg_nc_v4(vbase + (long long)j * p.v_sn + 8 * i) : make_uint4(0, 0, 0, 0);
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmK);
+    prefetch_tmap(&tmV);
+    for (int i = 0; i < kDecodeStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 4);
     }
+    fence_barrier_init();
   }
-  for (int st = 0; st < nsteps; ++st) {
-    const int j = j0 + st * KPS + kg;
-    const bool valid = j < j1;
-    // prefetch the next key of this group (one step ahead)
-    uint4 kn[NV], vn[NV];
-    const int jn = j + KPS;
-    const bool okn = jn < j1;
+  __syncthreads();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int t = 0; t < ntiles; ++t) {
+        const int slot = t % kDecodeStages;
+        mbar_wait(&empty[slot], ((t / kDecodeStages) & 1) ^ 1, p.err, 11);
+        mbar_arrive_expect_tx(&full[slot], 2 * kDecodeTileBytes);
+        uint8_t* sk = smem + slot * 2 * kDecodeTileBytes;
+        uint8_t* sv = sk + kDecodeTileBytes;
+        const int row = j0 + t * kDecodeTile;
 #pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      kn[i] = okn ? ldg_nc_v4(kbase + (long long)jn * p.k_sn + 8 * i) : make_uint4(0, 0, 0, 0);
-      vn[i] = okn ? ldg_nc_v4(vbase + (long long)jn * p.v_sn + 8 * i) : make_uint4(0, 0, 0, 0);
+        for (int h = 0; h < 2; ++h) {
+          tma_load_4d(sk + h * kDecodePanel, &tmK, &full[slot], h * 64, row, hkv, b);
+          tma_load_4d(sv + h * kDecodePanel, &tmV, &full[slot], h * 64, row, hkv, b);
+        }
+      }
     }
-    float kf[DPT], vf[DPT];
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      bf16x8_to_f32(kc[i], &kf[8 * i]);
-      bf16x8_to_f32(vc[i], &vf[8 * i]);
-    }
-    float sc[R];
+  } else {
+    const int tc = threadIdx.x - 32;
+    const int kg = tc / TPK, ds = tc % TPK;
+    const int d0 = ds * DPT;
+    const int panel = d0 / 64, chunk = (d0 % 64) / 8;
+
+    float q[R][DPT];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      float a0 = 0.f, a1 = 0.f;
+      const int h = hkv * p.g + r / p.Nq, n = r % p.Nq;
+      const __nv_bfloat16* qp = p.q + b * p.q_sb + h * p.q_sh + n * p.q_sn + d0;
+      bf16x8_to_f32(*reinterpret_cast<const uint4*>(qp), q[r]);
 #pragma unroll
-      for (int i = 0; i < DPT; i += 2) {
-        a0 = fmaf(q[r][i], kf[i], a0);
-        a1 = fmaf(q[r][i + 1], kf[i + 1], a1);
-      }
-      sc[r] = a0 + a1;
+      for (int i = 0; i < DPT; ++i) q[r][i] *= p.scale_log2;  // fold c*log2e into q
     }
+    float o[R][DPT], m[R], l[R];
 #pragma unroll
-    for (int off = 1; off < TPK; off <<= 1)
+    for (int r = 0; r < R; ++r) {
+      m[r] = __int_as_float(0xff800000);
+      l[r] = 0.f;
 #pragma unroll
-      for (int r = 0; r < R; ++r) sc[r] += __shfl_xor_sync(0xffffffffu, sc[r], off);
-    if (valid) {
+      for (int i = 0; i < DPT; ++i) o[r][i] = 0.f;
+    }
+
+    for (int t = 0; t < ntiles; ++t) {
+      const int slot = t % kDecodeStages;
+      mbar_wait(&full[slot], (t / kDecodeStages) & 1, p.err, 12);
+      const uint8_t* sk = smem + slot * 2 * kDecodeTileBytes + panel * kDecodePanel;
+      const uint8_t* sv = sk + kDecodeTileBytes;
+#pragma unroll 2
+      for (int u = 0; u < kDecodeTile / KPS; ++u) {
+        const int kr = u * KPS + kg;
+        const bool valid = j0 + t * kDecodeTile + kr < j1;
+        const int off = kr * 128 + ((chunk ^ (kr & 7)) << 4);
+        const uint4 kv = *reinterpret_cast<const uint4*>(sk + off);
+        const uint4 vv = *reinterpret_cast<const uint4*>(sv + off);
+        float kf[DPT], vf[DPT];
+        bf16x8_to_f32(kv, kf);
+        bf16x8_to_f32(vv, vf);
+        float sc[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+          for (int i = 0; i < DPT; i += 2) {
+            a0 = fmaf(q[r][i], kf[i], a0);
+            a1 = fmaf(q[r][i + 1], kf[i + 1], a1);
+          }
+          sc[r] = a0 + a1;
+        }
+#pragma unroll
+        for (int offx = 1; offx < TPK; offx <<= 1)
+#pragma unroll
+          for (int r = 0; r < R; ++r) sc[r] += __shfl_xor_sync(0xffffffffu, sc[r], offx);
+        if (valid) {
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            if (sc[r] > m[r] + 8.0f) {  // lazy rescale (exact identity; keeps p <= 2^8)
+              const float alpha = ex2(m[r] - sc[r]);
+              l[r] *= alpha;
+#pragma unroll
+              for (int i = 0; i < DPT; ++i) o[r][i] *= alpha;
+              m[r] = sc[r];
+            }
+            const float pr = ex2(sc[r] - m[r]);
+            l[r] += pr;
+#pragma unroll
+            for (int i = 0; i < DPT; ++i) o[r][i] = fmaf(pr, vf[i], o[r][i]);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+    }
+
+    // ---- merge the KPS key groups of this CTA (the ring is dead now: reuse it)
+    named_bar_sync(1, kDecodeThreads);
+    float* sm_m = reinterpret_cast<float*>(smem);            // [KPS][R]
+    float* sm_l = sm_m + KPS * R;                             // [KPS][R]
+    float* sm_o = sm_l + KPS * R;                             // [KPS][R][D]
+    if (ds == 0) {
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        if (sc[r] > m[r] + 8.0f) {  // lazy rescale (exact identity; keeps p <= 2^8)
-          const float alpha = ex2(m[r] - sc[r]);
-          l[r] *= alpha;
+        sm_m[kg * R + r] = m[r];
+        sm_l[kg * R + r] = l[r];
+      }
+    }
 #pragma unroll
-          for (int i = 0; i < DPT; ++i) o[r][i] *= alpha;
-          m[r] = sc[r];
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int i = 0; i < DPT; ++i) sm_o[(kg * R + r) * D + d0 + i] = o[r][i];
+    named_bar_sync(1, kDecodeThreads);
+    float* ws = p.ws + ((long long)grp * p.splits + s) * R * (D + 2);
+    for (int idx = tc; idx < R * D; idx += kDecodeThreads) {
+      const int r = idx / D, d = idx % D;
+      float mm = __int_as_float(0xff800000);
+#pragma unroll
+      for (int c = 0; c < KPS; ++c) mm = fmaxf(mm, sm_m[c * R + r]);
+      float ll = 0.f, oo = 0.f;
+      if (mm != __int_as_float(0xff800000)) {
+#pragma unroll
+        for (int c = 0; c < KPS; ++c) {
+          const float w = ex2(sm_m[c * R + r] - mm);
+          ll = fmaf(sm_l[c * R + r], w, ll);
+          oo = fmaf(sm_o[(c * R + r) * D + d], w, oo);
         }
-        const float pr = ex2(sc[r] - m[r]);
-        l[r] += pr;
-#pragma unroll
-        for (int i = 0; i < DPT; ++i) o[r][i] = fmaf(pr, vf[i], o[r][i]);
       }
-    }
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      kc[i] = kn[i];
-      vc[i] = vn[i];
-    }
-  }
-
-  // ---- merge the KPS key groups of this CTA
-  if (ds == 0) {
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      sm_m[kg][r] = m[r];
-      sm_l[kg][r] = l[r];
-    }
-  }
-#pragma unroll
-  for (int r = 0; r < R; ++r)
-#pragma unroll
-    for (int i = 0; i < DPT; ++i) sm_o[kg][r][d0 + i] = o[r][i];
-  __syncthreads();
-  float* ws = p.ws + ((long long)grp * p.splits + s) * R * (D + 2);
-  for (int idx = t; idx < R * D; idx += kDecodeThreads) {
-    const int r = idx / D, d = idx % D;
-    float mm = __int_as_float(0xff800000);
-#pragma unroll 4
-    for (int c = 0; c < KPS; ++c) mm = fmaxf(mm, sm_m[c][r]);
-    float ll = 0.f, oo = 0.f;
-    if (mm != __int_as_float(0xff800000)) {
-#pragma unroll 4
-      for (int c = 0; c < KPS; ++c) {
-        const float w = ex2(sm_m[c][r] - mm);
-        ll = fmaf(sm_l[c][r], w, ll);
-        oo = fmaf(sm_o[c][r][d], w, oo);
+      ws[r * (D + 2) + d] = oo;
+      if (d == 0) {
+        ws[r * (D + 2) + D] = mm;
+        ws[r * (D + 2) + D + 1] = ll;
       }
-    }
-    ws[r * (D + 2) + d] = oo;
-    if (d == 0) {
-      ws[r * (D + 2) + D] = mm;
-      ws[r * (D + 2) + D + 1] = ll;
     }
   }
 }
