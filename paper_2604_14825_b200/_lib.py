@@ -12,7 +12,8 @@ import threading
 
 from .errors import NativeLibraryMissing, raise_for_status
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_native", "libnautilus_b200.so")
+LIB_PATH = os.environ.get("NT_LIB_PATH") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "_native", "libnautilus_b200.so")
 
 NT_MASK_NONE, NT_MASK_CAUSAL, NT_MASK_TENSOR = 0, 1, 2
 NT_DTYPE_BF16, NT_DTYPE_F32 = 0, 1

@@ -49,37 +49,42 @@ def _mtime(p):
     return os.path.getmtime(p) if os.path.exists(p) else 0.0
 
 
-def _compile(src: str, force: bool) -> tuple[str, str]:
-    obj = os.path.join(OBJ_DIR, os.path.basename(src).replace(".cu", ".o"))
+def _compile(src: str, force: bool, defines=(), obj_dir=OBJ_DIR) -> tuple[str, str]:
+    obj = os.path.join(obj_dir, os.path.basename(src).replace(".cu", ".o"))
     newest_dep = max([_mtime(src)] + [_mtime(h) for h in headers()])
     if not force and _mtime(obj) > newest_dep:
         return obj, ""
-    cmd = [nvcc()] + ARCH + FLAGS + ["-c", src, "-o", obj]
+    cmd = [nvcc()] + ARCH + FLAGS + ["-D" + d for d in defines] + ["-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
     return obj, r.stderr
 
 
-def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -> str:
-    os.makedirs(OBJ_DIR, exist_ok=True)
+def build(force: bool = False, jobs: int | None = None, verbose: bool = False, defines=(),
+          out: str | None = None) -> str:
+    """Build the library; `defines`/`out` build an experiment variant (e.g. NT_POLY_EVERY=0)."""
+    lib = out or LIB
+    obj_dir = OBJ_DIR if not defines else os.path.join(OUT_DIR, "obj_" + "_".join(
+        d.replace("=", "") for d in defines))
+    os.makedirs(obj_dir, exist_ok=True)
     srcs = sources()
     jobs = jobs or min(len(srcs), os.cpu_count() or 4)
     with cf.ThreadPoolExecutor(jobs) as ex:
-        results = list(ex.map(lambda s: _compile(s, force), srcs))
+        results = list(ex.map(lambda s: _compile(s, force, defines, obj_dir), srcs))
     objs = [o for o, _ in results]
     if verbose:
         for _, log in results:
             if log:
                 print(log, file=sys.stderr)
-    if force or not os.path.exists(LIB) or _mtime(LIB) < max(_mtime(o) for o in objs):
+    if force or not os.path.exists(lib) or _mtime(lib) < max(_mtime(o) for o in objs):
         # static cudart; the driver API (cuTensorMapEncodeTiled) is resolved at run
         # time through cudaGetDriverEntryPoint, so libcuda is not a link dependency
-        cmd = [nvcc()] + ARCH + ["-shared", "-o", LIB] + objs
+        cmd = [nvcc()] + ARCH + ["-shared", "-o", lib] + objs
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    return LIB
+    return lib
 
 
 def main():
@@ -87,8 +92,11 @@ def main():
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--jobs", type=int, default=None)
     ap.add_argument("-v", "--verbose", action="store_true")
+    ap.add_argument("-D", "--define", action="append", default=[])
+    ap.add_argument("--out", default=None)
     a = ap.parse_args()
-    print(build(a.force, a.jobs, a.verbose))
+    out = os.path.join(OUT_DIR, a.out) if a.out else None
+    print(build(a.force, a.jobs, a.verbose, tuple(a.define), out))
 
 
 if __name__ == "__main__":

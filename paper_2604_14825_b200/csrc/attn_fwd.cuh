@@ -54,6 +54,11 @@ struct AttnFwdParams {
 
 constexpr int kAttnThreads = 384;
 constexpr float kRescaleLog2 = 8.0f;
+#ifndef NT_POLY_EVERY
+#define NT_POLY_EVERY 4
+#endif
+constexpr bool kPolyExp = NT_POLY_EVERY > 0;
+constexpr int kPolyEvery = NT_POLY_EVERY > 0 ? NT_POLY_EVERY : 1;
 
 template <int D>
 struct AttnCfg {
@@ -253,9 +258,21 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             if (kv0 + c > lim) s[c] = __float_as_uint(NINF);
         }
       }
-      float mx = __uint_as_float(s[0]);
+      float mx;
+      {
+        // tree max with 3-input FMNMX3, 4 independent chains
+        float a0 = __uint_as_float(s[0]), a1 = __uint_as_float(s[1]);
+        float a2 = __uint_as_float(s[2]), a3 = __uint_as_float(s[3]);
 #pragma unroll
-      for (int c = 1; c < 128; ++c) mx = fmaxf(mx, __uint_as_float(s[c]));
+        for (int c = 4; c < 128; c += 8) {
+          a0 = fmax3(a0, __uint_as_float(s[c]), __uint_as_float(s[c + 1]));
+          a1 = fmax3(a1, __uint_as_float(s[c + 2]), __uint_as_float(s[c + 3]));
+          a2 = fmax3(a2, __uint_as_float(s[c + 4]), __uint_as_float(s[c + 5]));
+          if (c + 7 < 128) a3 = fmax3(a3, __uint_as_float(s[c + 6]), __uint_as_float(s[c + 7]));
+          else a3 = fmaxf(a3, __uint_as_float(s[c + 6]));
+        }
+        mx = fmaxf(fmax3(a0, a1, a2), a3);
+      }
       const float m_new = fmaxf(m_run, mx * sc);
       const bool need = m_new > m_run + kRescaleLog2;
       if (__any_sync(0xffffffffu, need)) {
@@ -275,19 +292,28 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         m_run = m_new;
       }
       const float m_use = (m_run == NINF) ? 0.f : m_run;
-      float sum = 0.f;
+      const float2 sc2 = make_float2(sc, sc);
+      const float2 nm2 = make_float2(-m_use, -m_use);
+      float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
       for (int ch = 0; ch < 4; ++ch) {
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const float p0 = ex2(fmaf(__uint_as_float(s[ch * 32 + 2 * i]), sc, -m_use));
-          const float p1 = ex2(fmaf(__uint_as_float(s[ch * 32 + 2 * i + 1]), sc, -m_use));
-          sum += p0 + p1;
-          pk[i] = pack_bf16(p0, p1);
+          const float2 x = ffma2(make_float2(__uint_as_float(s[ch * 32 + 2 * i]),
+                                             __uint_as_float(s[ch * 32 + 2 * i + 1])), sc2, nm2);
+          float2 e;
+          if (kPolyExp && (i % kPolyEvery) == kPolyEvery - 1) {
+            e = ex2_poly2(x);  // FMA-pipe exp2 for 1/kPolyEvery of the pairs
+          } else {
+            e = make_float2(ex2(x.x), ex2(x.y));
+          }
+          sum2[i & 1] = fadd2(sum2[i & 1], e);
+          pk[i] = pack_bf16(e.x, e.y);
         }
         tmem_st16(tS + ch * 16, pk);
       }
+      const float sum = (sum2[0].x + sum2[0].y) + (sum2[1].x + sum2[1].y);
       l_run += sum;
       tmem_wait_st();
       tc_fence_before();

@@ -23,7 +23,7 @@ int sms() {
 
 int choose_splits(int groups, int M, int requested) {
   if (requested > 0) return std::min(requested, std::max(1, (M + 63) / 64));
-  const int by_occupancy = (16 * sms() + groups - 1) / groups;
+  const int by_occupancy = (8 * sms() + groups - 1) / groups;  // ~8 waves of 1-CTA/SM
   const int by_length = std::max(1, (M + 1023) / 1024);  // >= 16 tiles per split
   return std::max(1, std::min(by_occupancy, by_length));
 }
@@ -47,7 +47,7 @@ int launch(const nt_decode_args* a, DecodeParams& p, cudaStream_t st) {
     configured = true;
   }
   dim3 grid(p.splits, p.B * p.Hkv);
-  kern<<<grid, kDecodeThreads + 32, kDecodeSmem, st>>>(mk, mv, p);
+  kern<<<grid, kDecodeCTAThreads, kDecodeSmem, st>>>(mk, mv, p);
   g_launches++;
   if ((rc = check_cuda(cudaGetLastError(), "decode_split launch"))) return rc;
   const int rows = p.B * p.Hkv * R;

@@ -10,10 +10,10 @@
 //
 // The work is 4 flop/byte (GQA ratio 4), far below the tensor-core ridge, so
 // the kernel is built to stream: a producer warp keeps kDecodeStages K/V tile
-// pairs (64 keys each, swizzle-128B) in flight with TMA, and 128 consumer
-// threads do the dots on the FMA pipe from shared memory -- 16 threads share a
-// key (8 dims = one 16-byte chunk each), the R rows of the group live in
-// registers, partial dots are reduced with shuffles.
+// pairs (64 keys each, swizzle-128B) in flight with TMA, and 256 consumer
+// threads do the dots on the FMA pipe from shared memory -- 8 (R < 8) or 16
+// threads share a key, the R rows of the group live in registers, partial
+// dots are reduced with shuffles.
 #pragma once
 #include "sm100.cuh"
 
@@ -59,22 +59,30 @@ __device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
 }
 
 constexpr int kDecodeTile = 64;    // keys per TMA tile
-constexpr int kDecodeStages = 3;   // K+V tile pairs in flight per CTA
-constexpr int kDecodeTPK = 16;     // threads per key (8 dims = one 16-byte chunk each)
-constexpr int kDecodeKPS = kDecodeThreads / kDecodeTPK;  // keys per consumer step
+constexpr int kDecodeStages = 6;   // K+V tile pairs in flight per CTA (192 KB)
+constexpr int kDecodeConsumers = 256;                    // 8 consumer warps (warpgroups 1-2)
+constexpr int kDecodeCTAThreads = 128 + kDecodeConsumers;  // warpgroup 0: TMA producer + 3 idle warps
 constexpr int kDecodePanel = kDecodeTile * 128;          // one 64-dim swizzle-128B panel (8 KB)
 constexpr int kDecodeTileBytes = 2 * kDecodePanel;       // 64 keys x 128 dims bf16 (16 KB)
 constexpr int kDecodeSmem = kDecodeStages * 2 * kDecodeTileBytes + 1024 + 2 * kDecodeStages * 8 + 64;
+template <int R>
+struct DecodeShape {
+  static constexpr int TPK = (R >= 8) ? 16 : 8;  // threads per key
+  static constexpr int DPT = kDecodeD / TPK;      // dims per thread (16 or 8)
+  static constexpr int NCH = DPT / 8;             // 16-byte chunks per thread per row
+  static constexpr int KPS = kDecodeConsumers / TPK;  // keys per consumer step
+};
 
 // One CTA = (split, batch x kv-head group).  Warp 0 streams K/V tiles with TMA into a
-// kDecodeStages-deep ring; warps 1-4 (128 threads) consume them from shared memory.
+// kDecodeStages-deep ring; warpgroups 1-2 (256 threads) consume them from shared memory.
+// setmaxnreg moves the idle registers of warpgroup 0 to the consumers.
 template <int R>
-__global__ void __launch_bounds__(kDecodeThreads + 32, 2)
+__global__ void __launch_bounds__(kDecodeCTAThreads, 1)
     decode_split_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                         const DecodeParams p) {
   constexpr int D = kDecodeD;
-  constexpr int TPK = kDecodeTPK, DPT = D / TPK, KPS = kDecodeKPS;
-  static_assert(DPT == 8, "one 16-byte chunk per thread");
+  using SH = DecodeShape<R>;
+  constexpr int TPK = SH::TPK, DPT = SH::DPT, KPS = SH::KPS, NCH = SH::NCH;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_u32 = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_u32 + 1023u) & ~1023u) - raw_u32);
@@ -95,14 +103,15 @@ __global__ void __launch_bounds__(kDecodeThreads + 32, 2)
     prefetch_tmap(&tmV);
     for (int i = 0; i < kDecodeStages; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 4);
+      mbar_init(&empty[i], kDecodeConsumers / 32);
     }
     fence_barrier_init();
   }
   __syncthreads();
 
-  if (warp == 0) {
-    if (lane == 0) {
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
+    if (warp == 0 && lane == 0) {
       for (int t = 0; t < ntiles; ++t) {
         const int slot = t % kDecodeStages;
         mbar_wait(&empty[slot], ((t / kDecodeStages) & 1) ^ 1, p.err, 11);
@@ -118,7 +127,8 @@ __global__ void __launch_bounds__(kDecodeThreads + 32, 2)
       }
     }
   } else {
-    const int tc = threadIdx.x - 32;
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;");
+    const int tc = threadIdx.x - 128;
     const int kg = tc / TPK, ds = tc % TPK;
     const int d0 = ds * DPT;
     const int panel = d0 / 64, chunk = (d0 % 64) / 8;
@@ -128,7 +138,8 @@ __global__ void __launch_bounds__(kDecodeThreads + 32, 2)
     for (int r = 0; r < R; ++r) {
       const int h = hkv * p.g + r / p.Nq, n = r % p.Nq;
       const __nv_bfloat16* qp = p.q + b * p.q_sb + h * p.q_sh + n * p.q_sn + d0;
-      bf16x8_to_f32(*reinterpret_cast<const uint4*>(qp), q[r]);
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) bf16x8_to_f32(*reinterpret_cast<const uint4*>(qp + 8 * c), &q[r][8 * c]);
 #pragma unroll
       for (int i = 0; i < DPT; ++i) q[r][i] *= p.scale_log2;  // fold c*log2e into q
     }
@@ -150,12 +161,13 @@ __global__ void __launch_bounds__(kDecodeThreads + 32, 2)
       for (int u = 0; u < kDecodeTile / KPS; ++u) {
         const int kr = u * KPS + kg;
         const bool valid = j0 + t * kDecodeTile + kr < j1;
-        const int off = kr * 128 + ((chunk ^ (kr & 7)) << 4);
-        const uint4 kv = *reinterpret_cast<const uint4*>(sk + off);
-        const uint4 vv = *reinterpret_cast<const uint4*>(sv + off);
         float kf[DPT], vf[DPT];
-        bf16x8_to_f32(kv, kf);
-        bf16x8_to_f32(vv, vf);
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+          const int off = kr * 128 + (((chunk + c) ^ (kr & 7)) << 4);
+          bf16x8_to_f32(*reinterpret_cast<const uint4*>(sk + off), &kf[8 * c]);
+          bf16x8_to_f32(*reinterpret_cast<const uint4*>(sv + off), &vf[8 * c]);
+        }
         float sc[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -193,7 +205,7 @@ __global__ void __launch_bounds__(kDecodeThreads + 32, 2)
     }
 
     // ---- merge the KPS key groups of this CTA (the ring is dead now: reuse it)
-    named_bar_sync(1, kDecodeThreads);
+    named_bar_sync(1, kDecodeConsumers);
     float* sm_m = reinterpret_cast<float*>(smem);            // [KPS][R]
     float* sm_l = sm_m + KPS * R;                             // [KPS][R]
     float* sm_o = sm_l + KPS * R;                             // [KPS][R][D]
@@ -208,9 +220,9 @@ __global__ void __launch_bounds__(kDecodeThreads + 32, 2)
     for (int r = 0; r < R; ++r)
 #pragma unroll
       for (int i = 0; i < DPT; ++i) sm_o[(kg * R + r) * D + d0 + i] = o[r][i];
-    named_bar_sync(1, kDecodeThreads);
+    named_bar_sync(1, kDecodeConsumers);
     float* ws = p.ws + ((long long)grp * p.splits + s) * R * (D + 2);
-    for (int idx = tc; idx < R * D; idx += kDecodeThreads) {
+    for (int idx = tc; idx < R * D; idx += kDecodeConsumers) {
       const int r = idx / D, d = idx % D;
       float mm = __int_as_float(0xff800000);
 #pragma unroll

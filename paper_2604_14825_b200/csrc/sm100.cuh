@@ -235,4 +235,51 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return r;
 }
 
+// three-input max (FMNMX3)
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+// packed fp32x2 arithmetic (FFMA2 / FADD2)
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+// 2^x for a pair on the FMA pipe (offloads the MUFU): x = j + f, j = rint(x),
+// f in [-0.5, 0.5], 2^f by a degree-3 minimax polynomial (max rel. err 7.5e-5,
+// far below the bf16 rounding P gets next), 2^j added to the exponent bits.
+// x is clamped at -127 (masked -inf entries give ~1e-38 instead of 0).
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  const float2 magic = make_float2(12582912.0f, 12582912.0f);  // 1.5 * 2^23
+  x.x = fmaxf(x.x, -127.0f);
+  x.y = fmaxf(x.y, -127.0f);
+  const float2 t = fadd2(x, magic);
+  const float2 j = fadd2(t, make_float2(-12582912.0f, -12582912.0f));
+  const float2 f = ffma2(j, make_float2(-1.0f, -1.0f), x);
+  float2 q = ffma2(f, make_float2(0.05517161637544632f, 0.05517161637544632f),
+                   make_float2(0.24261116981506348f, 0.24261116981506348f));
+  q = ffma2(q, f, make_float2(0.6932610273361206f, 0.6932610273361206f));
+  q = ffma2(q, f, make_float2(0.9999280571937561f, 0.9999280571937561f));
+  // low mantissa bits of t hold j (two's complement); shifting them into the
+  // exponent field adds j to the exponent of q
+  const uint32_t r0 = __float_as_uint(q.x) + (__float_as_uint(t.x) << 23);
+  const uint32_t r1 = __float_as_uint(q.y) + (__float_as_uint(t.y) << 23);
+  return make_float2(__uint_as_float(r0), __uint_as_float(r1));
+}
+
 }  // namespace nt
