@@ -263,11 +263,12 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
 // 2^x for a pair on the FMA pipe (offloads the MUFU): x = j + f, j = rint(x),
 // f in [-0.5, 0.5], 2^f by a degree-3 minimax polynomial (max rel. err 7.5e-5,
 // far below the bf16 rounding P gets next), 2^j added to the exponent bits.
-// x is clamped at -127 (masked -inf entries give ~1e-38 instead of 0).
+// x is clamped at -126 so the exponent add cannot wrap below the denormal
+// range (masked -inf entries give ~1e-38 instead of 0).
 __device__ __forceinline__ float2 ex2_poly2(float2 x) {
   const float2 magic = make_float2(12582912.0f, 12582912.0f);  // 1.5 * 2^23
-  x.x = fmaxf(x.x, -127.0f);
-  x.y = fmaxf(x.y, -127.0f);
+  x.x = fmaxf(x.x, -126.0f);
+  x.y = fmaxf(x.y, -126.0f);
   const float2 t = fadd2(x, magic);
   const float2 j = fadd2(t, make_float2(-12582912.0f, -12582912.0f));
   const float2 f = ffma2(j, make_float2(-1.0f, -1.0f), x);

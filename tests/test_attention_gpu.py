@@ -160,3 +160,14 @@ def test_llama_8k_causal_two_heads_vs_fp64():
     got = _run_batched(q, k, v, scale, True)
     ref = reference_math.attention_batched_fp64(q, k, v, scale, True)
     _check(got, ref)
+
+
+def test_exp2_poly_no_nan_on_masked_tiles():
+    """Causal rows with long fully-masked spans (exercise the polynomial exp2 clamp)."""
+    B, Hq, Hkv, N, D = 1, 1, 1, 640, 128
+    q = _rand((B, Hq, N, D), 31, 3.0)  # large logits -> wide exponent range
+    k = _rand((B, Hkv, N, D), 32, 3.0)
+    v = _rand((B, Hkv, N, D), 33)
+    got = _run_batched(q, k, v, 0.08838834764831845, True)
+    ref = reference_math.attention_batched_fp64(q, k, v, 0.08838834764831845, True)
+    _check(got, ref)
