@@ -54,8 +54,12 @@ struct AttnFwdParams {
 
 constexpr int kAttnThreads = 384;
 constexpr float kRescaleLog2 = 8.0f;
+// Fraction of exp2 evaluated by the FMA-pipe polynomial instead of MUFU.EX2
+// (1 in NT_POLY_EVERY pairs; 0 = MUFU only).  Measured on B200 at Llama 8K
+// causal: 0 -> 1177, 8 -> 1163, 4 -> 1157, 2 -> 1107 TFLOP/s (profiles/), so
+// the MUFU is not the binding pipe of this kernel yet: off by default.
 #ifndef NT_POLY_EVERY
-#define NT_POLY_EVERY 4
+#define NT_POLY_EVERY 0
 #endif
 constexpr bool kPolyExp = NT_POLY_EVERY > 0;
 constexpr int kPolyEvery = NT_POLY_EVERY > 0 ? NT_POLY_EVERY : 1;

@@ -264,9 +264,10 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
 // f in [-0.5, 0.5], 2^f by a degree-3 minimax polynomial (max rel. err 7.5e-5,
 // far below the bf16 rounding P gets next), 2^j added to the exponent bits.
 // x is clamped at -126 so the exponent add cannot wrap below the denormal
-// range (masked -inf entries give ~1e-38 instead of 0).
+// range; inputs below -126 (masked -inf entries) return exactly 0.
 __device__ __forceinline__ float2 ex2_poly2(float2 x) {
   const float2 magic = make_float2(12582912.0f, 12582912.0f);  // 1.5 * 2^23
+  const bool z0 = x.x < -126.0f, z1 = x.y < -126.0f;  // exp2 underflows: exact 0 (masked -inf)
   x.x = fmaxf(x.x, -126.0f);
   x.y = fmaxf(x.y, -126.0f);
   const float2 t = fadd2(x, magic);
@@ -280,7 +281,7 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
   // exponent field adds j to the exponent of q
   const uint32_t r0 = __float_as_uint(q.x) + (__float_as_uint(t.x) << 23);
   const uint32_t r1 = __float_as_uint(q.y) + (__float_as_uint(t.y) << 23);
-  return make_float2(__uint_as_float(r0), __uint_as_float(r1));
+  return make_float2(z0 ? 0.f : __uint_as_float(r0), z1 ? 0.f : __uint_as_float(r1));
 }
 
 }  // namespace nt
