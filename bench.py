@@ -322,17 +322,10 @@ def cpu_binding(cfg):
 
 
 def shard(cfg, rank, world):
-    """(b0, b1, h0, h1) kv-group range of this rank: batch split if possible, else kv heads."""
-    B, Hkv = cfg["B"], cfg["Hkv"]
-    if world == 1:
-        return 0, B, 0, Hkv
-    if B % world == 0:
-        n = B // world
-        return rank * n, (rank + 1) * n, 0, Hkv
-    if Hkv % world == 0:
-        n = Hkv // world
-        return 0, B, rank * n, (rank + 1) * n
-    raise SystemExit(f"cannot shard B={B}, Hkv={Hkv} over {world} GPUs")
+    """(b0, b1, h0, h1) kv-group range of this rank (paper_2604_14825_b200.shard.plan_shard)."""
+    from paper_2604_14825_b200.shard import plan_shard
+    sh = plan_shard(cfg["B"], cfg["Hkv"], world, rank)
+    return sh.b0, sh.b1, sh.h0, sh.h1
 
 
 def build_workload(cfg, spec, rank, world, dev):

@@ -13,6 +13,9 @@ keep working unchanged.
 from __future__ import annotations
 
 try:  # pragma: no cover - depends on the environment
+    from .frontdoor import import_tilecc as _import_tilecc
+
+    _import_tilecc()  # sys.path or baseline/_ref
     from tilecc.errors import CompilerError as _RefCompilerError
     from tilecc.errors import OutOfBounds as _RefOutOfBounds
     from tilecc.numerics import DivisionByZero as _RefDivisionByZero

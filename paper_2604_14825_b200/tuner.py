@@ -1,0 +1,273 @@
+"""On-device tuner measurement, spread over GPUs (north-star subsystem 3).
+
+Reference: ``score`` / ``search`` (tilecc/tuner/tuner.py:123-206).  A
+reference "measurement" is the analytic ``cost_model`` of the full-size MA
+(+inf if ``check_capacity`` fails) plus the probe-size ``interpret_ma`` step
+count as tie-breaker.  Here:
+
+* ``DeviceScorer`` keeps ``score``'s signature
+  ``(base_full, base_probe, schedule, assignment, device) -> (cost, proxy)``:
+  the candidate is replayed and lowered by the reference pipeline exactly as
+  in ``score`` (tilecc/tuner/tuner.py:129-131), recognised, and its sm_100a
+  realisation is *timed on the GPU* (CUDA events, median of reps, µs).  The
+  proxy is the probe module's step count, which equals interpret_ma's
+  ``steps`` (static closed form, tilecc/ma/cost.py:66-104) -- no CPU
+  interpretation.  Timings are cached per realisation (identical kernels are
+  timed once; the reference re-measures duplicates).
+* ``search`` restates tilecc's evolutionary loop with a pluggable *batch*
+  scorer.  The RNG is consumed only when the population is built and mutated
+  (tilecc/tuner/tuner.py:166-171, 196-202), never while scoring, so scoring a
+  generation's candidates in parallel and appending them in list order
+  reproduces the sequential candidate sequence exactly.
+* ``GPUPoolScorer`` scores a batch on N GPUs with one worker process per GPU.
+"""
+
+from __future__ import annotations
+
+import json
+import math
+import random
+import statistics
+from typing import Callable, Optional, Sequence
+
+from . import cost, ma_ir
+from .frontdoor import import_tilecc
+from .recognize import AttentionSpec, GemmChainSpec, recognize
+
+
+def _lower(base, schedule, assignment, device):
+    """Replay + lower exactly as tilecc.tuner.tuner.score does (tuner.py:129-131)."""
+    from tilecc.ma.lower import lower_to_ma
+    from tilecc.schedule.replay import apply_schedule
+    from tilecc.vr.lower import lower_to_vr
+    from tilecc.vr.rewrite import rewrite
+
+    scalar = apply_schedule(base, schedule, assignment)
+    vr, _ = rewrite(lower_to_vr(scalar))
+    return lower_to_ma(vr, device)
+
+
+def realisation_key(spec, outer, mask_kind) -> tuple:
+    """Fields that determine the sm_100a launch (MA tile sizes do not: the GPU tile is fixed)."""
+    if isinstance(spec, AttentionSpec):
+        return ("attn", spec.n, spec.m, spec.d, spec.scale, spec.mask is not None, mask_kind, outer)
+    if isinstance(spec, GemmChainSpec):
+        return ("chain", spec.n, spec.k, spec.f, spec.e)
+    return (type(spec).__name__,)
+
+
+class DeviceScorer:
+    """Drop-in for tilecc.tuner.tuner.score that times candidates on a B200."""
+
+    def __init__(self, outer: Optional[tuple] = None, mask_kind: str = "auto", reps: int = 7,
+                 warmup: int = 2, cuda_device: Optional[int] = None):
+        self.outer = outer
+        self.mask_kind = mask_kind
+        self.reps, self.warmup = reps, warmup
+        self.cuda_device = cuda_device
+        self.cache: dict = {}
+        self.timed = 0
+
+    def __call__(self, base_full, base_probe, schedule, assignment, device):
+        import_tilecc()
+        ma_full = _lower(base_full, schedule, assignment, device)
+        mod = ma_ir.from_tilecc(ma_full)
+        specs = recognize(mod)  # UnsupportedMA is a CompilerError -> +inf in search
+        for s in specs:
+            if cost.b200_viable(s):
+                return float("inf"), 0
+        key = tuple(realisation_key(s, self.outer, self.mask_kind) for s in specs)
+        if key not in self.cache:
+            self.cache[key] = self._time(mod, specs)
+            self.timed += 1
+        ma_p = _lower(base_probe, schedule, assignment, device)
+        proxy = cost.cost_model(ma_ir.from_tilecc(ma_p)).steps
+        return self.cache[key], proxy
+
+    def _time(self, mod, specs) -> float:
+        import numpy as np
+        import torch
+
+        from .executor import execute_ma
+
+        if self.cuda_device is not None:
+            torch.cuda.set_device(self.cuda_device)
+        g = torch.Generator(device="cuda")
+        g.manual_seed(0)
+        inputs = {}
+        for b in mod.inputs():
+            if b.name == "Mask":
+                n, m = b.shape
+                i = torch.arange(n, device="cuda")[:, None]
+                j = torch.arange(m, device="cuda")[None, :]
+                inputs[b.name] = torch.where(j <= i, 0.0, float("-inf")).float()
+                continue
+            shape = tuple(b.shape)
+            if self.outer is not None and len(shape) == 2 and b.name in _outer_names(specs):
+                B, Hq, Hkv = self.outer
+                h = Hq if b.name == _q_name(specs) else Hkv
+                shape = (B, h) + shape
+            inputs[b.name] = (torch.randn(shape, generator=g, device="cuda") * 0.5).to(torch.bfloat16)
+        kw = dict(outer=self.outer, return_torch=True)
+        if self.mask_kind != "auto":
+            kw["mask_kind"] = self.mask_kind
+        for _ in range(self.warmup):
+            execute_ma(mod, inputs, **kw)
+        times = []
+        for _ in range(self.reps):
+            _, rep = execute_ma(mod, inputs, **kw)
+            times.append(rep.device_ms * 1e3)
+        return float(statistics.median(times))
+
+
+def _outer_names(specs):
+    out = set()
+    for s in specs:
+        if isinstance(s, AttentionSpec):
+            out |= {s.q, s.k, s.v}
+    return out
+
+
+def _q_name(specs):
+    for s in specs:
+        if isinstance(s, AttentionSpec):
+            return s.q
+    return None
+
+
+def search(seeds, base_full, base_probe, device, cfg=None, scorer: Optional[Callable] = None,
+           batch_scorer: Optional[Callable] = None):
+    """Restatement of tilecc.tuner.tuner.search (tuner.py:143-206) with batch scoring.
+
+    ``scorer`` has ``score``'s signature (default: the reference analytic
+    ``score``); ``batch_scorer(list of (seed_index, assignment)) -> list of
+    (cost, proxy)`` scores a whole generation (e.g. on several GPUs) and must
+    return +inf/0 for candidates that raise CompilerError.
+    """
+    import_tilecc()
+    from tilecc.errors import BudgetTooSmall, CompilerError
+    from tilecc.tuner import tuner as ref
+
+    from .errors import BackendError
+
+    cfg = cfg or ref.TunerConfig()
+    if cfg.budget < len(seeds):
+        raise BudgetTooSmall(f"budget {cfg.budget} cannot even score the {len(seeds)} seed defaults")
+    scorer = scorer or ref.score
+    rng = random.Random(cfg.seed)
+    spaces = [ref.extract_params(s) for s in seeds]
+
+    def random_assignment(si):
+        return {name: rng.choice(list(allowed)) for name, allowed in spaces[si].entries}
+
+    def mutate(si, assignment):
+        if not spaces[si].entries:
+            return dict(assignment)
+        out = dict(assignment)
+        name, allowed = spaces[si].entries[rng.randrange(len(spaces[si].entries))]
+        out[name] = rng.choice(list(allowed))
+        return out
+
+    def score_one(si, assignment):
+        try:
+            return scorer(base_full, base_probe, seeds[si], assignment, device)
+        except (CompilerError, BackendError):
+            return float("inf"), 0
+
+    population = [(si, dict(sp.defaults)) for si, sp in enumerate(spaces)]
+    while len(population) < cfg.population:
+        si = rng.randrange(len(seeds))
+        population.append((si, random_assignment(si)))
+
+    measured, log_lines = [], []
+    generation = 0
+    while len(measured) < cfg.budget:
+        batch = population[: cfg.budget - len(measured)]
+        if batch_scorer is not None:
+            results = batch_scorer(seeds, base_full, base_probe, device, batch)
+        else:
+            results = [score_one(si, a) for si, a in batch]
+        for (si, assignment), (cst, proxy) in zip(batch, results):
+            cand = ref.Candidate(si, assignment, cst, proxy, len(measured), generation)
+            measured.append(cand)
+            log_lines.append(json.dumps({
+                "gen": generation, "seed": si,
+                "assignment": {k: assignment[k] for k in sorted(assignment)},
+                "cost": ref._num(cst), "proxy": proxy}))
+        if len(measured) >= cfg.budget:
+            break
+        ranked = sorted(measured, key=lambda c: c.key())
+        elite = ranked[: max(1, cfg.population // 4)]
+        population = []
+        while len(population) < cfg.population:
+            parent = elite[rng.randrange(len(elite))]
+            population.append((parent.seed_index, mutate(parent.seed_index, parent.assignment)))
+        generation += 1
+    ranked = sorted(measured, key=lambda c: c.key())
+    return ref.TuneResult(ranked, log_lines, len(measured))
+
+
+# ---------------------------------------------------------------------------- multi-GPU
+
+
+_WORKER = {}
+
+
+def _worker_init(kind, dev_index, scorer_kwargs):
+    import_tilecc()
+    if kind == "device":
+        import torch
+        torch.cuda.set_device(dev_index.get())
+        _WORKER["scorer"] = DeviceScorer(cuda_device=torch.cuda.current_device(), **scorer_kwargs)
+    else:
+        from tilecc.tuner import tuner as ref
+        _WORKER["scorer"] = ref.score
+
+
+def _worker_score(args):
+    from tilecc.errors import CompilerError
+
+    from .errors import BackendError
+    seeds, base_full, base_probe, device, si, assignment = args
+    try:
+        return _WORKER["scorer"](base_full, base_probe, seeds[si], assignment, device)
+    except (CompilerError, BackendError):
+        return float("inf"), 0
+
+
+class PoolScorer:
+    """Score a generation on a pool of workers (one per GPU for kind="device").
+
+    Results are returned in candidate order, so ``search`` is deterministic in
+    the candidate sequence regardless of worker count.  kind="analytic" uses
+    the reference cost model (CPU; used to test the parallel merge).
+    """
+
+    def __init__(self, workers: int, kind: str = "device", scorer_kwargs: Optional[dict] = None):
+        import multiprocessing as mp
+
+        ctx = mp.get_context("spawn")
+        self.kind = kind
+        counter = ctx.Value("i", 0)
+        self._counter = counter
+        self.pool = ctx.Pool(workers, initializer=_pool_init, initargs=(kind, counter, scorer_kwargs or {}))
+
+    def __call__(self, seeds, base_full, base_probe, device, batch):
+        args = [(seeds, base_full, base_probe, device, si, a) for si, a in batch]
+        return self.pool.map(_worker_score, args, chunksize=1)
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+
+def _pool_init(kind, counter, scorer_kwargs):
+    with counter.get_lock():
+        idx = counter.value
+        counter.value += 1
+
+    class _Idx:
+        def get(self_inner):
+            return idx
+
+    _worker_init(kind, _Idx(), scorer_kwargs)
