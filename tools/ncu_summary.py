@@ -53,10 +53,16 @@ def summarise(rep, workload, alg_bytes=None, alg_flops=None):
         if m in d:
             out[k] = to_float(d[m][1])
             out[k + "_unit"] = d[m][0]
-    rd = out.get("dram_read_MB") or 0.0
-    wr = out.get("dram_write_MB") or 0.0
-    scale = 1e6 if out.get("dram_read_MB_unit", "Mbyte") == "Mbyte" else (1e9 if out.get("dram_read_MB_unit") == "Gbyte" else 1.0)
-    out["dram_bytes_per_launch"] = (rd + wr) * scale
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    rd = (out.get("dram_read_MB") or 0.0) * scale.get(out.get("dram_read_MB_unit", "Mbyte"), 1.0)
+    wr = (out.get("dram_write_MB") or 0.0) * scale.get(out.get("dram_write_MB_unit", "Mbyte"), 1.0)
+    out["dram_read_MB"], out["dram_write_MB"] = rd / 1e6, wr / 1e6
+    out["dram_read_MB_unit"] = out["dram_write_MB_unit"] = "Mbyte"
+    out["dram_bytes_per_launch"] = rd + wr
+    tscale = {"ns": 1e-3, "us": 1.0, "ms": 1e3, "s": 1e6}
+    if "duration_us" in out:
+        out["duration_us"] = out["duration_us"] * tscale.get(out.get("duration_us_unit", "us"), 1.0)
+        out["duration_us_unit"] = "us"
     tot = to_float(d.get("smsp__pcsamp_sample_count", ("", "0"))[1]) or 1.0
     out["stall_samples_pct"] = {s: round(100.0 * (to_float(d.get(f"smsp__pcsamp_warps_issue_stalled_{s}", ("", "0"))[1]) or 0.0) / tot, 1)
                                 for s in STALLS}
@@ -65,6 +71,9 @@ def summarise(rep, workload, alg_bytes=None, alg_flops=None):
     if alg_flops and out.get("duration_us"):
         out["algorithmic_flops"] = alg_flops
         out["tflops_under_ncu_clock"] = alg_flops / (out["duration_us"] * 1e-6) / 1e12
+    if alg_bytes and out.get("duration_us"):
+        out["gbs_under_ncu_clock"] = alg_bytes / (out["duration_us"] * 1e-6) / 1e9
+        out["traffic_over_algorithmic"] = out["dram_bytes_per_launch"] / alg_bytes
     return out
 
 
