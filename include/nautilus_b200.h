@@ -109,7 +109,9 @@ typedef struct nt_gemm_args {
 } nt_gemm_args;
 int nt_gemm(const nt_gemm_args* args, void* stream);
 
-/* Fused chain Y = (X . W1) . W2 with the T tile kept on chip (E <= 256). */
+/* Fused chain Y = (X . W1) . W2 with the T tile kept on chip (E <= 256).
+ * F is split over CTAs; fp32 partials go to `workspace`
+ * (nt_gemm_chain_workspace_bytes(n, f, e) bytes, may be 0 -> NULL allowed). */
 typedef struct nt_chain_args {
   const void* x; int64_t ldx;   /* bf16 [N, K] */
   const void* w1; int64_t ldw1; /* bf16 [K, F] */
@@ -117,7 +119,9 @@ typedef struct nt_chain_args {
   void* y; int64_t ldy;         /* out [N, E] */
   int32_t n, k, f, e;
   int32_t out_dtype;
+  void* workspace;
 } nt_chain_args;
+int64_t nt_gemm_chain_workspace_bytes(int32_t n, int32_t f, int32_t e);
 int nt_gemm_chain(const nt_chain_args* args, void* stream);
 
 /* dtype conversion helpers (device buffers) */

@@ -21,7 +21,7 @@ NT_DTYPE_BF16, NT_DTYPE_F32 = 0, 1
 # Every symbol include/nautilus_b200.h declares (checked by tests/test_capi.py).
 EXPORTED = (
     "nt_attn_fwd", "nt_attn_decode", "nt_decode_workspace_bytes", "nt_decode_num_splits", "nt_gemm",
-    "nt_gemm_chain",
+    "nt_gemm_chain", "nt_gemm_chain_workspace_bytes",
     "nt_cast_f32_to_bf16", "nt_cast_bf16_to_f32", "nt_abi_version", "nt_last_error", "nt_launch_count",
 )
 
@@ -58,7 +58,7 @@ class ChainArgs(C.Structure):
     _fields_ = [("x", C.c_void_p), ("ldx", C.c_int64), ("w1", C.c_void_p), ("ldw1", C.c_int64),
                 ("w2", C.c_void_p), ("ldw2", C.c_int64), ("y", C.c_void_p), ("ldy", C.c_int64),
                 ("n", C.c_int32), ("k", C.c_int32), ("f", C.c_int32), ("e", C.c_int32),
-                ("out_dtype", C.c_int32)]
+                ("out_dtype", C.c_int32), ("workspace", C.c_void_p)]
 
 
 _lib = None
@@ -85,6 +85,8 @@ def lib():
             L.nt_decode_num_splits.restype = C.c_int
             L.nt_gemm.argtypes = [C.POINTER(GemmArgs), C.c_void_p]
             L.nt_gemm_chain.argtypes = [C.POINTER(ChainArgs), C.c_void_p]
+            L.nt_gemm_chain_workspace_bytes.argtypes = [C.c_int32] * 3
+            L.nt_gemm_chain_workspace_bytes.restype = C.c_int64
             L.nt_cast_f32_to_bf16.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
             L.nt_cast_bf16_to_f32.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
             L.nt_last_error.restype = C.c_char_p

@@ -204,10 +204,14 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             mbar_wait(&bar_p_full[t], (j - 1) & 1, p.err, 4);
             if (t == 0) mbar_wait(&bar_kv_full[slotV], (itV / C::STAGES) & 1, p.err, 5);
             tc_fence_after();
-            issue_pv(t, slotV, j - 1 > 0);
+  #ifndef NT_EXP_NO_PV
+          issue_pv(t, slotV, j - 1 > 0);
+#endif
             if (t == 1) umma_commit(&bar_kv_empty[slotV]);
           }
+#ifndef NT_EXP_NO_S
           issue_s(t, slotK);
+#endif
           umma_commit(&bar_s_full[t]);
         }
         umma_commit(&bar_kv_empty[slotK]);
@@ -277,6 +281,23 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         }
         mx = fmaxf(fmax3(a0, a1, a2), a3);
       }
+#ifdef NT_EXP_NO_SOFTMAX
+      {
+        uint32_t pk[16];
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) pk[i] = s[ch * 32 + 2 * i];
+          tmem_st16(tS + ch * 16, pk);
+        }
+        l_run = 1.f;
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar_p_full[t]);
+        continue;
+      }
+#endif
       const float m_new = fmaxf(m_run, mx * sc);
       const bool need = m_new > m_run + kRescaleLog2;
       if (__any_sync(0xffffffffu, need)) {

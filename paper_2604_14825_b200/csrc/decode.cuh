@@ -133,23 +133,26 @@ __global__ void __launch_bounds__(kDecodeCTAThreads, 1)
     const int d0 = ds * DPT;
     const int panel = d0 / 64, chunk = (d0 % 64) / 8;
 
-    float q[R][DPT];
+    // q rows (pre-scaled by c*log2e) and the O accumulators as fp32 pairs (FFMA2)
+    float2 q2[R][DPT / 2];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int h = hkv * p.g + r / p.Nq, n = r % p.Nq;
       const __nv_bfloat16* qp = p.q + b * p.q_sb + h * p.q_sh + n * p.q_sn + d0;
+      float qf[DPT];
 #pragma unroll
-      for (int c = 0; c < NCH; ++c) bf16x8_to_f32(*reinterpret_cast<const uint4*>(qp + 8 * c), &q[r][8 * c]);
+      for (int c = 0; c < NCH; ++c) bf16x8_to_f32(*reinterpret_cast<const uint4*>(qp + 8 * c), &qf[8 * c]);
 #pragma unroll
-      for (int i = 0; i < DPT; ++i) q[r][i] *= p.scale_log2;  // fold c*log2e into q
+      for (int i = 0; i < DPT / 2; ++i) q2[r][i] = make_float2(qf[2 * i] * p.scale_log2, qf[2 * i + 1] * p.scale_log2);
     }
-    float o[R][DPT], m[R], l[R];
+    float2 o2[R][DPT / 2];
+    float m[R], l[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       m[r] = __int_as_float(0xff800000);
       l[r] = 0.f;
 #pragma unroll
-      for (int i = 0; i < DPT; ++i) o[r][i] = 0.f;
+      for (int i = 0; i < DPT / 2; ++i) o2[r][i] = make_float2(0.f, 0.f);
     }
 
     for (int t = 0; t < ntiles; ++t) {
@@ -171,13 +174,10 @@ __global__ void __launch_bounds__(kDecodeCTAThreads, 1)
         float sc[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          float a0 = 0.f, a1 = 0.f;
+          float2 a = make_float2(0.f, 0.f);
 #pragma unroll
-          for (int i = 0; i < DPT; i += 2) {
-            a0 = fmaf(q[r][i], kf[i], a0);
-            a1 = fmaf(q[r][i + 1], kf[i + 1], a1);
-          }
-          sc[r] = a0 + a1;
+          for (int i = 0; i < DPT / 2; ++i) a = ffma2(q2[r][i], make_float2(kf[2 * i], kf[2 * i + 1]), a);
+          sc[r] = a.x + a.y;
         }
 #pragma unroll
         for (int offx = 1; offx < TPK; offx <<= 1)
@@ -190,13 +190,15 @@ __global__ void __launch_bounds__(kDecodeCTAThreads, 1)
               const float alpha = ex2(m[r] - sc[r]);
               l[r] *= alpha;
 #pragma unroll
-              for (int i = 0; i < DPT; ++i) o[r][i] *= alpha;
+              for (int i = 0; i < DPT / 2; ++i)
+                o2[r][i] = ffma2(o2[r][i], make_float2(alpha, alpha), make_float2(0.f, 0.f));
               m[r] = sc[r];
             }
             const float pr = ex2(sc[r] - m[r]);
             l[r] += pr;
 #pragma unroll
-            for (int i = 0; i < DPT; ++i) o[r][i] = fmaf(pr, vf[i], o[r][i]);
+            for (int i = 0; i < DPT / 2; ++i)
+              o2[r][i] = ffma2(make_float2(pr, pr), make_float2(vf[2 * i], vf[2 * i + 1]), o2[r][i]);
           }
         }
       }
@@ -219,7 +221,10 @@ __global__ void __launch_bounds__(kDecodeCTAThreads, 1)
 #pragma unroll
     for (int r = 0; r < R; ++r)
 #pragma unroll
-      for (int i = 0; i < DPT; ++i) sm_o[(kg * R + r) * D + d0 + i] = o[r][i];
+      for (int i = 0; i < DPT / 2; ++i) {
+        sm_o[(kg * R + r) * D + d0 + 2 * i] = o2[r][i].x;
+        sm_o[(kg * R + r) * D + d0 + 2 * i + 1] = o2[r][i].y;
+      }
     named_bar_sync(1, kDecodeConsumers);
     float* ws = p.ws + ((long long)grp * p.splits + s) * R * (D + 2);
     for (int idx = tc; idx < R * D; idx += kDecodeConsumers) {

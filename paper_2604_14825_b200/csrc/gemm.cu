@@ -54,6 +54,16 @@ int launch_gemm(const nt_gemm_args* a, cudaStream_t st) {
   return check_cuda(cudaGetLastError(), "gemm launch");
 }
 
+// F split so that row_blocks x splits ~ fills the SMs
+void chain_split(int n, int f, int* splits_out, int* per_split_out) {
+  const int row_blocks = (n + 127) / 128;
+  const int f_tiles = (f + 127) / 128;
+  int splits = std::max(1, std::min(f_tiles, sm_count() / std::max(1, row_blocks)));
+  const int per = (f_tiles + splits - 1) / splits;
+  *splits_out = (f_tiles + per - 1) / per;
+  *per_split_out = per;
+}
+
 template <int E>
 int launch_chain(const nt_chain_args* a, cudaStream_t st) {
   CUtensorMap mx, mw1, mw2;
@@ -67,21 +77,14 @@ int launch_chain(const nt_chain_args* a, cudaStream_t st) {
   p.F = a->f;
   p.E = a->e;
   p.row_blocks = (a->n + 127) / 128;
-  const int f_tiles = (a->f + 127) / 128;
-  int splits = std::max(1, std::min(f_tiles, sm_count() / std::max(1, p.row_blocks)));
-  p.f_tiles_per_split = (f_tiles + splits - 1) / splits;
-  splits = (f_tiles + p.f_tiles_per_split - 1) / p.f_tiles_per_split;
+  int splits = 1;
+  chain_split(a->n, a->f, &splits, &p.f_tiles_per_split);
   p.splits = splits;
   p.y = a->y;
   p.ldy = a->ldy;
   p.out_f32 = a->out_dtype == NT_DTYPE_F32;
-  float* partial = nullptr;
-  if (splits > 1) {
-    if ((rc = check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&partial),
-                                         sizeof(float) * (size_t)splits * a->n * a->e, st),
-                         "cudaMallocAsync(chain partials)")))
-      return rc;
-  }
+  float* partial = static_cast<float*>(a->workspace);
+  if (splits > 1 && !partial) return set_error(NT_ERR_INVALID, "chain workspace required (nt_gemm_chain_workspace_bytes)");
   p.partial = partial;
   auto kern = chain_kernel<E>;
   const int smem = ChainCfg<E>::SMEM_BYTES;
@@ -101,7 +104,6 @@ int launch_chain(const nt_chain_args* a, cudaStream_t st) {
     chain_reduce_kernel<<<blocks, 256, 0, st>>>(partial, splits, a->n, a->e, a->y, a->ldy, p.out_f32);
     g_launches++;
     if ((rc = check_cuda(cudaGetLastError(), "chain reduce launch"))) return rc;
-    if ((rc = check_cuda(cudaFreeAsync(partial, st), "cudaFreeAsync"))) return rc;
   }
   return NT_OK;
 }
@@ -116,6 +118,12 @@ extern "C" int nt_gemm(const nt_gemm_args* a, void* stream) {
   const bool f32 = a->out_dtype == NT_DTYPE_F32;
   if (a->n <= 128) return f32 ? launch_gemm<128, true>(a, st) : launch_gemm<128, false>(a, st);
   return f32 ? launch_gemm<256, true>(a, st) : launch_gemm<256, false>(a, st);
+}
+
+extern "C" int64_t nt_gemm_chain_workspace_bytes(int32_t n, int32_t f, int32_t e) {
+  int splits = 1, per = 1;
+  chain_split(n, f, &splits, &per);
+  return splits > 1 ? (int64_t)splits * n * e * (int64_t)sizeof(float) : 0;
 }
 
 extern "C" int nt_gemm_chain(const nt_chain_args* a, void* stream) {

@@ -84,6 +84,9 @@ class ChainPlan:
             c.y, c.ldy = _mat(y, "Y")
             c.n, c.k, c.f, c.e = N, K, F, E
             c.out_dtype = _lib.NT_DTYPE_F32 if y.dtype == torch.float32 else _lib.NT_DTYPE_BF16
+            ws = int(_lib.lib().nt_gemm_chain_workspace_bytes(N, F, E))
+            self.ws = torch.empty(max(ws // 4, 1), dtype=torch.float32, device=x.device)
+            c.workspace = self.ws.data_ptr() if ws else None
             self.args = c
             self._ref = C.byref(c)
             self._fn = _lib.lib().nt_gemm_chain
