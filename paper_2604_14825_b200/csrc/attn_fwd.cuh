@@ -80,6 +80,20 @@ struct AttnCfg {
 
 __device__ __forceinline__ float f_ninf() { return __int_as_float(0xff800000); }
 
+#ifdef NT_TRACE
+// Debug timeline (NT_TRACE builds only): clock64 stamps of one CTA's pipeline.
+// trace[(role * 64 + iter) * 8 + event]; role 0 MMA, 1/2 softmax tile 0/1, 3 producer.
+__device__ unsigned long long* g_nt_trace = nullptr;
+__device__ int g_nt_trace_cta = 0;
+#define NT_STAMP(role, iter, ev)                                                               \
+  do {                                                                                         \
+    if (g_nt_trace && blockIdx.x == g_nt_trace_cta && (iter) < 64)                             \
+      g_nt_trace[((role) * 64 + (iter)) * 8 + (ev)] = clock64();                               \
+  } while (0)
+#else
+#define NT_STAMP(role, iter, ev) do {} while (0)
+#endif
+
 template <int D, int MASK, bool OUT_F32>
 __global__ void __launch_bounds__(kAttnThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -158,7 +172,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       for (int it = 0; it < 2 * n_kv; ++it) {
         const int slot = it % C::STAGES;
         const uint32_t ph = (it / C::STAGES) & 1;
+        NT_STAMP(3, it >> 1, (it & 1) * 2);
         mbar_wait(&bar_kv_empty[slot], ph ^ 1, p.err, 1);
+        NT_STAMP(3, it >> 1, (it & 1) * 2 + 1);
         mbar_arrive_expect_tx(&bar_kv_full[slot], C::TKV);
         const CUtensorMap* m = (it & 1) ? &tmV : &tmK;
         const int row = (it >> 1) * 128;
@@ -195,13 +211,16 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       for (int j = 0; j < n_kv; ++j) {
         const int itK = 2 * j;
         const int slotK = itK % C::STAGES;
+        NT_STAMP(0, j, 0);
         mbar_wait(&bar_kv_full[slotK], (itK / C::STAGES) & 1, p.err, 3);
+        NT_STAMP(0, j, 1);
         tc_fence_after();
         const int itV = 2 * (j - 1) + 1;
         const int slotV = (itV + C::STAGES) % C::STAGES;
         for (int t = 0; t < 2; ++t) {
           if (j > 0) {
             mbar_wait(&bar_p_full[t], (j - 1) & 1, p.err, 4);
+            NT_STAMP(0, j, 2 + 2 * t);
             if (t == 0) mbar_wait(&bar_kv_full[slotV], (itV / C::STAGES) & 1, p.err, 5);
             tc_fence_after();
   #ifndef NT_EXP_NO_PV
@@ -213,6 +232,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           issue_s(t, slotK);
 #endif
           umma_commit(&bar_s_full[t]);
+          NT_STAMP(0, j, 3 + 2 * t);
         }
         umma_commit(&bar_kv_empty[slotK]);
       }
@@ -243,12 +263,15 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     float m_run = NINF, l_run = 0.f;
 
     for (int j = 0; j < n_kv; ++j) {
+      if (lane == 0 && wq == 0) NT_STAMP(1 + t, j, 0);
       mbar_wait(&bar_s_full[t], j & 1, p.err, 8);
+      if (lane == 0 && wq == 0) NT_STAMP(1 + t, j, 1);
       tc_fence_after();
       uint32_t s[128];
 #pragma unroll
       for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, s + c * 32);
       tmem_wait_ld();
+      if (lane == 0 && wq == 0) NT_STAMP(1 + t, j, 2);
       const int kv0 = j * 128;
       if (MASK == MASK_TENSOR) {
         const float* mrow = p.mask + (long long)min(qi, p.N - 1) * p.mask_row_stride;
@@ -298,6 +321,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         continue;
       }
 #endif
+      if (lane == 0 && wq == 0) NT_STAMP(1 + t, j, 3);
       const float m_new = fmaxf(m_run, mx * sc);
       const bool need = m_new > m_run + kRescaleLog2;
       if (__any_sync(0xffffffffu, need)) {
@@ -339,8 +363,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         tmem_st16(tS + ch * 16, pk);
       }
       const float sum = (sum2[0].x + sum2[0].y) + (sum2[1].x + sum2[1].y);
+      if (lane == 0 && wq == 0) NT_STAMP(1 + t, j, 4);
       l_run += sum;
       tmem_wait_st();
+      if (lane == 0 && wq == 0) NT_STAMP(1 + t, j, 5);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_p_full[t]);

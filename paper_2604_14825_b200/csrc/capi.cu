@@ -221,6 +221,14 @@ extern "C" int nt_cast_bf16_to_f32(const void* src, float* dst, int64_t n, void*
   return check_cuda(cudaGetLastError(), "cast_bf16_f32");
 }
 
+#ifdef NT_TRACE
+extern "C" int nt_debug_set_trace(unsigned long long* buf, int cta) {
+  cudaMemcpyToSymbol(nt::g_nt_trace, &buf, sizeof(buf));
+  cudaMemcpyToSymbol(nt::g_nt_trace_cta, &cta, sizeof(cta));
+  return check_cuda(cudaGetLastError(), "nt_debug_set_trace");
+}
+#endif
+
 extern "C" int nt_abi_version(void) { return NT_ABI_VERSION; }
 extern "C" const char* nt_last_error(void) { return g_last_error.c_str(); }
 extern "C" int64_t nt_launch_count(void) { return g_launches.load(); }
