@@ -62,6 +62,11 @@ constexpr float kRescaleLog2 = 8.0f;
 #define NT_POLY_EVERY 0
 #endif
 constexpr bool kPolyExp = NT_POLY_EVERY > 0;
+// P -> bf16 packing on the ALU (1) or with cvt.rn.bf16x2 on the XU pipe (0)
+#ifndef NT_PACK_ALU
+#define NT_PACK_ALU 1
+#endif
+constexpr bool kPackAlu = NT_PACK_ALU != 0;
 constexpr int kPolyEvery = NT_POLY_EVERY > 0 ? NT_POLY_EVERY : 1;
 
 template <int D>
@@ -358,7 +363,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             e = make_float2(ex2(x.x), ex2(x.y));
           }
           sum2[i & 1] = fadd2(sum2[i & 1], e);
-          pk[i] = pack_bf16(e.x, e.y);
+          pk[i] = kPackAlu ? pack_bf16_alu(e.x, e.y) : pack_bf16(e.x, e.y);
         }
         tmem_st16(tS + ch * 16, pk);
       }

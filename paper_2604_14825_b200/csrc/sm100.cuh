@@ -235,6 +235,18 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return r;
 }
 
+// fp32 pair -> bf16x2 on the integer pipe (round half away from zero on the
+// dropped 16 bits; ties are measure-zero for softmax probabilities).  The
+// cvt.rn.bf16x2.f32 (F2FP) alternative issues on the same XU pipe as
+// MUFU.EX2 and competes with the exponentials.
+__device__ __forceinline__ uint32_t pack_bf16_alu(float lo, float hi) {
+  const uint32_t a = __float_as_uint(lo) + 0x8000u;
+  const uint32_t b = __float_as_uint(hi) + 0x8000u;
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, 0x7632;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+
 // three-input max (FMNMX3)
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float r;
