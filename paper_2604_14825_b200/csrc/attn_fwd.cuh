@@ -52,7 +52,7 @@ struct AttnFwdParams {
   int* err;  // bit 0: zero denominator (fully masked row); 0x100|k: pipeline timeout
 };
 
-constexpr int kAttnThreads = 384;
+constexpr int kAttnThreads = 640;  // 4 control warps + 2 tiles x 2 column halves x 4 warps
 constexpr float kRescaleLog2 = 8.0f;
 // Fraction of exp2 evaluated by the FMA-pipe polynomial instead of MUFU.EX2
 // (1 in NT_POLY_EVERY pairs; 0 = MUFU only).  Measured on B200 at Llama 8K
@@ -64,7 +64,7 @@ constexpr float kRescaleLog2 = 8.0f;
 constexpr bool kPolyExp = NT_POLY_EVERY > 0;
 // P -> bf16 packing on the ALU (1) or with cvt.rn.bf16x2 on the XU pipe (0)
 #ifndef NT_PACK_ALU
-#define NT_PACK_ALU 1
+#define NT_PACK_ALU 0
 #endif
 constexpr bool kPackAlu = NT_PACK_ALU != 0;
 constexpr int kPolyEvery = NT_POLY_EVERY > 0 ? NT_POLY_EVERY : 1;
@@ -80,7 +80,8 @@ struct AttnCfg {
   static constexpr int SMEM_KV = 2 * TQ;
   static constexpr int SMEM_BAR = SMEM_KV + STAGES * TKV;
   static constexpr int NBAR = 2 + 2 * STAGES + 2 + 2 + 2;
-  static constexpr int SMEM_BYTES = SMEM_BAR + NBAR * 8 + 16 + 1024;  // + alignment slack
+  static constexpr int SMEM_RED = SMEM_BAR + NBAR * 8 + 16;  // half-row max / sum exchange (6 KB)
+  static constexpr int SMEM_BYTES = SMEM_RED + 1536 * 4 + 1024;  // + alignment slack
 };
 
 __device__ __forceinline__ float f_ninf() { return __int_as_float(0xff800000); }
@@ -119,6 +120,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   uint64_t* bar_p_full = bar_s_full + 2;            // [2]
   uint64_t* bar_o_full = bar_p_full + 2;            // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBAR);
+  float* red = reinterpret_cast<float*>(smem + C::SMEM_RED);
 
   const int warp = __shfl_sync(0xffffffffu, threadIdx.x / 32, 0);
   const int lane = threadIdx.x & 31;
@@ -152,7 +154,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     }
     for (int t = 0; t < 2; ++t) {
       mbar_init(&bar_s_full[t], 1);
-      mbar_init(&bar_p_full[t], 4);
+      mbar_init(&bar_p_full[t], 8);
       mbar_init(&bar_o_full[t], 1);
     }
     fence_barrier_init();
@@ -164,7 +166,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp < 4) {
-  asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");  // per SMSP: 56 + 4 x 112 <= 512
   if (warp == 0) {
     // ================= TMA producer
     if (lane == 0) {
@@ -254,9 +256,13 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     }
   }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
-    // ================= softmax (+ lazy O correction + epilogue), one thread per query row
-    const int t = (warp - 4) / 4;
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 112;");
+    // ================= softmax (+ lazy O correction + epilogue)
+    // Warpgroup g = warp/4 - 1: tile t = g >> 1, column half h = g & 1.  Each thread owns one
+    // query row (TMEM lane) and 64 of the 128 key columns; the two halves of a row exchange
+    // their partial row max through shared memory once per KV tile.
+    const int g = warp / 4 - 1;
+    const int t = g >> 1, h = g & 1;
     const int wq = warp & 3;  // TMEM sub-partition this warp may access
     const int r = wq * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
@@ -265,32 +271,37 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     const int qi = q_row0 + t * 128 + r;
     const float NINF = f_ninf();
     const float sc = (MASK == MASK_TENSOR) ? 1.0f : p.scale_log2;
+    float* xmax = red + t * 512;        // [2 buffers][2 halves][128 rows]
+    float* xsum = red + 1024 + t * 256;  // [2 halves][128 rows]
+    const uint32_t bar_id = 1 + t;       // named barrier of the 256 threads of tile t
+    constexpr int HC = 64;               // key columns per half
+    constexpr int DH = D / 2;            // O columns per half
     float m_run = NINF, l_run = 0.f;
 
     for (int j = 0; j < n_kv; ++j) {
-      if (lane == 0 && wq == 0) NT_STAMP(1 + t, j, 0);
+      if (lane == 0 && wq == 0 && h == 0) NT_STAMP(1 + t, j, 0);
       mbar_wait(&bar_s_full[t], j & 1, p.err, 8);
-      if (lane == 0 && wq == 0) NT_STAMP(1 + t, j, 1);
+      if (lane == 0 && wq == 0 && h == 0) NT_STAMP(1 + t, j, 1);
       tc_fence_after();
-      uint32_t s[128];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, s + c * 32);
+      uint32_t s[HC];
+      tmem_ld32(tS + h * HC, s);
+      tmem_ld32(tS + h * HC + 32, s + 32);
       tmem_wait_ld();
-      if (lane == 0 && wq == 0) NT_STAMP(1 + t, j, 2);
-      const int kv0 = j * 128;
+      if (lane == 0 && wq == 0 && h == 0) NT_STAMP(1 + t, j, 2);
+      const int kv0 = j * 128 + h * HC;
       if (MASK == MASK_TENSOR) {
         const float* mrow = p.mask + (long long)min(qi, p.N - 1) * p.mask_row_stride;
 #pragma unroll
-        for (int c = 0; c < 128; ++c) {
+        for (int c = 0; c < HC; ++c) {
           const int kv = kv0 + c;
           const float mk = (kv < p.M) ? __ldg(mrow + kv) : NINF;
           s[c] = __float_as_uint(fmaf(__uint_as_float(s[c]), p.scale_log2, mk * 1.4426950408889634f));
         }
       } else {
         const int lim = (MASK == MASK_CAUSAL) ? min(qi + p.causal_offset, p.M - 1) : (p.M - 1);
-        if (kv0 + 127 > lim) {
+        if (kv0 + HC - 1 > lim) {
 #pragma unroll
-          for (int c = 0; c < 128; ++c)
+          for (int c = 0; c < HC; ++c)
             if (kv0 + c > lim) s[c] = __float_as_uint(NINF);
         }
       }
@@ -300,46 +311,35 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         float a0 = __uint_as_float(s[0]), a1 = __uint_as_float(s[1]);
         float a2 = __uint_as_float(s[2]), a3 = __uint_as_float(s[3]);
 #pragma unroll
-        for (int c = 4; c < 128; c += 8) {
+        for (int c = 4; c < HC; c += 8) {
           a0 = fmax3(a0, __uint_as_float(s[c]), __uint_as_float(s[c + 1]));
           a1 = fmax3(a1, __uint_as_float(s[c + 2]), __uint_as_float(s[c + 3]));
           a2 = fmax3(a2, __uint_as_float(s[c + 4]), __uint_as_float(s[c + 5]));
-          if (c + 7 < 128) a3 = fmax3(a3, __uint_as_float(s[c + 6]), __uint_as_float(s[c + 7]));
+          if (c + 7 < HC) a3 = fmax3(a3, __uint_as_float(s[c + 6]), __uint_as_float(s[c + 7]));
           else a3 = fmaxf(a3, __uint_as_float(s[c + 6]));
         }
         mx = fmaxf(fmax3(a0, a1, a2), a3);
       }
-#ifdef NT_EXP_NO_SOFTMAX
-      {
-        uint32_t pk[16];
-#pragma unroll
-        for (int ch = 0; ch < 4; ++ch) {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) pk[i] = s[ch * 32 + 2 * i];
-          tmem_st16(tS + ch * 16, pk);
-        }
-        l_run = 1.f;
-        tmem_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&bar_p_full[t]);
-        continue;
-      }
-#endif
-      if (lane == 0 && wq == 0) NT_STAMP(1 + t, j, 3);
+      // exchange the half-row maxima (double-buffered on j so one barrier per tile suffices)
+      float* xm = xmax + (j & 1) * 256;
+      xm[h * 128 + r] = mx;
+      named_bar_sync(bar_id, 256);
+      mx = fmaxf(mx, xm[(h ^ 1) * 128 + r]);
+      if (lane == 0 && wq == 0 && h == 0) NT_STAMP(1 + t, j, 3);
       const float m_new = fmaxf(m_run, mx * sc);
       const bool need = m_new > m_run + kRescaleLog2;
+      // both halves hold the same rows (same TMEM lanes) -> identical warp decisions
       if (__any_sync(0xffffffffu, need)) {
         const float alpha = (m_new == NINF) ? 1.0f : ex2(m_run - m_new);
         if (j > 0) {
 #pragma unroll
-          for (int c = 0; c < D / 16; ++c) {
+          for (int c = 0; c < DH / 16; ++c) {
             uint32_t o[16];
-            tmem_ld16(tO + c * 16, o);
+            tmem_ld16(tO + h * DH + c * 16, o);
             tmem_wait_ld();
 #pragma unroll
             for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-            tmem_st16(tO + c * 16, o);
+            tmem_st16(tO + h * DH + c * 16, o);
           }
         }
         l_run *= alpha;
@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       const float2 nm2 = make_float2(-m_use, -m_use);
       float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-      for (int ch = 0; ch < 4; ++ch) {
+      for (int ch = 0; ch < 2; ++ch) {
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
@@ -365,30 +365,33 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           sum2[i & 1] = fadd2(sum2[i & 1], e);
           pk[i] = kPackAlu ? pack_bf16_alu(e.x, e.y) : pack_bf16(e.x, e.y);
         }
-        tmem_st16(tS + ch * 16, pk);
+        tmem_st16(tS + h * (HC / 2) + ch * 16, pk);  // P (bf16) over this half's key columns
       }
       const float sum = (sum2[0].x + sum2[0].y) + (sum2[1].x + sum2[1].y);
-      if (lane == 0 && wq == 0) NT_STAMP(1 + t, j, 4);
+      if (lane == 0 && wq == 0 && h == 0) NT_STAMP(1 + t, j, 4);
       l_run += sum;
       tmem_wait_st();
-      if (lane == 0 && wq == 0) NT_STAMP(1 + t, j, 5);
+      if (lane == 0 && wq == 0 && h == 0) NT_STAMP(1 + t, j, 5);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_p_full[t]);
     }
 
-    // ---- epilogue: O / l
+    // ---- epilogue: O / l  (l = sum of the two half-row partial sums)
+    xsum[h * 128 + r] = l_run;
     mbar_wait(&bar_o_full[t], 0, p.err, 9);
     tc_fence_after();
+    named_bar_sync(bar_id, 256);
+    const float l_tot = l_run + xsum[(h ^ 1) * 128 + r];
     const bool valid = qi < p.N;
-    if (valid && !(l_run > 0.f) && p.err) atomicOr(p.err, 1);
-    const float inv = (l_run > 0.f) ? 1.0f / l_run : 0.f;
+    if (valid && h == 0 && !(l_tot > 0.f) && p.err) atomicOr(p.err, 1);
+    const float inv = (l_tot > 0.f) ? 1.0f / l_tot : 0.f;
     if (OUT_F32) {
-      float* orow = p.o_f32 + (long long)b * p.o_sb + (long long)hq * p.o_sh + (long long)qi * p.o_sn;
+      float* orow = p.o_f32 + (long long)b * p.o_sb + (long long)hq * p.o_sh + (long long)qi * p.o_sn + h * DH;
 #pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
+      for (int c = 0; c < DH / 32; ++c) {
         uint32_t o[32];
-        tmem_ld32(tO + c * 32, o);
+        tmem_ld32(tO + h * DH + c * 32, o);
         tmem_wait_ld();
         if (valid) {
 #pragma unroll
@@ -402,27 +405,28 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     } else {
       uint8_t* stage = sQ + t * C::TQ;  // Q_t is dead once O_t is final
 #pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
+      for (int c = 0; c < DH / 32; ++c) {
         uint32_t o[32];
-        tmem_ld32(tO + c * 32, o);
+        tmem_ld32(tO + h * DH + c * 32, o);
         tmem_wait_ld();
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i)
           pk[i] = pack_bf16(__uint_as_float(o[2 * i]) * inv, __uint_as_float(o[2 * i + 1]) * inv);
-        uint8_t* rowp = stage + (c >> 1) * C::HALF + r * 128;
+        const int col0 = h * DH + c * 32;  // first O column of this 32-column chunk
+        uint8_t* rowp = stage + (col0 >> 6) * C::HALF + r * 128;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const int chunk = ((c & 1) * 4 + q) ^ (r & 7);
+          const int chunk = (((col0 & 63) >> 3) + q) ^ (r & 7);
           *reinterpret_cast<uint4*>(rowp + chunk * 16) = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
         }
       }
       fence_proxy_async_smem();
-      named_bar_sync(1 + t, 128);
-      if (r == 0) {
+      named_bar_sync(bar_id, 256);
+      if (h == 0 && r == 0) {
 #pragma unroll
-        for (int h = 0; h < D / 64; ++h)
-          tma_store_4d(&tmO, stage + h * C::HALF, h * 64, q_row0 + t * 128, hq, b);
+        for (int hh = 0; hh < D / 64; ++hh)
+          tma_store_4d(&tmO, stage + hh * C::HALF, hh * 64, q_row0 + t * 128, hq, b);
         bulk_commit();
         bulk_wait_read0();
       }
