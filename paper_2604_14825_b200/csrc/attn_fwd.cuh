@@ -166,7 +166,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp < 4) {
-  asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");  // per SMSP: 56 + 4 x 112 <= 512
+  // setmaxnreg only redistributes the launch allocation (640 x 96 regs):
+  // 128 x 40 + 512 x 104 = 58368 <= 61440
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
   if (warp == 0) {
     // ================= TMA producer
     if (lane == 0) {
@@ -256,7 +258,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     }
   }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 112;");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 104;");
     // ================= softmax (+ lazy O correction + epilogue)
     // Warpgroup g = warp/4 - 1: tile t = g >> 1, column half h = g & 1.  Each thread owns one
     // query row (TMEM lane) and 64 of the 128 key columns; the two halves of a row exchange
