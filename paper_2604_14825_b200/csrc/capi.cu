@@ -162,7 +162,7 @@ extern "C" int nt_attn_fwd(const nt_attn_args* a, void* stream) {
   p.N = a->seq_q;
   p.M = a->seq_kv;
   p.q_per_kv = a->heads_q / a->heads_kv;
-  p.n_mblocks = (a->seq_q + 255) / 256;
+  p.n_mblocks = (a->seq_q + kAttnBM - 1) / kAttnBM;
   p.n_kv_total = (a->seq_kv + 127) / 128;
   p.causal_offset = a->causal_offset;
   p.scale_log2 = a->scale * 1.4426950408889634f;
