@@ -162,7 +162,7 @@ extern "C" int nt_attn_fwd(const nt_attn_args* a, void* stream) {
   p.N = a->seq_q;
   p.M = a->seq_kv;
   p.q_per_kv = a->heads_q / a->heads_kv;
-  p.n_mblocks = (a->seq_q + kAttnBM - 1) / kAttnBM;
+  p.n_mblocks = (a->seq_q + 255) / 256;
   p.n_kv_total = (a->seq_kv + 127) / 128;
   p.causal_offset = a->causal_offset;
   p.scale_log2 = a->scale * 1.4426950408889634f;
@@ -220,14 +220,6 @@ extern "C" int nt_cast_bf16_to_f32(const void* src, float* dst, int64_t n, void*
   g_launches++;
   return check_cuda(cudaGetLastError(), "cast_bf16_f32");
 }
-
-#ifdef NT_TRACE
-extern "C" int nt_debug_set_trace(unsigned long long* buf, int cta) {
-  cudaMemcpyToSymbol(nt::g_nt_trace, &buf, sizeof(buf));
-  cudaMemcpyToSymbol(nt::g_nt_trace_cta, &cta, sizeof(cta));
-  return check_cuda(cudaGetLastError(), "nt_debug_set_trace");
-}
-#endif
 
 extern "C" int nt_abi_version(void) { return NT_ABI_VERSION; }
 extern "C" const char* nt_last_error(void) { return g_last_error.c_str(); }
