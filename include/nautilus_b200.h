@@ -21,6 +21,7 @@
 #ifndef NAUTILUS_B200_H_
 #define NAUTILUS_B200_H_
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -123,6 +124,22 @@ typedef struct nt_chain_args {
 } nt_chain_args;
 int64_t nt_gemm_chain_workspace_bytes(int32_t n, int32_t f, int32_t e);
 int nt_gemm_chain(const nt_chain_args* args, void* stream);
+
+/*
+ * Generic MA programs: MA kernels with no tcgen05
+ * family above (element-wise chains, reductions, small matmuls, fp64
+ * programs, ...) are lowered by paper_2604_14825_b200/simt.py to CUDA C that
+ * mirrors interpret_ma statement by statement (tilecc/ma/interp.py:174-280),
+ * compiled by nvcc to an sm_100a cubin (cached by content hash) and run
+ * through these entry points -- the load / launch / unload surface of
+ * SURVEY.md 8(b).  `image` is a cubin; `fn` is a CUfunction handle; `params`
+ * is the cuLaunchKernel parameter array.  Launches are 1-D.
+ */
+typedef struct nt_module nt_module;
+int nt_module_load(const void* image, size_t nbytes, nt_module** out);
+int nt_module_function(nt_module* module, const char* entry, void** fn);
+int nt_launch(void* fn, uint32_t grid_x, uint32_t block_x, uint32_t smem_bytes, void** params, void* stream);
+int nt_module_unload(nt_module* module);
 
 /* dtype conversion helpers (device buffers) */
 int nt_cast_f32_to_bf16(const float* src, void* dst, int64_t n, void* stream);

@@ -23,6 +23,7 @@ EXPORTED = (
     "nt_attn_fwd", "nt_attn_decode", "nt_decode_workspace_bytes", "nt_decode_num_splits", "nt_gemm",
     "nt_gemm_chain", "nt_gemm_chain_workspace_bytes",
     "nt_cast_f32_to_bf16", "nt_cast_bf16_to_f32", "nt_abi_version", "nt_last_error", "nt_launch_count",
+    "nt_module_load", "nt_module_function", "nt_launch", "nt_module_unload",
 )
 
 
@@ -89,10 +90,16 @@ def lib():
             L.nt_gemm_chain_workspace_bytes.restype = C.c_int64
             L.nt_cast_f32_to_bf16.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
             L.nt_cast_bf16_to_f32.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
+            L.nt_module_load.argtypes = [C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p)]
+            L.nt_module_function.argtypes = [C.c_void_p, C.c_char_p, C.POINTER(C.c_void_p)]
+            L.nt_launch.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(C.c_void_p),
+                                    C.c_void_p]
+            L.nt_module_unload.argtypes = [C.c_void_p]
             L.nt_last_error.restype = C.c_char_p
             L.nt_launch_count.restype = C.c_int64
             for name in ("nt_attn_fwd", "nt_attn_decode", "nt_gemm", "nt_gemm_chain",
-                         "nt_cast_f32_to_bf16", "nt_cast_bf16_to_f32", "nt_abi_version"):
+                         "nt_cast_f32_to_bf16", "nt_cast_bf16_to_f32", "nt_abi_version",
+                         "nt_module_load", "nt_module_function", "nt_launch", "nt_module_unload"):
                 getattr(L, name).restype = C.c_int
             _lib = L
     return _lib

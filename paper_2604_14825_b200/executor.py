@@ -12,8 +12,9 @@ Reference seam:
   adds the batch x head (x GQA) outer grid the reference cannot express;
 * ``device`` -- accepted for signature compatibility (a VirtualDevice or
   ``B200Profile``); the hardware is the device;
-* ``precision`` -- "fp32" (the MA precision; realised as bf16 operands with
-  fp32 accumulation) -- fp64/rational have no device realisation and raise.
+* ``precision`` -- "fp32" (the MA precision: the tcgen05 families realise it
+  as bf16 operands with fp32 accumulation, the SIMT lowering in fp32) or
+  "fp64" (SIMT lowering); the exact "rational" mode is CPU-only and raises.
 
 It returns ``(buffers, ExecReport)`` where ``buffers`` maps every Global
 buffer name to an array (inputs as given, the output computed on the GPU) --
@@ -176,16 +177,58 @@ def _recognize_cached(obj, mod):
     return specs
 
 
+def _execute_simt(module, mod, inputs, prec, stream, return_torch):
+    """Generic MA program on the SIMT lowering (simt.py): interpret_ma semantics in the MA precision."""
+    from . import simt
+
+    report = ExecReport(kernels=len(mod.kernels))
+    static = _static_cached(module, mod)
+    for f in ("bytes_global", "bytes_shared", "bytes_register", "flops", "steps", "modeled_cost"):
+        setattr(report, f, getattr(static, f))
+    l0 = _lib.launch_count()
+    bufs, info = simt.execute(module, inputs, prec, stream=stream, return_torch=return_torch)
+    report.launches = _lib.launch_count() - l0
+    report.device_ms = info["device_ms"]
+    report.realisation.append(info)
+    return bufs, report
+
+
+BACKENDS = ("auto", "tcgen05", "simt")
+
+
 def execute_ma(module, inputs: dict, device=None, precision=None, *, outer=None, mask_kind=None,
-               out_dtype=None, stream=None, timing: bool = True, return_torch: bool = False):
-    """Run an MA module on the B200 (see module docstring)."""
+               out_dtype=None, stream=None, timing: bool = True, return_torch: bool = False,
+               backend: str = "auto"):
+    """Run an MA module on the B200 (see module docstring).
+
+    ``backend``: "tcgen05" runs only the recognised tensor-core families
+    (bf16 operands, fp32 accumulation) and raises ``UnsupportedMA`` for
+    anything else; "simt" runs the generic lowering in the MA precision
+    (fp32 / fp64, interpret_ma's operation order); "auto" (default) uses the
+    tensor-core kernels for fp32 programs they recognise and the SIMT lowering
+    for every other program and for fp64.
+    """
     mod = ir.as_module(module)
     prec = precision if precision is None or isinstance(precision, str) else getattr(precision, "value", precision)
-    if prec not in (None, "fp32"):
+    if backend not in BACKENDS:
+        raise ValueError(f"backend must be one of {BACKENDS}")
+    if prec not in (None, "fp32", "fp64"):
         raise UnsupportedMA(f"precision {prec!r} has no device realisation")
     if not torch.cuda.is_available():
         raise UnsupportedMA("no CUDA device: the B200 executor has no CPU fallback")
-    specs = _recognize_cached(module, mod)
+    eff = prec or mod.precision
+    if backend == "simt" or (backend == "auto" and eff == "fp64"):
+        if outer is not None:
+            raise UnsupportedMA("the runtime outer grid is a tcgen05-family feature")
+        return _execute_simt(module, mod, inputs, prec, stream, return_torch)
+    if eff != "fp32":
+        raise UnsupportedMA(f"precision {eff!r}: the tcgen05 families compute in bf16 / fp32")
+    try:
+        specs = _recognize_cached(module, mod)
+    except UnsupportedMA:
+        if backend == "auto" and outer is None:
+            return _execute_simt(module, mod, inputs, prec, stream, return_torch)
+        raise
     dev = torch.device("cuda", torch.cuda.current_device())
     report = ExecReport(kernels=len(mod.kernels))
     static = _static_cached(module, mod)
