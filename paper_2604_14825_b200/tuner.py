@@ -14,6 +14,9 @@ count as tie-breaker.  Here:
   ``steps`` (static closed form, tilecc/ma/cost.py:66-104) -- no CPU
   interpretation.  Timings are cached per realisation (identical kernels are
   timed once; the reference re-measures duplicates).
+  Programs outside the tensor-core families are timed on their generic SIMT
+  realisation (simt.py), so every schedule the reference can lower is
+  measured on the device.
 * ``search`` restates tilecc's evolutionary loop with a pluggable *batch*
   scorer.  The RNG is consumed only when the population is built and mutated
   (tilecc/tuner/tuner.py:166-171, 196-202), never while scoring, so scoring a
@@ -31,6 +34,7 @@ import statistics
 from typing import Callable, Optional, Sequence
 
 from . import cost, ma_ir
+from .errors import UnsupportedMA
 from .frontdoor import import_tilecc
 from .recognize import AttentionSpec, GemmChainSpec, recognize
 
@@ -72,17 +76,49 @@ class DeviceScorer:
         import_tilecc()
         ma_full = _lower(base_full, schedule, assignment, device)
         mod = ma_ir.from_tilecc(ma_full)
-        specs = recognize(mod)  # UnsupportedMA is a CompilerError -> +inf in search
-        for s in specs:
-            if cost.b200_viable(s):
-                return float("inf"), 0
-        key = tuple(realisation_key(s, self.outer, self.mask_kind) for s in specs)
-        if key not in self.cache:
-            self.cache[key] = self._time(mod, specs)
-            self.timed += 1
+        try:
+            specs = recognize(mod)
+        except UnsupportedMA:
+            if self.outer is not None:
+                raise  # the outer grid is a tcgen05-family feature -> +inf in search
+            specs = None
+        if specs is None:
+            # no tensor-core family: time the generic SIMT realisation (simt.py)
+            from . import simt
+            key = ("simt", simt.lower(mod).digest)
+            if key not in self.cache:
+                self.cache[key] = self._time_simt(mod)
+                self.timed += 1
+        else:
+            for s in specs:
+                if cost.b200_viable(s):
+                    return float("inf"), 0
+            key = tuple(realisation_key(s, self.outer, self.mask_kind) for s in specs)
+            if key not in self.cache:
+                self.cache[key] = self._time(mod, specs)
+                self.timed += 1
         ma_p = _lower(base_probe, schedule, assignment, device)
         proxy = cost.cost_model(ma_ir.from_tilecc(ma_p)).steps
         return self.cache[key], proxy
+
+    def _time_simt(self, mod) -> float:
+        import numpy as np
+        import torch
+
+        from .executor import execute_ma
+
+        if self.cuda_device is not None:
+            torch.cuda.set_device(self.cuda_device)
+        rng = np.random.default_rng(0)
+        inputs = {b.name: torch.from_numpy(rng.standard_normal(tuple(b.shape)).astype(np.float32)).cuda()
+                  for b in mod.inputs()}
+        for _ in range(self.warmup):
+            execute_ma(mod, inputs, backend="simt", return_torch=True)
+        times = []
+        for _ in range(self.reps):
+            _, rep = execute_ma(mod, inputs, backend="simt", return_torch=True)
+            times.append(rep.device_ms * 1e3)
+        return float(statistics.median(times))
 
     def _time(self, mod, specs) -> float:
         import numpy as np
