@@ -150,6 +150,100 @@ def _prepare_attention(spec: AttentionSpec, module: ir.Module, inputs: dict, out
     return plan, o, outer
 
 
+def _streamable(spec, inputs, outer, mask_kind, out) -> bool:
+    if out is None or out.is_cuda:
+        return False
+    xs = [inputs[spec.q], inputs[spec.k], inputs[spec.v]]
+    if not all(isinstance(x, torch.Tensor) and not x.is_cuda for x in xs):
+        return False
+    if outer is None and xs[0].dim() != 4:
+        return False
+    if spec.mask is not None and not (mask_kind == "causal" and spec.mask not in inputs):
+        return False  # explicit mask tensors take the resident path
+    return mask_kind in (None, "none", "causal", "auto") and spec.d == spec.dv
+
+
+def _attention_streamed(spec: AttentionSpec, inputs: dict, outer, mask_kind, out: torch.Tensor, dev,
+                        chunks: int):
+    """Chunked H2D -> kernel -> D2H pipeline over (batch, kv-head) groups (see execute_ma)."""
+    q_h, k_h, v_h = inputs[spec.q], inputs[spec.k], inputs[spec.v]
+    if outer is None:
+        outer = (q_h.shape[0], q_h.shape[1], k_h.shape[1])
+    B, Hq, Hkv = outer
+    g = Hq // Hkv
+    q_h = q_h.reshape(B, Hq, spec.n, spec.d)
+    k_h = k_h.reshape(B, Hkv, spec.m, spec.d)
+    v_h = v_h.reshape(B, Hkv, spec.m, spec.dv)
+    o_h = out.reshape(B, Hq, spec.n, spec.dv)
+    kind = "causal" if (mask_kind == "causal" or spec.mask is not None) else "none"
+    odt = o_h.dtype
+    if odt not in (torch.bfloat16, torch.float32):
+        raise UnsupportedMA("streamed output must be bf16 or fp32")
+    cast = q_h.dtype != torch.bfloat16
+    q_d = torch.empty(q_h.shape, dtype=q_h.dtype, device=dev)
+    k_d = torch.empty(k_h.shape, dtype=k_h.dtype, device=dev)
+    v_d = torch.empty(v_h.shape, dtype=v_h.dtype, device=dev)
+    o_d = torch.empty(o_h.shape, dtype=odt, device=dev)
+    comp = torch.cuda.current_stream(dev)
+    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    s_in.wait_stream(comp)  # device buffers were allocated on the compute stream
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    units = B * Hkv
+    n = max(1, min(chunks, units))
+    bounds = [units * i // n for i in range(n + 1)]
+    pieces = []  # (b, h0, h1) kv-head ranges inside one batch entry
+    for c in range(n):
+        u, u1 = bounds[c], bounds[c + 1]
+        while u < u1:
+            b, h0 = divmod(u, Hkv)
+            h1 = min(Hkv, h0 + (u1 - u))
+            pieces.append((c, b, h0, h1))
+            u += h1 - h0
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(comp)
+    flops, launches, plans = 0.0, 0, []
+    for c in range(n):
+        mine = [p for p in pieces if p[0] == c]
+        with torch.cuda.stream(s_in):
+            for _, b, h0, h1 in mine:
+                q_d[b, h0 * g:h1 * g].copy_(q_h[b, h0 * g:h1 * g], non_blocking=True)
+                k_d[b, h0:h1].copy_(k_h[b, h0:h1], non_blocking=True)
+                v_d[b, h0:h1].copy_(v_h[b, h0:h1], non_blocking=True)
+        comp.wait_stream(s_in)
+        for _, b, h0, h1 in mine:
+            qv, kv, vv = q_d[b, h0 * g:h1 * g][None], k_d[b, h0:h1][None], v_d[b, h0:h1][None]
+            if cast:
+                qv, kv, vv = to_bf16(qv), to_bf16(kv), to_bf16(vv)
+            ov = o_d[b, h0 * g:h1 * g][None]
+            rows = g * spec.n
+            if decode_eligible(rows, spec.d, kind) and spec.m >= 1024:
+                plan = DecodePlan(qv, kv, vv, ov, spec.scale, err_flag=err)
+            else:
+                plan = AttentionPlan(qv, kv, vv, ov, spec.scale, kind, err_flag=err)
+            plan.launch(comp)
+            plans.append(plan)  # keep argument structs / workspaces alive until the sync
+            flops += plan.flops()
+            launches += 1
+        s_out.wait_stream(comp)
+        with torch.cuda.stream(s_out):
+            for _, b, h0, h1 in mine:
+                o_h[b, h0 * g:h1 * g].copy_(o_d[b, h0 * g:h1 * g], non_blocking=True)
+    comp.wait_stream(s_out)
+    ev1.record(comp)
+    ev1.synchronize()
+    for t in (q_d, k_d, v_d, o_d):
+        t.record_stream(s_in)
+        t.record_stream(s_out)
+    flag = int(err.item())
+    if flag & 1:
+        raise DivisionByZero("tile divide: softmax denominator is zero (row fully masked)")
+    if flag & 0x100:
+        raise RuntimeError(f"device pipeline timeout (code {flag & 0xff})")
+    info = {"kernel": type(plans[0]).__name__, "streamed": True, "chunks": n, "mask": kind,
+            "launches": launches, "ma_tile": (spec.block_m, spec.block_n)}
+    return out, ev0.elapsed_time(ev1), flops, info
+
+
 _SPEC_CACHE: dict = {}
 _COST_CACHE: dict = {}
 
@@ -198,7 +292,7 @@ BACKENDS = ("auto", "tcgen05", "simt")
 
 def execute_ma(module, inputs: dict, device=None, precision=None, *, outer=None, mask_kind=None,
                out_dtype=None, stream=None, timing: bool = True, return_torch: bool = False,
-               backend: str = "auto"):
+               backend: str = "auto", out: Optional[torch.Tensor] = None, chunks: int = 4):
     """Run an MA module on the B200 (see module docstring).
 
     ``backend``: "tcgen05" runs only the recognised tensor-core families
@@ -207,6 +301,13 @@ def execute_ma(module, inputs: dict, device=None, precision=None, *, outer=None,
     (fp32 / fp64, interpret_ma's operation order); "auto" (default) uses the
     tensor-core kernels for fp32 programs they recognise and the SIMT lowering
     for every other program and for fp64.
+
+    ``out``: optional preallocated tensor (host or device) that receives the
+    module output.  With host (CPU) q/k/v inputs over an outer grid and a host
+    ``out``, the attention path is *streamed*: the (batch, kv-head) groups are
+    split into ``chunks`` pieces whose host->device copies, kernels and
+    device->host copies run on three streams, so PCIe transfers overlap the
+    kernels (pinned host memory makes the copies asynchronous).
     """
     mod = ir.as_module(module)
     prec = precision if precision is None or isinstance(precision, str) else getattr(precision, "value", precision)
@@ -238,7 +339,13 @@ def execute_ma(module, inputs: dict, device=None, precision=None, *, outer=None,
     l0 = _lib.launch_count()
     for spec in specs:
         report.specs.append(spec)
-        if isinstance(spec, AttentionSpec):
+        if isinstance(spec, AttentionSpec) and _streamable(spec, inputs, outer, mask_kind, out):
+            o, ms, fl, info = _attention_streamed(spec, inputs, outer, mask_kind, out, dev, chunks)
+            report.realisation.append(info)
+            report.device_ms += ms
+            report.algorithmic_flops += fl
+            outputs[spec.o] = o
+        elif isinstance(spec, AttentionSpec):
             plan, o, outer_used = _prepare_attention(spec, mod, inputs, outer, mask_kind, out_dtype, dev)
             if isinstance(plan, DecodePlan):
                 report.realisation.append({"kernel": "attn_decode_splitkv", "mask": "none",
@@ -256,10 +363,16 @@ def execute_ma(module, inputs: dict, device=None, precision=None, *, outer=None,
             report.device_ms += ev0.elapsed_time(ev1)
             report.algorithmic_flops += plan.flops()
             res = o if outer_used is not None else o[0, 0]
+            if out is not None and spec.o == mod.output:
+                out.copy_(res.reshape(out.shape))
+                res = out
             outputs[spec.o] = res
         elif isinstance(spec, GemmChainSpec):
             from .gemm import run_gemm_chain
             y, ms, fl, info = run_gemm_chain(spec, inputs, dev, out_dtype)
+            if out is not None and spec.y == mod.output:
+                out.copy_(y.reshape(out.shape))
+                y = out
             report.realisation.append(info)
             report.device_ms += ms
             report.algorithmic_flops += fl
