@@ -67,6 +67,11 @@ typedef struct nt_attn_args {
   int64_t mask_stride_row;
   int32_t out_dtype; /* NT_DTYPE_BF16 | NT_DTYPE_F32 */
   int32_t* err_flag; /* device int32 or NULL: bit0 = zero softmax denominator */
+  /* device int32[2], zero before the first launch, or NULL.  The kernel is
+   * persistent (one CTA per SM); with a counter the CTAs draw work items
+   * greedily in LPT order and the last CTA resets it, so one counter serves
+   * every launch ordered on one stream.  NULL = static round-robin items. */
+  int32_t* work_counter;
 } nt_attn_args;
 int nt_attn_fwd(const nt_attn_args* args, void* stream);
 

@@ -11,15 +11,23 @@
 //   O' = dot(P, V, acc = O * a)
 //   O  = O / l   after the loop (telescoped division)
 //
-// CTA = two 128-row query tiles (256 rows = 256/t0_i consecutive MA blocks)
-// sharing each 128-row K/V tile (128/t0_j consecutive MA j0 iterations; the
-// rolling-update law makes the coarsening exact up to rounding).
+// Work item = two 128-row query tiles (256 rows = 256/t0_i consecutive MA
+// blocks) of one (batch, head), sharing each 128-row K/V tile (128/t0_j
+// consecutive MA j0 iterations; the rolling-update law makes the coarsening
+// exact up to rounding).  The kernel is PERSISTENT: a grid of at most one CTA
+// per SM walks the item list (heaviest causal items first), each CTA drawing
+// its next item from a global counter when it starts one (greedy LPT, like the
+// hardware block scheduler), and keeps TMEM, barriers and the K/V ring alive
+// across items, so the next item's Q load and first score GEMMs overlap the
+// current item's epilogue.  The producer warp draws items and hands them to
+// the MMA and softmax warps through a small ring in shared memory.
 //
-//   warp 0      TMA producer: Q0,Q1 once, then K0,V0,K1,V1,... into a STAGES ring
+//   warp 0      TMA producer: per item Q0,Q1 (once their previous contents are
+//               consumed), then K0,V0,K1,V1,... into a STAGES ring
 //   warp 1      MMA issuer (one thread): S_t = Q_t K_j^T (SS), O_t += P_t V_j (TS, P from TMEM)
 //   warps 2-3   idle (warpgroup 0 donates registers via setmaxnreg)
-//   warps 4-7   softmax for tile 0 (one thread per query row = TMEM lane)
-//   warps 8-11  softmax for tile 1
+//   warps 4-7   softmax + epilogue for tile 0 (one thread per query row = TMEM lane)
+//   warps 8-11  softmax + epilogue for tile 1
 // TMEM (512 cols): S0 [0,128) S1 [128,256) O0 [256,256+D) O1 [384,384+D);
 // P_t (bf16, 64 cols) aliases the first half of S_t.
 //
@@ -41,23 +49,24 @@ enum { MASK_NONE = 0, MASK_CAUSAL = 1, MASK_TENSOR = 2 };
 struct AttnFwdParams {
   int B, Hq, Hkv, N, M;
   int q_per_kv;
-  int n_mblocks;    // ceil(N / 256)
-  int n_kv_total;   // ceil(M / 128)
+  int n_mblocks;      // ceil(N / 256)
+  int n_kv_total;     // ceil(M / 128)
+  int n_items;        // n_mblocks * B * Hq
   int causal_offset;  // key j visible to query i iff j <= i + causal_offset
   float scale_log2;   // c * log2(e)
   const float* mask;  // MASK_TENSOR: fp32 [N, M]
   long long mask_row_stride;
-  float* o_f32;  // fp32 output (OUT_F32), element strides below
+  void* o;            // output (bf16, or fp32 if OUT_F32), element strides below; D contiguous
   long long o_sb, o_sh, o_sn;
   int* err;  // bit 0: zero denominator (fully masked row); 0x100|k: pipeline timeout
+  int* work;  // [next, done] dynamic item counter (zero at launch, reset by the last CTA) or null
 };
 
 constexpr int kAttnThreads = 384;
+constexpr int kItemRing = 4;  // work-item slots handed from the producer to the MMA / softmax warps
 constexpr float kRescaleLog2 = 8.0f;
 // Fraction of exp2 evaluated by the FMA-pipe polynomial instead of MUFU.EX2
-// (1 in NT_POLY_EVERY pairs; 0 = MUFU only).  Measured on B200 at Llama 8K
-// causal: 0 -> 1177, 8 -> 1163, 4 -> 1157, 2 -> 1107 TFLOP/s (profiles/), so
-// the MUFU is not the binding pipe of this kernel yet: off by default.
+// (1 in NT_POLY_EVERY pairs; 0 = MUFU only).
 #ifndef NT_POLY_EVERY
 #define NT_POLY_EVERY 0
 #endif
@@ -70,21 +79,62 @@ struct AttnCfg {
   static constexpr int HALF = 128 * 64 * 2;  // one 128-row x 64-col bf16 swizzle-128B panel
   static constexpr int TQ = BM * D * 2;
   static constexpr int TKV = BN * D * 2;
-  static constexpr int STAGES = (D == 128) ? 4 : 6;
+  static constexpr int STAGES = (D == 128) ? 4 : 8;
   static constexpr int SMEM_Q = 0;
   static constexpr int SMEM_KV = 2 * TQ;
   static constexpr int SMEM_BAR = SMEM_KV + STAGES * TKV;
-  static constexpr int NBAR = 2 + 2 * STAGES + 2 + 2 + 2;
-  static constexpr int SMEM_BYTES = SMEM_BAR + NBAR * 8 + 16 + 1024;  // + alignment slack
+  static constexpr int NBAR = 2 + 2 + 2 * STAGES + 2 + 2 + 2 + 2 * kItemRing;
+  static constexpr int SMEM_BYTES = SMEM_BAR + NBAR * 8 + 16 + 4 * kItemRing + 1024;  // + alignment slack
 };
 
 __device__ __forceinline__ float f_ninf() { return __int_as_float(0xff800000); }
 
+#ifdef NT_TRACE
+// Debug timeline (NT_TRACE builds only): clock64 stamps of one CTA's pipeline
+// for its first work item.  trace[(role * 64 + iter) * 8 + event]; role 0 MMA,
+// 1/2 softmax tile 0/1, 3 producer.
+__device__ unsigned long long* g_nt_trace = nullptr;
+__device__ int g_nt_trace_cta = 0;
+#define NT_STAMP(role, iter, ev)                                                               \
+  do {                                                                                         \
+    if (g_nt_trace && blockIdx.x == g_nt_trace_cta && (iter) < 64)                             \
+      g_nt_trace[((role) * 64 + (iter)) * 8 + (ev)] = clock64();                               \
+  } while (0)
+#else
+#define NT_STAMP(role, iter, ev) do {} while (0)
+#endif
+
+// Work item -> coordinates.  Items are ordered heaviest first for causal masks
+// (largest query block first: LPT over the strided CTA assignment).
+struct AttnItem {
+  int b, hq, hkv, q_row0, n_kv;
+};
+
+template <int MASK>
+__device__ __forceinline__ AttnItem attn_item(const AttnFwdParams& p, int w) {
+  const int BH = p.B * p.Hq;
+  const int bh = w % BH;
+  const int mbi = w / BH;
+  const int mb = (MASK == MASK_CAUSAL) ? (p.n_mblocks - 1 - mbi) : mbi;
+  AttnItem it;
+  it.hq = bh % p.Hq;
+  it.b = bh / p.Hq;
+  it.hkv = it.hq / p.q_per_kv;
+  it.q_row0 = mb * 256;
+  int n_kv = p.n_kv_total;
+  if (MASK == MASK_CAUSAL) {
+    const int last_q = min(it.q_row0 + 255, p.N - 1) + p.causal_offset;
+    n_kv = min(n_kv, last_q / 128 + 1);
+    n_kv = max(n_kv, 1);
+  }
+  it.n_kv = n_kv;
+  return it;
+}
+
 template <int D, int MASK, bool OUT_F32>
 __global__ void __launch_bounds__(kAttnThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
-                    const AttnFwdParams p) {
+                    const __grid_constant__ CUtensorMap tmV, const AttnFwdParams p) {
   using C = AttnCfg<D>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_u32 = smem_u32(smem_raw);
@@ -93,48 +143,39 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   uint8_t* sQ = smem + C::SMEM_Q;
   uint8_t* sKV = smem + C::SMEM_KV;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::SMEM_BAR);
-  uint64_t* bar_q = bars;                      // [2]
-  uint64_t* bar_kv_full = bars + 2;            // [STAGES]
-  uint64_t* bar_kv_empty = bars + 2 + C::STAGES;  // [STAGES]
-  uint64_t* bar_s_full = bars + 2 + 2 * C::STAGES;  // [2]
-  uint64_t* bar_p_full = bar_s_full + 2;            // [2]
-  uint64_t* bar_o_full = bar_p_full + 2;            // [2]
+  uint64_t* bar_q = bars;                            // [2] Q_t landed
+  uint64_t* bar_q_empty = bars + 2;                  // [2] last S_t of the item done (Q_t reusable)
+  uint64_t* bar_kv_full = bars + 4;                  // [STAGES]
+  uint64_t* bar_kv_empty = bars + 4 + C::STAGES;     // [STAGES]
+  uint64_t* bar_s_full = bars + 4 + 2 * C::STAGES;   // [2]
+  uint64_t* bar_p_full = bar_s_full + 2;             // [2]
+  uint64_t* bar_o_full = bar_p_full + 2;             // [2]
+  uint64_t* bar_item_full = bar_o_full + 2;          // [kItemRing] item index published
+  uint64_t* bar_item_empty = bar_item_full + kItemRing;  // [kItemRing] read by MMA + 8 softmax warps
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBAR);
+  int* item_ring = reinterpret_cast<int*>(tmem_slot + 4);
 
   const int warp = __shfl_sync(0xffffffffu, threadIdx.x / 32, 0);
   const int lane = threadIdx.x & 31;
-
-  // ---- tile coordinates (causal: heaviest query blocks first -> LPT order)
-  const int BH = p.B * p.Hq;
-  const int bh = blockIdx.x % BH;
-  const int mbi = blockIdx.x / BH;
-  const int mb = (MASK == MASK_CAUSAL) ? (p.n_mblocks - 1 - mbi) : mbi;
-  const int hq = bh % p.Hq;
-  const int b = bh / p.Hq;
-  const int hkv = hq / p.q_per_kv;
-  const int q_row0 = mb * 256;
-  int n_kv = p.n_kv_total;
-  if (MASK == MASK_CAUSAL) {
-    const int last_q = min(q_row0 + 255, p.N - 1) + p.causal_offset;
-    n_kv = min(n_kv, last_q / 128 + 1);
-    n_kv = max(n_kv, 1);
-  }
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmQ);
     prefetch_tmap(&tmK);
     prefetch_tmap(&tmV);
-    if (!OUT_F32) prefetch_tmap(&tmO);
-    mbar_init(&bar_q[0], 1);
-    mbar_init(&bar_q[1], 1);
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&bar_q[t], 1);
+      mbar_init(&bar_q_empty[t], 1);
+      mbar_init(&bar_s_full[t], 1);
+      mbar_init(&bar_p_full[t], 4);
+      mbar_init(&bar_o_full[t], 1);
+    }
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&bar_kv_full[s], 1);
       mbar_init(&bar_kv_empty[s], 1);
     }
-    for (int t = 0; t < 2; ++t) {
-      mbar_init(&bar_s_full[t], 1);
-      mbar_init(&bar_p_full[t], 4);
-      mbar_init(&bar_o_full[t], 1);
+    for (int s = 0; s < kItemRing; ++s) {
+      mbar_init(&bar_item_full[s], 1);
+      mbar_init(&bar_item_empty[s], 9);
     }
     fence_barrier_init();
   }
@@ -145,91 +186,127 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp < 4) {
-  asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
-  if (warp == 0) {
-    // ================= TMA producer
-    if (lane == 0) {
-      for (int t = 0; t < 2; ++t) {
-        mbar_arrive_expect_tx(&bar_q[t], C::TQ);
+    // setmaxnreg only redistributes the launch allocation (384 x 168 = 64512
+    // registers): 128 x 72 + 256 x 216 = 64512
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
+    if (warp == 0) {
+      // ================= TMA producer
+      if (lane == 0) {
+        int kv_base = 0;
+        for (int li = 0;; ++li) {
+          // ---- schedule: first item static, then greedy (LPT order) from the global counter
+          const int slot_i = li % kItemRing;
+          if (li >= kItemRing) mbar_wait(&bar_item_empty[slot_i], ((li / kItemRing) - 1) & 1, p.err, 12);
+          int w;
+          if (li == 0) w = blockIdx.x;
+          else if (p.work) w = gridDim.x + atomicAdd(p.work, 1);
+          else w = blockIdx.x + li * gridDim.x;
+          item_ring[slot_i] = w;
+          mbar_arrive(&bar_item_full[slot_i]);
+          if (w >= p.n_items) break;
+          const AttnItem itm = attn_item<MASK>(p, w);
+          for (int t = 0; t < 2; ++t) {
+            if (li > 0) mbar_wait(&bar_q_empty[t], (li - 1) & 1, p.err, 11);
+            mbar_arrive_expect_tx(&bar_q[t], C::TQ);
 #pragma unroll
-        for (int h = 0; h < D / 64; ++h)
-          tma_load_4d(sQ + t * C::TQ + h * C::HALF, &tmQ, &bar_q[t], h * 64, q_row0 + t * 128, hq, b);
-      }
-      for (int it = 0; it < 2 * n_kv; ++it) {
-        const int slot = it % C::STAGES;
-        const uint32_t ph = (it / C::STAGES) & 1;
-        mbar_wait(&bar_kv_empty[slot], ph ^ 1, p.err, 1);
-        mbar_arrive_expect_tx(&bar_kv_full[slot], C::TKV);
-        const CUtensorMap* m = (it & 1) ? &tmV : &tmK;
-        const int row = (it >> 1) * 128;
-#pragma unroll
-        for (int h = 0; h < D / 64; ++h)
-          tma_load_4d(sKV + slot * C::TKV + h * C::HALF, m, &bar_kv_full[slot], h * 64, row, hkv, b);
-      }
-    }
-  } else if (warp == 1) {
-    // ================= MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idS = idesc_bf16(128, 128, 0, 0);
-      constexpr uint32_t idO = idesc_bf16(128, D, 0, 1);
-      const uint32_t sQa = smem_u32(sQ), sKVa = smem_u32(sKV);
-      auto issue_s = [&](int t, int slot) {
-#pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint32_t off = (k >> 2) * C::HALF + (k & 3) * 32;
-          const uint64_t a = sdesc_sw128(sQa + t * C::TQ + off, 16, 1024);
-          const uint64_t bd = sdesc_sw128(sKVa + slot * C::TKV + off, 16, 1024);
-          umma_ss(tmem + t * 128, a, bd, idS, k > 0 ? 1u : 0u);
-        }
-      };
-      auto issue_pv = [&](int t, int slot, bool acc) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint64_t bd = sdesc_sw128(sKVa + slot * C::TKV + k * 2048, C::HALF, 1024);
-          umma_ts(tmem + 256 + t * 128, tmem + t * 128 + k * 8, bd, idO, (acc || k > 0) ? 1u : 0u);
-        }
-      };
-      mbar_wait(&bar_q[0], 0, p.err, 2);
-      mbar_wait(&bar_q[1], 0, p.err, 2);
-      tc_fence_after();
-      for (int j = 0; j < n_kv; ++j) {
-        const int itK = 2 * j;
-        const int slotK = itK % C::STAGES;
-        mbar_wait(&bar_kv_full[slotK], (itK / C::STAGES) & 1, p.err, 3);
-        tc_fence_after();
-        const int itV = 2 * (j - 1) + 1;
-        const int slotV = (itV + C::STAGES) % C::STAGES;
-        for (int t = 0; t < 2; ++t) {
-          if (j > 0) {
-            mbar_wait(&bar_p_full[t], (j - 1) & 1, p.err, 4);
-            if (t == 0) mbar_wait(&bar_kv_full[slotV], (itV / C::STAGES) & 1, p.err, 5);
-            tc_fence_after();
-  #ifndef NT_EXP_NO_PV
-          issue_pv(t, slotV, j - 1 > 0);
-#endif
-            if (t == 1) umma_commit(&bar_kv_empty[slotV]);
+            for (int h = 0; h < D / 64; ++h)
+              tma_load_4d(sQ + t * C::TQ + h * C::HALF, &tmQ, &bar_q[t], h * 64, itm.q_row0 + t * 128, itm.hq,
+                          itm.b);
           }
-#ifndef NT_EXP_NO_S
-          issue_s(t, slotK);
-#endif
-          umma_commit(&bar_s_full[t]);
+          for (int it = 0; it < 2 * itm.n_kv; ++it) {
+            const int g = kv_base + it;
+            const int slot = g % C::STAGES;
+            const uint32_t ph = (g / C::STAGES) & 1;
+            if (li == 0) NT_STAMP(3, it >> 1, (it & 1) * 2);
+            mbar_wait(&bar_kv_empty[slot], ph ^ 1, p.err, 1);
+            if (li == 0) NT_STAMP(3, it >> 1, (it & 1) * 2 + 1);
+            mbar_arrive_expect_tx(&bar_kv_full[slot], C::TKV);
+            const CUtensorMap* m = (it & 1) ? &tmV : &tmK;
+            const int row = (it >> 1) * 128;
+#pragma unroll
+            for (int h = 0; h < D / 64; ++h)
+              tma_load_4d(sKV + slot * C::TKV + h * C::HALF, m, &bar_kv_full[slot], h * 64, row, itm.hkv, itm.b);
+          }
+          kv_base += 2 * itm.n_kv;
         }
-        umma_commit(&bar_kv_empty[slotK]);
       }
-      const int itV = 2 * (n_kv - 1) + 1;
-      const int slotV = itV % C::STAGES;
-      for (int t = 0; t < 2; ++t) {
-        mbar_wait(&bar_p_full[t], (n_kv - 1) & 1, p.err, 6);
-        if (t == 0) mbar_wait(&bar_kv_full[slotV], (itV / C::STAGES) & 1, p.err, 7);
-        tc_fence_after();
-        issue_pv(t, slotV, n_kv - 1 > 0);
-        umma_commit(&bar_o_full[t]);
+    } else if (warp == 1) {
+      // ================= MMA issuer
+      if (lane == 0) {
+        constexpr uint32_t idS = idesc_bf16(128, 128, 0, 0);
+        constexpr uint32_t idO = idesc_bf16(128, D, 0, 1);
+        const uint32_t sQa = smem_u32(sQ), sKVa = smem_u32(sKV);
+        auto issue_s = [&](int t, int slot) {
+#pragma unroll
+          for (int k = 0; k < D / 16; ++k) {
+            const uint32_t off = (k >> 2) * C::HALF + (k & 3) * 32;
+            const uint64_t a = sdesc_sw128(sQa + t * C::TQ + off, 16, 1024);
+            const uint64_t bd = sdesc_sw128(sKVa + slot * C::TKV + off, 16, 1024);
+            umma_ss(tmem + t * 128, a, bd, idS, k > 0 ? 1u : 0u);
+          }
+        };
+        auto issue_pv = [&](int t, int slot, bool acc) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const uint64_t bd = sdesc_sw128(sKVa + slot * C::TKV + k * 2048, C::HALF, 1024);
+            umma_ts(tmem + 256 + t * 128, tmem + t * 128 + k * 8, bd, idO, (acc || k > 0) ? 1u : 0u);
+          }
+        };
+        int kv_base = 0;
+        uint32_t p_phase[2] = {0u, 0u};
+        for (int li = 0;; ++li) {
+          const int slot_i = li % kItemRing;
+          mbar_wait(&bar_item_full[slot_i], (li / kItemRing) & 1, p.err, 13);
+          const int w = item_ring[slot_i];
+          mbar_arrive(&bar_item_empty[slot_i]);
+          if (w >= p.n_items) break;
+          const int n_kv = attn_item<MASK>(p, w).n_kv;
+          mbar_wait(&bar_q[0], li & 1, p.err, 2);
+          mbar_wait(&bar_q[1], li & 1, p.err, 2);
+          tc_fence_after();
+          for (int j = 0; j < n_kv; ++j) {
+            const int gK = kv_base + 2 * j;
+            const int slotK = gK % C::STAGES;
+            if (li == 0) NT_STAMP(0, j, 0);
+            mbar_wait(&bar_kv_full[slotK], (gK / C::STAGES) & 1, p.err, 3);
+            if (li == 0) NT_STAMP(0, j, 1);
+            tc_fence_after();
+            const int gV = gK - 1;  // V_{j-1}
+            const int slotV = (gV + C::STAGES) % C::STAGES;
+            for (int t = 0; t < 2; ++t) {
+              if (j > 0) {
+                mbar_wait(&bar_p_full[t], p_phase[t], p.err, 4);
+                p_phase[t] ^= 1u;
+                if (li == 0) NT_STAMP(0, j, 2 + 2 * t);
+                if (t == 0) mbar_wait(&bar_kv_full[slotV], (gV / C::STAGES) & 1, p.err, 5);
+                tc_fence_after();
+                issue_pv(t, slotV, j - 1 > 0);
+                if (t == 1) umma_commit(&bar_kv_empty[slotV]);
+              }
+              issue_s(t, slotK);
+              umma_commit(&bar_s_full[t]);
+              if (j == n_kv - 1) umma_commit(&bar_q_empty[t]);
+              if (li == 0) NT_STAMP(0, j, 3 + 2 * t);
+            }
+            umma_commit(&bar_kv_empty[slotK]);
+          }
+          const int gV = kv_base + 2 * (n_kv - 1) + 1;
+          const int slotV = gV % C::STAGES;
+          for (int t = 0; t < 2; ++t) {
+            mbar_wait(&bar_p_full[t], p_phase[t], p.err, 6);
+            p_phase[t] ^= 1u;
+            if (t == 0) mbar_wait(&bar_kv_full[slotV], (gV / C::STAGES) & 1, p.err, 7);
+            tc_fence_after();
+            issue_pv(t, slotV, n_kv - 1 > 0);
+            umma_commit(&bar_o_full[t]);
+          }
+          umma_commit(&bar_kv_empty[slotV]);
+          kv_base += 2 * n_kv;
+        }
       }
-      umma_commit(&bar_kv_empty[slotV]);
     }
-  }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 216;");
     // ================= softmax (+ lazy O correction + epilogue), one thread per query row
     const int t = (warp - 4) / 4;
     const int wq = warp & 3;  // TMEM sub-partition this warp may access
@@ -237,164 +314,146 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
     const uint32_t tS = tmem + t * 128 + lane_off;
     const uint32_t tO = tmem + 256 + t * 128 + lane_off;
-    const int qi = q_row0 + t * 128 + r;
     const float NINF = f_ninf();
     const float sc = (MASK == MASK_TENSOR) ? 1.0f : p.scale_log2;
-    float m_run = NINF, l_run = 0.f;
+    uint32_t s_phase = 0u;
+    for (int li = 0;; ++li) {
+      const int slot_i = li % kItemRing;
+      mbar_wait(&bar_item_full[slot_i], (li / kItemRing) & 1, p.err, 14);
+      const int w = item_ring[slot_i];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_item_empty[slot_i]);
+      if (w >= p.n_items) break;
+      const AttnItem itm = attn_item<MASK>(p, w);
+      const int qi = itm.q_row0 + t * 128 + r;
+      float m_run = NINF, l_run = 0.f;
 
-    for (int j = 0; j < n_kv; ++j) {
-      mbar_wait(&bar_s_full[t], j & 1, p.err, 8);
-      tc_fence_after();
-      uint32_t s[128];
+      for (int j = 0; j < itm.n_kv; ++j) {
+        if (li == 0 && lane == 0 && wq == 0) NT_STAMP(1 + t, j, 0);
+        mbar_wait(&bar_s_full[t], s_phase, p.err, 8);
+        s_phase ^= 1u;
+        if (li == 0 && lane == 0 && wq == 0) NT_STAMP(1 + t, j, 1);
+        tc_fence_after();
+        uint32_t s[128];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, s + c * 32);
-      tmem_wait_ld();
-      const int kv0 = j * 128;
-      if (MASK == MASK_TENSOR) {
-        const float* mrow = p.mask + (long long)min(qi, p.N - 1) * p.mask_row_stride;
+        for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, s + c * 32);
+        tmem_wait_ld();
+        if (li == 0 && lane == 0 && wq == 0) NT_STAMP(1 + t, j, 2);
+        const int kv0 = j * 128;
+        if (MASK == MASK_TENSOR) {
+          const float* mrow = p.mask + (long long)min(qi, p.N - 1) * p.mask_row_stride;
 #pragma unroll
-        for (int c = 0; c < 128; ++c) {
-          const int kv = kv0 + c;
-          const float mk = (kv < p.M) ? __ldg(mrow + kv) : NINF;
-          s[c] = __float_as_uint(fmaf(__uint_as_float(s[c]), p.scale_log2, mk * 1.4426950408889634f));
+          for (int c = 0; c < 128; ++c) {
+            const int kv = kv0 + c;
+            const float mk = (kv < p.M) ? __ldg(mrow + kv) : NINF;
+            s[c] = __float_as_uint(fmaf(__uint_as_float(s[c]), p.scale_log2, mk * 1.4426950408889634f));
+          }
+        } else {
+          const int lim = (MASK == MASK_CAUSAL) ? min(qi + p.causal_offset, p.M - 1) : (p.M - 1);
+          if (kv0 + 127 > lim) {
+#pragma unroll
+            for (int c = 0; c < 128; ++c)
+              if (kv0 + c > lim) s[c] = __float_as_uint(NINF);
+          }
         }
-      } else {
-        const int lim = (MASK == MASK_CAUSAL) ? min(qi + p.causal_offset, p.M - 1) : (p.M - 1);
-        if (kv0 + 127 > lim) {
+        float mx;
+        {
+          // tree max with 3-input FMNMX3, 4 independent chains
+          float a0 = __uint_as_float(s[0]), a1 = __uint_as_float(s[1]);
+          float a2 = __uint_as_float(s[2]), a3 = __uint_as_float(s[3]);
 #pragma unroll
-          for (int c = 0; c < 128; ++c)
-            if (kv0 + c > lim) s[c] = __float_as_uint(NINF);
+          for (int c = 4; c < 128; c += 8) {
+            a0 = fmax3(a0, __uint_as_float(s[c]), __uint_as_float(s[c + 1]));
+            a1 = fmax3(a1, __uint_as_float(s[c + 2]), __uint_as_float(s[c + 3]));
+            a2 = fmax3(a2, __uint_as_float(s[c + 4]), __uint_as_float(s[c + 5]));
+            if (c + 7 < 128) a3 = fmax3(a3, __uint_as_float(s[c + 6]), __uint_as_float(s[c + 7]));
+            else a3 = fmaxf(a3, __uint_as_float(s[c + 6]));
+          }
+          mx = fmaxf(fmax3(a0, a1, a2), a3);
         }
-      }
-      float mx;
-      {
-        // tree max with 3-input FMNMX3, 4 independent chains
-        float a0 = __uint_as_float(s[0]), a1 = __uint_as_float(s[1]);
-        float a2 = __uint_as_float(s[2]), a3 = __uint_as_float(s[3]);
+        if (li == 0 && lane == 0 && wq == 0) NT_STAMP(1 + t, j, 3);
+        const float m_new = fmaxf(m_run, mx * sc);
+        const bool need = m_new > m_run + kRescaleLog2;
+        if (__any_sync(0xffffffffu, need)) {
+          const float alpha = (m_new == NINF) ? 1.0f : ex2(m_run - m_new);
+          if (j > 0) {
 #pragma unroll
-        for (int c = 4; c < 128; c += 8) {
-          a0 = fmax3(a0, __uint_as_float(s[c]), __uint_as_float(s[c + 1]));
-          a1 = fmax3(a1, __uint_as_float(s[c + 2]), __uint_as_float(s[c + 3]));
-          a2 = fmax3(a2, __uint_as_float(s[c + 4]), __uint_as_float(s[c + 5]));
-          if (c + 7 < 128) a3 = fmax3(a3, __uint_as_float(s[c + 6]), __uint_as_float(s[c + 7]));
-          else a3 = fmaxf(a3, __uint_as_float(s[c + 6]));
+            for (int c = 0; c < D / 16; ++c) {
+              uint32_t o[16];
+              tmem_ld16(tO + c * 16, o);
+              tmem_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+              tmem_st16(tO + c * 16, o);
+            }
+          }
+          l_run *= alpha;
+          m_run = m_new;
         }
-        mx = fmaxf(fmax3(a0, a1, a2), a3);
-      }
-#ifdef NT_EXP_NO_SOFTMAX
-      {
-        uint32_t pk[16];
+        const float m_use = (m_run == NINF) ? 0.f : m_run;
+        const float2 sc2 = make_float2(sc, sc);
+        const float2 nm2 = make_float2(-m_use, -m_use);
+        float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
         for (int ch = 0; ch < 4; ++ch) {
+          uint32_t pk[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) pk[i] = s[ch * 32 + 2 * i];
+          for (int i = 0; i < 16; ++i) {
+            const float2 x = ffma2(make_float2(__uint_as_float(s[ch * 32 + 2 * i]),
+                                               __uint_as_float(s[ch * 32 + 2 * i + 1])), sc2, nm2);
+            float2 e;
+            if (kPolyExp && (i % kPolyEvery) == kPolyEvery - 1) {
+              e = ex2_poly2(x);  // FMA-pipe exp2 for 1/kPolyEvery of the pairs
+            } else {
+              e = make_float2(ex2(x.x), ex2(x.y));
+            }
+            sum2[i & 1] = fadd2(sum2[i & 1], e);
+            pk[i] = pack_bf16(e.x, e.y);
+          }
           tmem_st16(tS + ch * 16, pk);
         }
-        l_run = 1.f;
+        const float sum = (sum2[0].x + sum2[0].y) + (sum2[1].x + sum2[1].y);
+        if (li == 0 && lane == 0 && wq == 0) NT_STAMP(1 + t, j, 4);
+        l_run += sum;
         tmem_wait_st();
+        if (li == 0 && lane == 0 && wq == 0) NT_STAMP(1 + t, j, 5);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&bar_p_full[t]);
-        continue;
       }
-#endif
-      const float m_new = fmaxf(m_run, mx * sc);
-      const bool need = m_new > m_run + kRescaleLog2;
-      if (__any_sync(0xffffffffu, need)) {
-        const float alpha = (m_new == NINF) ? 1.0f : ex2(m_run - m_new);
-        if (j > 0) {
-#pragma unroll
-          for (int c = 0; c < D / 16; ++c) {
-            uint32_t o[16];
-            tmem_ld16(tO + c * 16, o);
-            tmem_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-            tmem_st16(tO + c * 16, o);
-          }
-        }
-        l_run *= alpha;
-        m_run = m_new;
-      }
-      const float m_use = (m_run == NINF) ? 0.f : m_run;
-      const float2 sc2 = make_float2(sc, sc);
-      const float2 nm2 = make_float2(-m_use, -m_use);
-      float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-#pragma unroll
-      for (int ch = 0; ch < 4; ++ch) {
-        uint32_t pk[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const float2 x = ffma2(make_float2(__uint_as_float(s[ch * 32 + 2 * i]),
-                                             __uint_as_float(s[ch * 32 + 2 * i + 1])), sc2, nm2);
-          float2 e;
-          if (kPolyExp && (i % kPolyEvery) == kPolyEvery - 1) {
-            e = ex2_poly2(x);  // FMA-pipe exp2 for 1/kPolyEvery of the pairs
-          } else {
-            e = make_float2(ex2(x.x), ex2(x.y));
-          }
-          sum2[i & 1] = fadd2(sum2[i & 1], e);
-          pk[i] = pack_bf16(e.x, e.y);
-        }
-        tmem_st16(tS + ch * 16, pk);
-      }
-      const float sum = (sum2[0].x + sum2[0].y) + (sum2[1].x + sum2[1].y);
-      l_run += sum;
-      tmem_wait_st();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bar_p_full[t]);
-    }
 
-    // ---- epilogue: O / l
-    mbar_wait(&bar_o_full[t], 0, p.err, 9);
-    tc_fence_after();
-    const bool valid = qi < p.N;
-    if (valid && !(l_run > 0.f) && p.err) atomicOr(p.err, 1);
-    const float inv = (l_run > 0.f) ? 1.0f / l_run : 0.f;
-    if (OUT_F32) {
-      float* orow = p.o_f32 + (long long)b * p.o_sb + (long long)hq * p.o_sh + (long long)qi * p.o_sn;
+      // ---- epilogue: O / l straight from TMEM to global (one row per thread)
+      mbar_wait(&bar_o_full[t], li & 1, p.err, 9);
+      tc_fence_after();
+      const bool valid = qi < p.N;
+      if (valid && !(l_run > 0.f) && p.err) atomicOr(p.err, 1);
+      const float inv = (l_run > 0.f) ? 1.0f / l_run : 0.f;
+      const long long row_off = (long long)itm.b * p.o_sb + (long long)itm.hq * p.o_sh + (long long)qi * p.o_sn;
 #pragma unroll
       for (int c = 0; c < D / 32; ++c) {
         uint32_t o[32];
         tmem_ld32(tO + c * 32, o);
         tmem_wait_ld();
-        if (valid) {
+        if (!valid) continue;
+        if (OUT_F32) {
+          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.o) + row_off + c * 32);
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            float4 v = make_float4(__uint_as_float(o[4 * i]) * inv, __uint_as_float(o[4 * i + 1]) * inv,
-                                   __uint_as_float(o[4 * i + 2]) * inv, __uint_as_float(o[4 * i + 3]) * inv);
-            *reinterpret_cast<float4*>(orow + c * 32 + 4 * i) = v;
-          }
+          for (int i = 0; i < 8; ++i)
+            dst[i] = make_float4(__uint_as_float(o[4 * i]) * inv, __uint_as_float(o[4 * i + 1]) * inv,
+                                 __uint_as_float(o[4 * i + 2]) * inv, __uint_as_float(o[4 * i + 3]) * inv);
+        } else {
+          uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.o) + row_off + c * 32);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            dst[q] = make_uint4(pack_bf16(__uint_as_float(o[8 * q]) * inv, __uint_as_float(o[8 * q + 1]) * inv),
+                                pack_bf16(__uint_as_float(o[8 * q + 2]) * inv, __uint_as_float(o[8 * q + 3]) * inv),
+                                pack_bf16(__uint_as_float(o[8 * q + 4]) * inv, __uint_as_float(o[8 * q + 5]) * inv),
+                                pack_bf16(__uint_as_float(o[8 * q + 6]) * inv, __uint_as_float(o[8 * q + 7]) * inv));
         }
       }
-    } else {
-      uint8_t* stage = sQ + t * C::TQ;  // Q_t is dead once O_t is final
-#pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t o[32];
-        tmem_ld32(tO + c * 32, o);
-        tmem_wait_ld();
-        uint32_t pk[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i)
-          pk[i] = pack_bf16(__uint_as_float(o[2 * i]) * inv, __uint_as_float(o[2 * i + 1]) * inv);
-        uint8_t* rowp = stage + (c >> 1) * C::HALF + r * 128;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int chunk = ((c & 1) * 4 + q) ^ (r & 7);
-          *reinterpret_cast<uint4*>(rowp + chunk * 16) = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-        }
-      }
-      fence_proxy_async_smem();
-      named_bar_sync(1 + t, 128);
-      if (r == 0) {
-#pragma unroll
-        for (int h = 0; h < D / 64; ++h)
-          tma_store_4d(&tmO, stage + h * C::HALF, h * 64, q_row0 + t * 128, hq, b);
-        bulk_commit();
-        bulk_wait_read0();
-      }
+      // O_t is read out: the next item's first PV_t (issued after this warp's
+      // next p_full arrival) may overwrite it
+      tc_fence_before();
     }
   }
 
@@ -404,6 +463,15 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
+  }
+  if (threadIdx.x == 0 && p.work) {
+    // every CTA has drawn its terminal item before arriving here: the last one
+    // resets the counter for the next launch on this stream
+    __threadfence();
+    if (atomicAdd(p.work + 1, 1) == (int)gridDim.x - 1) {
+      atomicExch(p.work, 0);
+      atomicExch(p.work + 1, 0);
+    }
   }
 }
 

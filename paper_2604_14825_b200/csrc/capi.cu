@@ -28,6 +28,12 @@ int check_cuda(cudaError_t e, const char* what) {
   return NT_OK;
 }
 
+int num_sms() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 148;
+}
+
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -86,8 +92,8 @@ int make_map_2d(CUtensorMap* m, const void* ptr, int64_t inner, int64_t outer, i
 
 // ----------------------------------------------------------------- attention
 template <int D, int MASK, bool F32>
-static int launch_attn(const nt_attn_args* a, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
-                       const CUtensorMap& mo, const AttnFwdParams& p, cudaStream_t st) {
+static int launch_attn(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const AttnFwdParams& p,
+                       cudaStream_t st) {
   auto kern = attn_fwd_kernel<D, MASK, F32>;
   const int smem = AttnCfg<D>::SMEM_BYTES;
   static bool configured = false;
@@ -97,26 +103,27 @@ static int launch_attn(const nt_attn_args* a, const CUtensorMap& mq, const CUten
     if (rc) return rc;
     configured = true;
   }
-  dim3 grid(p.n_mblocks * a->batch * a->heads_q);
-  kern<<<grid, kAttnThreads, smem, st>>>(mq, mk, mv, mo, p);
+  // persistent: at most one CTA per SM, each walking items blockIdx.x + k * gridDim.x
+  const int grid = std::min(p.n_items, num_sms());
+  kern<<<grid, kAttnThreads, smem, st>>>(mq, mk, mv, p);
   g_launches++;
   return check_cuda(cudaGetLastError(), "attn_fwd launch");
 }
 
 template <int D>
 static int dispatch_attn(const nt_attn_args* a, const CUtensorMap& mq, const CUtensorMap& mk,
-                         const CUtensorMap& mv, const CUtensorMap& mo, const AttnFwdParams& p, cudaStream_t st) {
+                         const CUtensorMap& mv, const AttnFwdParams& p, cudaStream_t st) {
   const bool f32 = a->out_dtype == NT_DTYPE_F32;
   switch (a->mask_kind) {
     case NT_MASK_NONE:
-      return f32 ? launch_attn<D, MASK_NONE, true>(a, mq, mk, mv, mo, p, st)
-                 : launch_attn<D, MASK_NONE, false>(a, mq, mk, mv, mo, p, st);
+      return f32 ? launch_attn<D, MASK_NONE, true>(mq, mk, mv, p, st)
+                 : launch_attn<D, MASK_NONE, false>(mq, mk, mv, p, st);
     case NT_MASK_CAUSAL:
-      return f32 ? launch_attn<D, MASK_CAUSAL, true>(a, mq, mk, mv, mo, p, st)
-                 : launch_attn<D, MASK_CAUSAL, false>(a, mq, mk, mv, mo, p, st);
+      return f32 ? launch_attn<D, MASK_CAUSAL, true>(mq, mk, mv, p, st)
+                 : launch_attn<D, MASK_CAUSAL, false>(mq, mk, mv, p, st);
     case NT_MASK_TENSOR:
-      return f32 ? launch_attn<D, MASK_TENSOR, true>(a, mq, mk, mv, mo, p, st)
-                 : launch_attn<D, MASK_TENSOR, false>(a, mq, mk, mv, mo, p, st);
+      return f32 ? launch_attn<D, MASK_TENSOR, true>(mq, mk, mv, p, st)
+                 : launch_attn<D, MASK_TENSOR, false>(mq, mk, mv, p, st);
   }
   return set_error(NT_ERR_INVALID, "unknown mask_kind");
 }
@@ -135,7 +142,7 @@ extern "C" int nt_attn_fwd(const nt_attn_args* a, void* stream) {
   if (!(a->scale > 0.f)) return set_error(NT_ERR_UNSUPPORTED, "scale must be positive");
   if (a->mask_kind == NT_MASK_TENSOR && !a->mask) return set_error(NT_ERR_INVALID, "tensor mask missing");
   const int D = a->head_dim;
-  CUtensorMap mq, mk, mv, mo;
+  CUtensorMap mq, mk, mv;
   int rc;
   if ((rc = make_map_4d(&mq, a->q.ptr, D, a->seq_q, a->heads_q, a->batch, a->q.stride_s, a->q.stride_h,
                         a->q.stride_b, 128, 2)))
@@ -146,15 +153,12 @@ extern "C" int nt_attn_fwd(const nt_attn_args* a, void* stream) {
   if ((rc = make_map_4d(&mv, a->v.ptr, D, a->seq_kv, a->heads_kv, a->batch, a->v.stride_s, a->v.stride_h,
                         a->v.stride_b, 128, 2)))
     return rc;
-  if (a->out_dtype == NT_DTYPE_BF16) {
-    if ((rc = make_map_4d(&mo, a->o.ptr, D, a->seq_q, a->heads_q, a->batch, a->o.stride_s, a->o.stride_h,
-                          a->o.stride_b, 128, 2)))
-      return rc;
-  } else {
-    memset(&mo, 0, sizeof(mo));
-    if (reinterpret_cast<uintptr_t>(a->o.ptr) % 16 || a->o.stride_s % 4)
-      return set_error(NT_ERR_INVALID, "fp32 output must be 16B aligned with row stride % 4 == 0");
-  }
+  // the epilogue stores O rows straight from registers (16-byte vectors)
+  if (reinterpret_cast<uintptr_t>(a->o.ptr) % 16 ||
+      (a->o.stride_s * (a->out_dtype == NT_DTYPE_F32 ? 4 : 2)) % 16 ||
+      (a->o.stride_h * (a->out_dtype == NT_DTYPE_F32 ? 4 : 2)) % 16 ||
+      (a->o.stride_b * (a->out_dtype == NT_DTYPE_F32 ? 4 : 2)) % 16)
+    return set_error(NT_ERR_INVALID, "output must be 16B aligned with 16B-multiple strides");
   AttnFwdParams p{};
   p.B = a->batch;
   p.Hq = a->heads_q;
@@ -164,17 +168,19 @@ extern "C" int nt_attn_fwd(const nt_attn_args* a, void* stream) {
   p.q_per_kv = a->heads_q / a->heads_kv;
   p.n_mblocks = (a->seq_q + 255) / 256;
   p.n_kv_total = (a->seq_kv + 127) / 128;
+  p.n_items = p.n_mblocks * a->batch * a->heads_q;
   p.causal_offset = a->causal_offset;
   p.scale_log2 = a->scale * 1.4426950408889634f;
   p.mask = a->mask;
   p.mask_row_stride = a->mask_stride_row;
-  p.o_f32 = static_cast<float*>(a->o.ptr);
+  p.o = a->o.ptr;
   p.o_sb = a->o.stride_b;
   p.o_sh = a->o.stride_h;
   p.o_sn = a->o.stride_s;
   p.err = a->err_flag;
+  p.work = a->work_counter;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  return D == 64 ? dispatch_attn<64>(a, mq, mk, mv, mo, p, st) : dispatch_attn<128>(a, mq, mk, mv, mo, p, st);
+  return D == 64 ? dispatch_attn<64>(a, mq, mk, mv, p, st) : dispatch_attn<128>(a, mq, mk, mv, p, st);
 }
 
 // ----------------------------------------------------------------- casts
@@ -220,6 +226,15 @@ extern "C" int nt_cast_bf16_to_f32(const void* src, float* dst, int64_t n, void*
   g_launches++;
   return check_cuda(cudaGetLastError(), "cast_bf16_f32");
 }
+
+#ifdef NT_TRACE
+// debug builds only: route the K1 pipeline timeline stamps of one CTA into `buf`
+extern "C" int nt_debug_set_trace(unsigned long long* buf, int cta) {
+  cudaMemcpyToSymbol(nt::g_nt_trace, &buf, sizeof(buf));
+  cudaMemcpyToSymbol(nt::g_nt_trace_cta, &cta, sizeof(cta));
+  return check_cuda(cudaGetLastError(), "nt_debug_set_trace");
+}
+#endif
 
 extern "C" int nt_abi_version(void) { return NT_ABI_VERSION; }
 extern "C" const char* nt_last_error(void) { return g_last_error.c_str(); }

@@ -75,6 +75,9 @@ class AttentionPlan:
             a.mask_stride_row = mask.stride(0)
         a.out_dtype = _lib.NT_DTYPE_F32 if o.dtype == torch.float32 else _lib.NT_DTYPE_BF16
         a.err_flag = self.err.data_ptr()
+        # dynamic (greedy LPT) item counter of the persistent kernel; reset on device by the last CTA
+        self.work = torch.zeros(2, dtype=torch.int32, device=q.device)
+        a.work_counter = self.work.data_ptr()
         self.args = a
         self.shape = (B, Hq, Hkv, N, M, D)
         self._fn = _lib.lib().nt_attn_fwd

@@ -1,0 +1,54 @@
+"""Dump the NT_TRACE pipeline timeline of one attention CTA (debug tool).
+
+    NT_LIB_PATH=.../libnt_trace.so python tools/trace_attn.py [--cta 0] [--n 8192]
+"""
+import argparse
+import ctypes
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2604_14825_b200 import _lib  # noqa: E402
+from paper_2604_14825_b200.runtime import AttentionPlan  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--cta", type=int, default=0)
+ap.add_argument("--n", type=int, default=8192)
+ap.add_argument("--causal", type=int, default=1)
+ap.add_argument("--out", default="gpurun_out/trace.json")
+a = ap.parse_args()
+L = _lib.lib()
+L.nt_debug_set_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
+buf = torch.zeros(4 * 64 * 8, dtype=torch.int64, device="cuda")
+N, D = a.n, 128
+q = torch.randn(1, 32, N, D, device="cuda").bfloat16()
+k = torch.randn(1, 8, N, D, device="cuda").bfloat16()
+v = torch.randn(1, 8, N, D, device="cuda").bfloat16()
+o = torch.empty(1, 32, N, D, device="cuda").bfloat16()
+plan = AttentionPlan(q, k, v, o, 0.0883883, "causal" if a.causal else "none")
+for _ in range(3):
+    plan.launch()
+torch.cuda.synchronize()
+L.nt_debug_set_trace(buf.data_ptr(), a.cta)
+plan.launch()
+torch.cuda.synchronize()
+L.nt_debug_set_trace(None, a.cta)
+t = buf.view(4, 64, 8).cpu().numpy()
+base = t[t > 0].min()
+res = {}
+for role, name in enumerate(["mma", "softmax0", "softmax1", "producer"]):
+    rows = []
+    for it in range(64):
+        r = t[role, it]
+        if (r > 0).any():
+            rows.append([int(x - base) if x > 0 else None for x in r])
+    res[name] = rows
+os.makedirs(os.path.dirname(a.out), exist_ok=True)
+json.dump(res, open(a.out, "w"))
+for name in ("mma", "softmax0", "softmax1"):
+    print(name)
+    for i, r in enumerate(res[name][:12]):
+        print(i, r)
