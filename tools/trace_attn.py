@@ -19,16 +19,21 @@ ap.add_argument("--cta", type=int, default=0)
 ap.add_argument("--n", type=int, default=8192)
 ap.add_argument("--causal", type=int, default=1)
 ap.add_argument("--out", default="gpurun_out/trace.json")
+ap.add_argument("--d", type=int, default=128)
+ap.add_argument("--b", type=int, default=1)
+ap.add_argument("--hq", type=int, default=32)
+ap.add_argument("--hkv", type=int, default=8)
+ap.add_argument("--scale", type=float, default=0.0883883)
 a = ap.parse_args()
 L = _lib.lib()
 L.nt_debug_set_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
 buf = torch.zeros(4 * 64 * 8, dtype=torch.int64, device="cuda")
-N, D = a.n, 128
-q = torch.randn(1, 32, N, D, device="cuda").bfloat16()
-k = torch.randn(1, 8, N, D, device="cuda").bfloat16()
-v = torch.randn(1, 8, N, D, device="cuda").bfloat16()
-o = torch.empty(1, 32, N, D, device="cuda").bfloat16()
-plan = AttentionPlan(q, k, v, o, 0.0883883, "causal" if a.causal else "none")
+N, D = a.n, a.d
+q = torch.randn(a.b, a.hq, N, D, device="cuda").bfloat16()
+k = torch.randn(a.b, a.hkv, N, D, device="cuda").bfloat16()
+v = torch.randn(a.b, a.hkv, N, D, device="cuda").bfloat16()
+o = torch.empty(a.b, a.hq, N, D, device="cuda").bfloat16()
+plan = AttentionPlan(q, k, v, o, a.scale, "causal" if a.causal else "none")
 for _ in range(3):
     plan.launch()
 torch.cuda.synchronize()
