@@ -80,10 +80,15 @@ struct AttnCfg {
   static constexpr int TQ = BM * D * 2;
   static constexpr int TKV = BN * D * 2;
   static constexpr int STAGES = (D == 128) ? 4 : 8;
+  // D = 64: O_t needs only 64 TMEM columns, so P_t gets its own 64 columns
+  // next to it instead of aliasing S_t.  S_t(j+1) can then be computed as soon
+  // as the softmax warps have loaded S_t(j) into registers, i.e. while they
+  // compute P_t(j), and the tile's GEMMs leave the softmax critical path.
+  static constexpr bool SEP_P = (D == 64);
   static constexpr int SMEM_Q = 0;
   static constexpr int SMEM_KV = 2 * TQ;
   static constexpr int SMEM_BAR = SMEM_KV + STAGES * TKV;
-  static constexpr int NBAR = 2 + 2 + 2 * STAGES + 2 + 2 + 2 + 2 * kItemRing;
+  static constexpr int NBAR = 2 + 2 + 2 * STAGES + 2 + 2 + 2 + 2 + 2 + 2 * kItemRing;
   static constexpr int SMEM_BYTES = SMEM_BAR + NBAR * 8 + 16 + 4 * kItemRing + 1024;  // + alignment slack
 };
 
@@ -150,7 +155,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   uint64_t* bar_s_full = bars + 4 + 2 * C::STAGES;   // [2]
   uint64_t* bar_p_full = bar_s_full + 2;             // [2]
   uint64_t* bar_o_full = bar_p_full + 2;             // [2]
-  uint64_t* bar_item_full = bar_o_full + 2;          // [kItemRing] item index published
+  uint64_t* bar_s_free = bar_o_full + 2;             // [2] SEP_P: S_t loaded into registers (4 warps)
+  uint64_t* bar_pv_done = bar_s_free + 2;            // [2] SEP_P: PV_t completed (P_t / O_t reusable)
+  uint64_t* bar_item_full = bar_pv_done + 2;         // [kItemRing] item index published
   uint64_t* bar_item_empty = bar_item_full + kItemRing;  // [kItemRing] read by MMA + 8 softmax warps
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBAR);
   int* item_ring = reinterpret_cast<int*>(tmem_slot + 4);
@@ -168,6 +175,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       mbar_init(&bar_s_full[t], 1);
       mbar_init(&bar_p_full[t], 4);
       mbar_init(&bar_o_full[t], 1);
+      mbar_init(&bar_s_free[t], 4);
+      mbar_init(&bar_pv_done[t], 1);
     }
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&bar_kv_full[s], 1);
@@ -249,11 +258,13 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
             const uint64_t bd = sdesc_sw128(sKVa + slot * C::TKV + k * 2048, C::HALF, 1024);
-            umma_ts(tmem + 256 + t * 128, tmem + t * 128 + k * 8, bd, idO, (acc || k > 0) ? 1u : 0u);
+            const uint32_t pcol = C::SEP_P ? (256 + t * 128 + 64) : (t * 128);
+            umma_ts(tmem + 256 + t * 128, tmem + pcol + k * 8, bd, idO, (acc || k > 0) ? 1u : 0u);
           }
         };
         int kv_base = 0;
         uint32_t p_phase[2] = {0u, 0u};
+        uint32_t sf_phase[2] = {0u, 0u};
         for (int li = 0;; ++li) {
           const int slot_i = li % kItemRing;
           mbar_wait(&bar_item_full[slot_i], (li / kItemRing) & 1, p.err, 13);
@@ -264,6 +275,56 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           mbar_wait(&bar_q[0], li & 1, p.err, 2);
           mbar_wait(&bar_q[1], li & 1, p.err, 2);
           tc_fence_after();
+          if constexpr (C::SEP_P) {
+            // stream per tile: S(0), S(1), PV(0), S(2), PV(1), ... -- S(j) waits only
+            // until the softmax warps have read S(j-1) out of TMEM
+            for (int j = 0; j < n_kv; ++j) {
+              const int gK = kv_base + 2 * j;
+              const int slotK = gK % C::STAGES;
+              mbar_wait(&bar_kv_full[slotK], (gK / C::STAGES) & 1, p.err, 3);
+              tc_fence_after();
+              for (int t = 0; t < 2; ++t) {
+                if (j > 0) {
+                  mbar_wait(&bar_s_free[t], sf_phase[t], p.err, 15);
+                  sf_phase[t] ^= 1u;
+                  tc_fence_after();
+                }
+                issue_s(t, slotK);
+                umma_commit(&bar_s_full[t]);
+                if (j == n_kv - 1) umma_commit(&bar_q_empty[t]);
+              }
+              umma_commit(&bar_kv_empty[slotK]);
+              if (j > 0) {
+                const int gV = gK - 1;
+                const int slotV = gV % C::STAGES;
+                for (int t = 0; t < 2; ++t) {
+                  mbar_wait(&bar_p_full[t], p_phase[t], p.err, 4);
+                  p_phase[t] ^= 1u;
+                  if (t == 0) mbar_wait(&bar_kv_full[slotV], (gV / C::STAGES) & 1, p.err, 5);
+                  tc_fence_after();
+                  issue_pv(t, slotV, j - 1 > 0);
+                  umma_commit(&bar_pv_done[t]);
+                }
+                umma_commit(&bar_kv_empty[slotV]);
+              }
+            }
+            const int gV = kv_base + 2 * (n_kv - 1) + 1;
+            const int slotV = gV % C::STAGES;
+            for (int t = 0; t < 2; ++t) {
+              mbar_wait(&bar_s_free[t], sf_phase[t], p.err, 16);
+              sf_phase[t] ^= 1u;
+              mbar_wait(&bar_p_full[t], p_phase[t], p.err, 6);
+              p_phase[t] ^= 1u;
+              if (t == 0) mbar_wait(&bar_kv_full[slotV], (gV / C::STAGES) & 1, p.err, 7);
+              tc_fence_after();
+              issue_pv(t, slotV, n_kv - 1 > 0);
+              umma_commit(&bar_pv_done[t]);
+              umma_commit(&bar_o_full[t]);
+            }
+            umma_commit(&bar_kv_empty[slotV]);
+            kv_base += 2 * n_kv;
+            continue;
+          }
           for (int j = 0; j < n_kv; ++j) {
             const int gK = kv_base + 2 * j;
             const int slotK = gK % C::STAGES;
@@ -314,9 +375,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
     const uint32_t tS = tmem + t * 128 + lane_off;
     const uint32_t tO = tmem + 256 + t * 128 + lane_off;
+    const uint32_t tP = C::SEP_P ? (tO + 64) : tS;  // where P_t (bf16 pairs) is stored
     const float NINF = f_ninf();
     const float sc = (MASK == MASK_TENSOR) ? 1.0f : p.scale_log2;
     uint32_t s_phase = 0u;
+    int pv_base = 0;  // SEP_P: PV_t completions of earlier items
     for (int li = 0;; ++li) {
       const int slot_i = li % kItemRing;
       mbar_wait(&bar_item_full[slot_i], (li / kItemRing) & 1, p.err, 14);
@@ -338,6 +401,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 #pragma unroll
         for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, s + c * 32);
         tmem_wait_ld();
+        if constexpr (C::SEP_P) {  // S_t is in registers: let S_t(j+1) overwrite it
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bar_s_free[t]);
+        }
         if (li == 0 && lane == 0 && wq == 0) NT_STAMP(1 + t, j, 2);
         const int kv0 = j * 128;
         if (MASK == MASK_TENSOR) {
@@ -372,6 +440,12 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           mx = fmaxf(fmax3(a0, a1, a2), a3);
         }
         if (li == 0 && lane == 0 && wq == 0) NT_STAMP(1 + t, j, 3);
+        if (C::SEP_P && j > 0) {
+          // PV_t(j-1) must be complete before O_t is rescaled or P_t overwritten;
+          // completions up to j-2 were waited for at j-1, so the parity is exact
+          mbar_wait(&bar_pv_done[t], (pv_base + j - 1) & 1, p.err, 10);
+          tc_fence_after();
+        }
         const float m_new = fmaxf(m_run, mx * sc);
         const bool need = m_new > m_run + kRescaleLog2;
         if (__any_sync(0xffffffffu, need)) {
@@ -410,7 +484,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             sum2[i & 1] = fadd2(sum2[i & 1], e);
             pk[i] = pack_bf16(e.x, e.y);
           }
-          tmem_st16(tS + ch * 16, pk);
+          tmem_st16(tP + ch * 16, pk);
         }
         const float sum = (sum2[0].x + sum2[0].y) + (sum2[1].x + sum2[1].y);
         if (li == 0 && lane == 0 && wq == 0) NT_STAMP(1 + t, j, 4);
@@ -421,6 +495,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&bar_p_full[t]);
       }
+
+      pv_base += itm.n_kv;
 
       // ---- epilogue: O / l straight from TMEM to global (one row per thread)
       mbar_wait(&bar_o_full[t], li & 1, p.err, 9);
