@@ -54,6 +54,14 @@ CONFIGS = {
     # config 5: decode, the 4 q-heads of a GQA group packed as the MA's 4 rows
     "decode32k": dict(kind="decode", prog="llama", B=64, Hq=32, Hkv=8, N=1, M=32768, D=128, causal=False,
                       golden="decode4_32k", scale=LLAMA_SCALE),
+    # the same decode over a paged KV cache (16-token pages, shuffled block table)
+    "decode32k_paged16": dict(kind="decode", prog="llama", B=64, Hq=32, Hkv=8, N=1, M=32768, D=128, causal=False,
+                              golden="decode4_32k", scale=LLAMA_SCALE, page_size=16),
+    "decode32k_paged16_hnd": dict(kind="decode", prog="llama", B=64, Hq=32, Hkv=8, N=1, M=32768, D=128,
+                                  causal=False, golden="decode4_32k", scale=LLAMA_SCALE, page_size=16,
+                                  page_layout="HND"),
+    "decode32k_paged64": dict(kind="decode", prog="llama", B=64, Hq=32, Hkv=8, N=1, M=32768, D=128, causal=False,
+                              golden="decode4_32k", scale=LLAMA_SCALE, page_size=64),
     # config 2: (X.W1).W2 at 4096^3 x E=4096 (schedulable with max_tile_elems >= 262144)
     "gemm_chain_e4096": dict(kind="gemm_chain", prog="gemm2", N=4096, K=4096, F=4096, E=4096,
                              golden="gemm4k_e4096", causal=False, B=1, Hq=1, Hkv=1, D=0),
@@ -362,6 +370,28 @@ def build_workload(cfg, spec, rank, world, dev):
         v = torch.randn((Bl, Hkvl, M, D), generator=gen, device=dev).to(torch.bfloat16)
         o = torch.empty((Bl, Hkvl, g * N, D), dtype=torch.bfloat16, device=dev)
         plan = DecodePlan(q, k, v, o, spec.scale)
+        if cfg.get("page_size"):
+            # NHD page pools [pages, page_size, Hkv, D] in a shuffled physical order
+            from paper_2604_14825_b200.runtime import PagedDecodePlan
+            ps = cfg["page_size"]
+            npp = M // ps
+            perm = torch.randperm(Bl * npp, generator=gen, device=dev).to(torch.int32)
+            layout = cfg.get("page_layout", "NHD")
+            pools = []
+            for t in (k, v):
+                if layout == "NHD":
+                    pool = torch.empty((Bl * npp, ps, Hkvl, D), dtype=torch.bfloat16, device=dev)
+                    pool[perm.long()] = t.permute(0, 2, 1, 3).reshape(Bl * npp, ps, Hkvl, D)
+                else:
+                    pool = torch.empty((Bl * npp, Hkvl, ps, D), dtype=torch.bfloat16, device=dev)
+                    pool[perm.long()] = t.reshape(Bl, Hkvl, npp, ps, D).permute(0, 2, 1, 3, 4).reshape(
+                        Bl * npp, Hkvl, ps, D)
+                pools.append(pool)
+            block_table = perm.reshape(Bl, npp).contiguous()
+            seq_lens = torch.full((Bl,), M, dtype=torch.int32, device=dev)
+            plan = PagedDecodePlan(q, pools[0], pools[1], block_table, seq_lens, o, spec.scale, layout=layout,
+                                   max_seq_kv=M)
+            w["pools"] = pools
         kv_bytes = 2 * Bl * Hkvl * M * D * 2
         w.update(plan=plan, out=o, local_flops=4.0 * Bl * Hkvl * g * N * M * D,
                  total_flops=4.0 * cfg["B"] * cfg["Hq"] * N * M * D, bound="hbm",
@@ -485,7 +515,8 @@ def run_ours(args, cfg, rank, world, dist):
         peak = peaks["hbm_gbs"]
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})",
-                "algorithmic_bytes_per_launch": w["local_bytes"], "kernel": "decode_split_kernel + combine"}
+                "algorithmic_bytes_per_launch": w["local_bytes"],
+                "kernel": "decode_split_kernel<paged> + combine" if cfg.get("page_size") else "decode_split_kernel + combine"}
     else:
         achieved = w["local_flops"] / (ms_kernel_local * 1e-3) / 1e12
         peak = peaks["bf16_tflops"]

@@ -100,6 +100,36 @@ int nt_decode_num_splits(int32_t batch, int32_t heads_kv, int32_t seq_kv, int32_
 int nt_attn_decode(const nt_decode_args* args, void* stream);
 
 /*
+ * K2 over a PAGED KV cache: the same split-KV decode,
+ * with K/V gathered by TMA page by page from page pools through a block table
+ * -- the serving layout of the decode MA's K/V buffers (vLLM/FlashInfer-style
+ * "NHD" pools [num_pages, page_size, heads_kv, 128] or "HND" pools
+ * [num_pages, heads_kv, page_size, 128]; any element strides with head_dim
+ * contiguous).  Sequence b attends to its first seq_lens[b] keys;
+ * block_table[b * block_table_stride + i] is the physical page of its
+ * logical page i.  page_size: 8, 16, 32, 64 or a multiple of 64.
+ * Workspace: nt_decode_workspace_bytes(batch, heads_kv, rows, 128, num_splits),
+ * splits from nt_decode_num_splits(batch, heads_kv, max_seq_kv, requested).
+ */
+typedef struct nt_decode_paged_args {
+  nt_tensor4 q, o;                /* [batch, heads_q, seq_q, 128] */
+  const void* k_pages;            /* bf16 page pools */
+  const void* v_pages;
+  int64_t page_stride, token_stride, head_stride; /* element strides, same for K and V */
+  int32_t num_pages, page_size;
+  const int32_t* block_table;     /* device int32 [batch, block_table_stride] */
+  int32_t block_table_stride;
+  const int32_t* seq_lens;        /* device int32 [batch] */
+  int32_t batch, heads_q, heads_kv, seq_q, max_seq_kv, head_dim;
+  float scale;
+  int32_t num_splits;
+  int32_t out_dtype;
+  void* workspace;
+  int32_t* err_flag;
+} nt_decode_paged_args;
+int nt_attn_decode_paged(const nt_decode_paged_args* args, void* stream);
+
+/*
  * K3 GEMM (tcgen05, fp32 accumulate): C[M,N] = A[M,K] . B[K,N] with bf16 A, B
  * (row-major, unit inner stride) and bf16 or fp32 C
  * (the MA's zero-initialised `acc=Y[...]` accumulation is the GEMM's own K loop).

@@ -23,7 +23,7 @@ EXPORTED = (
     "nt_attn_fwd", "nt_attn_decode", "nt_decode_workspace_bytes", "nt_decode_num_splits", "nt_gemm",
     "nt_gemm_chain", "nt_gemm_chain_workspace_bytes",
     "nt_cast_f32_to_bf16", "nt_cast_bf16_to_f32", "nt_abi_version", "nt_last_error", "nt_launch_count",
-    "nt_module_load", "nt_module_function", "nt_launch", "nt_module_unload",
+    "nt_module_load", "nt_module_function", "nt_launch", "nt_module_unload", "nt_attn_decode_paged",
 )
 
 
@@ -45,6 +45,17 @@ class DecodeArgs(C.Structure):
     _fields_ = [("q", Tensor4), ("k", Tensor4), ("v", Tensor4), ("o", Tensor4),
                 ("batch", C.c_int32), ("heads_q", C.c_int32), ("heads_kv", C.c_int32),
                 ("seq_q", C.c_int32), ("seq_kv", C.c_int32), ("head_dim", C.c_int32),
+                ("scale", C.c_float), ("num_splits", C.c_int32), ("out_dtype", C.c_int32),
+                ("workspace", C.c_void_p), ("err_flag", C.c_void_p)]
+
+
+class DecodePagedArgs(C.Structure):
+    _fields_ = [("q", Tensor4), ("o", Tensor4), ("k_pages", C.c_void_p), ("v_pages", C.c_void_p),
+                ("page_stride", C.c_int64), ("token_stride", C.c_int64), ("head_stride", C.c_int64),
+                ("num_pages", C.c_int32), ("page_size", C.c_int32), ("block_table", C.c_void_p),
+                ("block_table_stride", C.c_int32), ("seq_lens", C.c_void_p),
+                ("batch", C.c_int32), ("heads_q", C.c_int32), ("heads_kv", C.c_int32),
+                ("seq_q", C.c_int32), ("max_seq_kv", C.c_int32), ("head_dim", C.c_int32),
                 ("scale", C.c_float), ("num_splits", C.c_int32), ("out_dtype", C.c_int32),
                 ("workspace", C.c_void_p), ("err_flag", C.c_void_p)]
 
@@ -80,6 +91,7 @@ def lib():
             L = C.CDLL(LIB_PATH)
             L.nt_attn_fwd.argtypes = [C.POINTER(AttnArgs), C.c_void_p]
             L.nt_attn_decode.argtypes = [C.POINTER(DecodeArgs), C.c_void_p]
+            L.nt_attn_decode_paged.argtypes = [C.POINTER(DecodePagedArgs), C.c_void_p]
             L.nt_decode_workspace_bytes.argtypes = [C.c_int32] * 5
             L.nt_decode_workspace_bytes.restype = C.c_int64
             L.nt_decode_num_splits.argtypes = [C.c_int32] * 4
@@ -97,7 +109,7 @@ def lib():
             L.nt_module_unload.argtypes = [C.c_void_p]
             L.nt_last_error.restype = C.c_char_p
             L.nt_launch_count.restype = C.c_int64
-            for name in ("nt_attn_fwd", "nt_attn_decode", "nt_gemm", "nt_gemm_chain",
+            for name in ("nt_attn_fwd", "nt_attn_decode", "nt_attn_decode_paged", "nt_gemm", "nt_gemm_chain",
                          "nt_cast_f32_to_bf16", "nt_cast_bf16_to_f32", "nt_abi_version",
                          "nt_module_load", "nt_module_function", "nt_launch", "nt_module_unload"):
                 getattr(L, name).restype = C.c_int

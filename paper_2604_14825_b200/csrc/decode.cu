@@ -28,17 +28,10 @@ int choose_splits(int groups, int M, int requested) {
   return std::max(1, std::min(by_occupancy, by_length));
 }
 
-template <int R>
-int launch(const nt_decode_args* a, DecodeParams& p, cudaStream_t st) {
-  CUtensorMap mk, mv;
+template <int R, bool PAGED>
+int launch(const CUtensorMap& mk, const CUtensorMap& mv, DecodeParams& p, cudaStream_t st) {
   int rc;
-  if ((rc = make_map_4d(&mk, a->k.ptr, kDecodeD, a->seq_kv, a->heads_kv, a->batch, a->k.stride_s, a->k.stride_h,
-                        a->k.stride_b, kDecodeTile, 2)))
-    return rc;
-  if ((rc = make_map_4d(&mv, a->v.ptr, kDecodeD, a->seq_kv, a->heads_kv, a->batch, a->v.stride_s, a->v.stride_h,
-                        a->v.stride_b, kDecodeTile, 2)))
-    return rc;
-  auto kern = decode_split_kernel<R>;
+  auto kern = decode_split_kernel<R, PAGED>;
   static bool configured = false;
   if (!configured) {
     if ((rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kDecodeSmem),
@@ -54,6 +47,15 @@ int launch(const nt_decode_args* a, DecodeParams& p, cudaStream_t st) {
   decode_combine_kernel<<<(rows + 3) / 4, 128, 0, st>>>(p, R);
   g_launches++;
   return check_cuda(cudaGetLastError(), "decode_combine launch");
+}
+template <bool PAGED>
+int dispatch(int R, const CUtensorMap& mk, const CUtensorMap& mv, DecodeParams& p, cudaStream_t st) {
+  switch (R) {
+    case 1: return launch<1, PAGED>(mk, mv, p, st);
+    case 2: return launch<2, PAGED>(mk, mv, p, st);
+    case 4: return launch<4, PAGED>(mk, mv, p, st);
+    default: return launch<8, PAGED>(mk, mv, p, st);
+  }
 }
 }  // namespace
 
@@ -91,13 +93,62 @@ extern "C" int nt_attn_decode(const nt_decode_args* a, void* stream) {
   p.keys_per_split = ((a->seq_kv + p.splits - 1) / p.splits + kDecodeTile - 1) / kDecodeTile * kDecodeTile;
   p.ws = static_cast<float*>(a->workspace);
   p.err = a->err_flag;
+  p.seq_lens = nullptr;
+  p.block_table = nullptr;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  switch (R) {
-    case 1: return launch<1>(a, p, st);
-    case 2: return launch<2>(a, p, st);
-    case 4: return launch<4>(a, p, st);
-    default: return launch<8>(a, p, st);
-  }
+  CUtensorMap mk, mv;
+  int rc;
+  if ((rc = make_map_4d(&mk, a->k.ptr, kDecodeD, a->seq_kv, a->heads_kv, a->batch, a->k.stride_s, a->k.stride_h,
+                        a->k.stride_b, kDecodeTile, 2)))
+    return rc;
+  if ((rc = make_map_4d(&mv, a->v.ptr, kDecodeD, a->seq_kv, a->heads_kv, a->batch, a->v.stride_s, a->v.stride_h,
+                        a->v.stride_b, kDecodeTile, 2)))
+    return rc;
+  return dispatch<false>(R, mk, mv, p, st);
+}
+
+extern "C" int nt_attn_decode_paged(const nt_decode_paged_args* a, void* stream) {
+  if (!a) return set_error(NT_ERR_INVALID, "null args");
+  if (a->head_dim != kDecodeD) return set_error(NT_ERR_UNSUPPORTED, "decode kernel is built for head_dim 128");
+  if (a->heads_q % a->heads_kv) return set_error(NT_ERR_INVALID, "heads_q must be a multiple of heads_kv");
+  const int g = a->heads_q / a->heads_kv;
+  const int R = g * a->seq_q;
+  if (R != 1 && R != 2 && R != 4 && R != 8)
+    return set_error(NT_ERR_UNSUPPORTED, "decode kernel packs 1, 2, 4 or 8 query rows per kv group");
+  const int ps = a->page_size;
+  if (ps <= 0 || ps % 8 || (ps < kDecodeTile && kDecodeTile % ps) || (ps > kDecodeTile && ps % kDecodeTile))
+    return set_error(NT_ERR_UNSUPPORTED, "page_size must be 8, 16, 32, 64 or a multiple of 64");
+  if (!a->workspace || !a->block_table || !a->seq_lens) return set_error(NT_ERR_INVALID, "workspace, block_table and seq_lens required");
+  if (a->max_seq_kv <= 0 || a->num_pages <= 0) return set_error(NT_ERR_INVALID, "empty cache");
+  for (const nt_tensor4* t : {&a->q})
+    if (reinterpret_cast<uintptr_t>(t->ptr) % 16 || t->stride_s % 8 || t->stride_h % 8 || t->stride_b % 8)
+      return set_error(NT_ERR_INVALID, "q must be 16-byte aligned with strides % 8 == 0");
+  DecodeParams p{};
+  p.q = static_cast<const __nv_bfloat16*>(a->q.ptr);
+  p.q_sb = a->q.stride_b; p.q_sh = a->q.stride_h; p.q_sn = a->q.stride_s;
+  p.o = a->o.ptr;
+  p.o_sb = a->o.stride_b; p.o_sh = a->o.stride_h; p.o_sn = a->o.stride_s;
+  p.out_f32 = a->out_dtype == NT_DTYPE_F32;
+  p.B = a->batch; p.Hq = a->heads_q; p.Hkv = a->heads_kv; p.Nq = a->seq_q; p.M = a->max_seq_kv; p.g = g;
+  p.scale_log2 = a->scale * 1.4426950408889634f;
+  p.splits = std::max(1, a->num_splits);
+  p.keys_per_split = ((a->max_seq_kv + p.splits - 1) / p.splits + kDecodeTile - 1) / kDecodeTile * kDecodeTile;
+  p.ws = static_cast<float*>(a->workspace);
+  p.err = a->err_flag;
+  p.block_table = a->block_table;
+  p.bt_stride = a->block_table_stride;
+  p.page_size = ps;
+  p.seq_lens = a->seq_lens;
+  CUtensorMap mk, mv;
+  int rc;
+  const int rows = std::min(ps, kDecodeTile);
+  if ((rc = make_map_4d(&mk, a->k_pages, kDecodeD, ps, a->heads_kv, a->num_pages, a->token_stride, a->head_stride,
+                        a->page_stride, rows, 2)))
+    return rc;
+  if ((rc = make_map_4d(&mv, a->v_pages, kDecodeD, ps, a->heads_kv, a->num_pages, a->token_stride, a->head_stride,
+                        a->page_stride, rows, 2)))
+    return rc;
+  return dispatch<true>(R, mk, mv, p, static_cast<cudaStream_t>(stream));
 }
 
 extern "C" int nt_decode_num_splits(int32_t batch, int32_t heads_kv, int32_t seq_kv, int32_t requested) {

@@ -34,6 +34,12 @@ struct DecodeParams {
   int splits, keys_per_split;
   float* ws;  // [B*Hkv, splits, R, D + 2]  (O, m, l)
   int* err;
+  // paged KV cache (decode_split_kernel<R, true>): K/V tokens live in pages of
+  // `page_size` tokens; block_table[b * bt_stride + i] is the physical page of
+  // logical page i of sequence b, seq_lens[b] its key count (<= M)
+  const int* block_table;
+  int bt_stride, page_size;
+  const int* seq_lens;
 };
 
 constexpr int kDecodeThreads = 128;
@@ -64,7 +70,8 @@ constexpr int kDecodeConsumers = 256;                    // 8 consumer warps (wa
 constexpr int kDecodeCTAThreads = 128 + kDecodeConsumers;  // warpgroup 0: TMA producer + 3 idle warps
 constexpr int kDecodePanel = kDecodeTile * 128;          // one 64-dim swizzle-128B panel (8 KB)
 constexpr int kDecodeTileBytes = 2 * kDecodePanel;       // 64 keys x 128 dims bf16 (16 KB)
-constexpr int kDecodeSmem = kDecodeStages * 2 * kDecodeTileBytes + 1024 + 2 * kDecodeStages * 8 + 64;
+constexpr int kDecodeBtChunk = 2048;  // paged: block-table entries staged in shared memory at a time
+constexpr int kDecodeSmem = kDecodeStages * 2 * kDecodeTileBytes + 1024 + 2 * kDecodeStages * 8 + 64 + 4 * kDecodeBtChunk;
 template <int R>
 struct DecodeShape {
   static constexpr int TPK = (R >= 8) ? 16 : 8;  // threads per key
@@ -76,7 +83,7 @@ struct DecodeShape {
 // One CTA = (split, batch x kv-head group).  Warp 0 streams K/V tiles with TMA into a
 // kDecodeStages-deep ring; warpgroups 1-2 (256 threads) consume them from shared memory.
 // setmaxnreg moves the idle registers of warpgroup 0 to the consumers.
-template <int R>
+template <int R, bool PAGED = false>
 __global__ void __launch_bounds__(kDecodeCTAThreads, 1)
     decode_split_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                         const DecodeParams p) {
@@ -88,6 +95,7 @@ __global__ void __launch_bounds__(kDecodeCTAThreads, 1)
   uint8_t* smem = smem_raw + (((raw_u32 + 1023u) & ~1023u) - raw_u32);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kDecodeStages * 2 * kDecodeTileBytes);
   uint64_t* empty = full + kDecodeStages;
+  int* sbt = reinterpret_cast<int*>(empty + kDecodeStages + 8);  // paged: block-table chunk
 
   const int s = blockIdx.x;
   const int grp = blockIdx.y;  // b * Hkv + hkv
@@ -95,7 +103,8 @@ __global__ void __launch_bounds__(kDecodeCTAThreads, 1)
   const int warp = __shfl_sync(0xffffffffu, threadIdx.x / 32, 0);
   const int lane = threadIdx.x & 31;
   const int j0 = s * p.keys_per_split;  // multiple of kDecodeTile
-  const int j1 = min(p.M, j0 + p.keys_per_split);
+  const int seq_len = PAGED ? min(p.M, p.seq_lens[b]) : p.M;
+  const int j1 = min(seq_len, j0 + p.keys_per_split);
   const int ntiles = (j1 > j0) ? (j1 - j0 + kDecodeTile - 1) / kDecodeTile : 0;
 
   if (warp == 0 && lane == 0) {
@@ -111,7 +120,52 @@ __global__ void __launch_bounds__(kDecodeCTAThreads, 1)
 
   if (warp < 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
-    if (warp == 0 && lane == 0) {
+    if (PAGED && warp == 0) {
+      // the whole warp stages this split's block-table entries in shared memory
+      // (coalesced, 8 independent loads in flight per lane); lane 0 then issues
+      // the page-gather TMAs.  Entries past kDecodeBtChunk are read from global.
+      const int rows = min(kDecodeTile, p.page_size);
+      const int last_page = (seq_len - 1) / p.page_size;
+      const int* bt = p.block_table + (long long)b * p.bt_stride;
+      const int first = j0 / p.page_size;
+      const int n_pages = (ntiles > 0) ? min(kDecodeBtChunk, min(last_page, (j1 - 1) / p.page_size) - first + 1) : 0;
+      for (int i0 = 0; i0 < n_pages; i0 += 32 * 8) {
+        int v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = i0 + u * 32 + lane;
+          v[u] = (i < n_pages) ? __ldg(bt + first + i) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = i0 + u * 32 + lane;
+          if (i < n_pages) sbt[i] = v[u];
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        for (int t = 0; t < ntiles; ++t) {
+          const int slot = t % kDecodeStages;
+          mbar_wait(&empty[slot], ((t / kDecodeStages) & 1) ^ 1, p.err, 11);
+          mbar_arrive_expect_tx(&full[slot], 2 * kDecodeTileBytes);
+          uint8_t* sk = smem + slot * 2 * kDecodeTileBytes;
+          uint8_t* sv = sk + kDecodeTileBytes;
+          const int row = j0 + t * kDecodeTile;
+          for (int sub = 0; sub < kDecodeTile / rows; ++sub) {
+            const int tok = row + sub * rows;
+            // tokens past the sequence end read its last page; the consumers mask them
+            const int lp = min(tok / p.page_size, last_page);
+            const int page = (lp - first < n_pages) ? sbt[lp - first] : __ldg(bt + lp);
+            const int in_page = tok % p.page_size;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              tma_load_4d(sk + h * kDecodePanel + sub * rows * 128, &tmK, &full[slot], h * 64, in_page, hkv, page);
+              tma_load_4d(sv + h * kDecodePanel + sub * rows * 128, &tmV, &full[slot], h * 64, in_page, hkv, page);
+            }
+          }
+        }
+      }
+    } else if (!PAGED && warp == 0 && lane == 0) {
       for (int t = 0; t < ntiles; ++t) {
         const int slot = t % kDecodeStages;
         mbar_wait(&empty[slot], ((t / kDecodeStages) & 1) ^ 1, p.err, 11);
@@ -119,10 +173,12 @@ __global__ void __launch_bounds__(kDecodeCTAThreads, 1)
         uint8_t* sk = smem + slot * 2 * kDecodeTileBytes;
         uint8_t* sv = sk + kDecodeTileBytes;
         const int row = j0 + t * kDecodeTile;
+        {
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          tma_load_4d(sk + h * kDecodePanel, &tmK, &full[slot], h * 64, row, hkv, b);
-          tma_load_4d(sv + h * kDecodePanel, &tmV, &full[slot], h * 64, row, hkv, b);
+          for (int h = 0; h < 2; ++h) {
+            tma_load_4d(sk + h * kDecodePanel, &tmK, &full[slot], h * 64, row, hkv, b);
+            tma_load_4d(sv + h * kDecodePanel, &tmV, &full[slot], h * 64, row, hkv, b);
+          }
         }
       }
     }

@@ -163,5 +163,83 @@ class DecodePlan:
             raise DivisionByZero("tile divide: softmax denominator is zero")
 
 
+class PagedDecodePlan:
+    """K2 split-KV decode over a paged KV cache (nt_attn_decode_paged).
+
+    ``k_pages`` / ``v_pages``: bf16 page pools, ``layout="NHD"`` ->
+    [num_pages, page_size, Hkv, 128] or ``"HND"`` -> [num_pages, Hkv, page_size, 128]
+    (any strides with the head dim contiguous).  ``block_table``: int32
+    [B, max_pages]; ``seq_lens``: int32 [B] keys per sequence.  ``q`` / ``o``:
+    [B, Hq, Nq, 128].  The MA program is the dense decode kernel; paging is how
+    a serving runtime lays out its K/V buffers.
+    """
+
+    def __init__(self, q: torch.Tensor, k_pages: torch.Tensor, v_pages: torch.Tensor, block_table: torch.Tensor,
+                 seq_lens: torch.Tensor, o: torch.Tensor, scale: Optional[float], layout: str = "NHD",
+                 max_seq_kv: Optional[int] = None, num_splits: int = 0, err_flag: Optional[torch.Tensor] = None):
+        q, o = _as4(q), _as4(o)
+        for name, t in (("q", q), ("k_pages", k_pages), ("v_pages", v_pages)):
+            if t.dtype != torch.bfloat16 or not t.is_cuda:
+                raise InvalidArguments(f"{name} must be a CUDA bf16 tensor")
+        if k_pages.shape != v_pages.shape or k_pages.stride() != v_pages.stride() or k_pages.dim() != 4:
+            raise InvalidArguments("k_pages / v_pages must be rank-4 pools of identical shape and strides")
+        if block_table.dtype != torch.int32 or seq_lens.dtype != torch.int32:
+            raise InvalidArguments("block_table and seq_lens must be int32")
+        if layout == "NHD":
+            P, ps, Hkv, D = k_pages.shape
+            sp, st, sh = k_pages.stride(0), k_pages.stride(1), k_pages.stride(2)
+        elif layout == "HND":
+            P, Hkv, ps, D = k_pages.shape
+            sp, sh, st = k_pages.stride(0), k_pages.stride(1), k_pages.stride(2)
+        else:
+            raise InvalidArguments("layout must be 'NHD' or 'HND'")
+        B, Hq, Nq, Dq = q.shape
+        if Dq != D or k_pages.stride(-1) != 1 or tuple(o.shape) != (B, Hq, Nq, D) or Hq % Hkv:
+            raise InvalidArguments("q/o/page shapes inconsistent")
+        bt = block_table.contiguous()
+        if bt.dim() != 2 or bt.shape[0] != B or seq_lens.shape != (B,):
+            raise InvalidArguments("block_table must be [B, max_pages] and seq_lens [B]")
+        M = int(max_seq_kv) if max_seq_kv is not None else int(bt.shape[1]) * ps
+        L = _lib.lib()
+        splits = int(L.nt_decode_num_splits(B, Hkv, M, int(num_splits)))
+        rows = (Hq // Hkv) * Nq
+        ws_bytes = int(L.nt_decode_workspace_bytes(B, Hkv, rows, D, splits))
+        self.ws = torch.empty(max(ws_bytes // 4, 1), dtype=torch.float32, device=q.device)
+        self.err = err_flag if err_flag is not None else torch.zeros(1, dtype=torch.int32, device=q.device)
+        a = _lib.DecodePagedArgs()
+        a.q, a.o = _t4(q), _t4(o)
+        a.k_pages, a.v_pages = k_pages.data_ptr(), v_pages.data_ptr()
+        a.page_stride, a.token_stride, a.head_stride = sp, st, sh
+        a.num_pages, a.page_size = P, ps
+        a.block_table, a.block_table_stride = bt.data_ptr(), bt.stride(0)
+        a.seq_lens = seq_lens.data_ptr()
+        a.batch, a.heads_q, a.heads_kv, a.seq_q, a.max_seq_kv, a.head_dim = B, Hq, Hkv, Nq, M, D
+        a.scale = 1.0 if scale is None else float(scale)
+        a.num_splits = splits
+        a.out_dtype = _lib.NT_DTYPE_F32 if o.dtype == torch.float32 else _lib.NT_DTYPE_BF16
+        a.workspace = self.ws.data_ptr()
+        a.err_flag = self.err.data_ptr()
+        self.args, self.splits = a, splits
+        self.tensors = (q, k_pages, v_pages, bt, seq_lens, o)
+        self.shape = (B, Hq, Hkv, Nq, M, D)
+        self._fn = L.nt_attn_decode_paged
+        self._ref = C.byref(a)
+        self.mask_kind = "none"
+
+    def launch(self, stream=None) -> None:
+        st = self._fn(self._ref, _stream_handle(stream))
+        if st:
+            _lib.check(st, "nt_attn_decode_paged")
+
+    def kv_bytes(self) -> int:
+        """K+V bytes the launch streams: every sequence's keys (seq_lens, read on the host)."""
+        _, _, Hkv, _, _, D = self.shape
+        return int(self.tensors[4].sum().item()) * Hkv * D * 2 * 2
+
+    def check_errors(self) -> None:
+        if int(self.err.item()) & 1:
+            raise DivisionByZero("tile divide: softmax denominator is zero (empty sequence)")
+
+
 def decode_eligible(n_rows_per_group: int, d: int, mask_kind: str) -> bool:
     return mask_kind == "none" and d == 128 and n_rows_per_group in (1, 2, 4, 8)
