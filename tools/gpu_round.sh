@@ -1,11 +1,21 @@
-# full GPU gate + per-kernel ncu captures (one GPU, short commands)
-mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q --timeout 300 > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?; tail -3 gpurun_out/pytest_gpu.log
-timeout 120 python -c "import __graft_entry__ as g; g.smoke()"; echo smoke=$?
-for c in llama8k_causal bert512 decode32k gemm_chain_e4096 gemm_chain_e128 attn256 llama2k_causal llama16k_causal; do
-  timeout 300 python bench.py --config $c --steps 10 --warmup 3 > gpurun_out/bench_$c.log 2>&1; echo bench_$c=$?
+# Round gate on one B200: GPU tests, smoke, every bench config (with CPU baseline),
+# the reference arm, ncu captures of each kernel family and the default launch list.
+mkdir -p gpurun_out/round
+cd $GRAFT_REPO_ROOT 2>/dev/null || true
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/round/nvidia_smi.txt
+timeout 1500 python -m pytest tests -m gpu -q --timeout 300 > gpurun_out/round/pytest_gpu.log 2>&1; echo pytest=$?
+tail -3 gpurun_out/round/pytest_gpu.log
+timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/round/smoke.log 2>&1; echo smoke=$?
+for c in llama8k_causal llama2k_causal llama16k_causal bert512 attn256 decode32k decode32k_paged16 decode32k_paged64 gemm_chain_e4096 gemm_chain_e128; do
+  timeout 600 python bench.py --config $c --steps 10 --warmup 3 > gpurun_out/round/bench_$c.json.log 2>&1; echo bench_$c=$?
 done
-timeout 300 ncu --set full --clock-control none --import-source on -k regex:decode_split -s 3 -c 1 -o gpurun_out/decode32k python bench.py --config decode32k --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_decode.log 2>&1; echo ncu_decode=$?
-timeout 300 ncu --set full --clock-control none --import-source on -k regex:gemm_kernel -s 6 -c 1 -o gpurun_out/gemm4k python bench.py --config gemm_chain_e4096 --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_gemm.log 2>&1; echo ncu_gemm=$?
-timeout 300 ncu --set full --clock-control none --import-source on -k regex:attn_fwd -s 3 -c 1 -o gpurun_out/attn8k python bench.py --config llama8k_causal --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_attn.log 2>&1; echo ncu_attn=$?
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --csv --log-file gpurun_out/launches_llama8k.csv python bench.py --config llama8k_causal --steps 5 --warmup 3 --no-cpu-baseline > /dev/null 2>&1; echo ncu_launches=$?
+timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/round/bench_reference.json.log 2>&1; echo ref=$?
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/round/launches_llama8k.csv python bench.py --steps 5 --warmup 3 --no-cpu-baseline > /dev/null 2>&1; echo launches=$?
+cap() { timeout 600 ncu --set full --clock-control none --import-source on -k regex:$2 -s $3 -c 1 -o gpurun_out/round/$1 python bench.py --config $4 --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/round/ncu_$1.log 2>&1; echo ncu_$1=$?; }
+cap attn_llama8k attn_fwd 3 llama8k_causal
+cap attn_bert512 attn_fwd 3 bert512
+cap decode32k decode_split 3 decode32k
+cap decode32k_paged16 decode_split 3 decode32k_paged16
+cap gemm4k gemm_kernel 6 gemm_chain_e4096
+cap chain_e128 chain_kernel 3 gemm_chain_e128
+ls -la gpurun_out/round | head -40
