@@ -4,8 +4,12 @@ The MA kernel computes per 64-row block
 ``T = dot(X_rows, W1[:, f-tile])`` then ``Y += dot(T, W2[f-tile, :])`` with Y
 read-modify-written in Global every iteration.  On B200:
 
-* E <= 256: ``nt_gemm_chain`` keeps T and the Y accumulator in TMEM (one
-  fused kernel, T rounded to bf16 as the second MMA's operand);
+* E <= 256 and N < 2048: ``nt_gemm_chain`` keeps T and the Y accumulator in
+  TMEM (one fused kernel, T rounded to bf16 as the second MMA's operand);
+  with N >= 2048 rows the two-GEMM realisation fills the machine better and
+  wins despite the T round trip through HBM (B200 A/B, ``tools/chain_ab.py``:
+  4096^3 x 128: fused 207 us, two GEMMs 124 us; 1024 x 4096^2 x 128: fused
+  49 us, two GEMMs 52 us);
 * E > 256 (BASELINE config 2 at E=4096, schedulable only with
   max_tile_elems >= 262144): the 128 x E fp32 accumulator
   cannot live in TMEM, so the same MA is realised as T = X.W1 (bf16) then
@@ -63,6 +67,9 @@ class GemmPlan:
             _lib.check(st, "nt_gemm")
 
 
+FUSED_MAX_ROWS = 2048
+
+
 class ChainPlan:
     """Y = (X . W1) . W2 -- fused (E <= 256) or as two GEMMs."""
 
@@ -74,7 +81,7 @@ class ChainPlan:
         if K2 != K or F2 != F or tuple(y.shape) != (N, E):
             raise InvalidArguments("GEMM chain shapes inconsistent")
         self.flops = 2.0 * N * K * F + 2.0 * N * F * E
-        self.fused = E <= 256 and not force_two_gemms
+        self.fused = E <= 256 and N < FUSED_MAX_ROWS and not force_two_gemms
         self.tensors = (x, w1, w2, y)
         if self.fused:
             c = _lib.ChainArgs()

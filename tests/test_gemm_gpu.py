@@ -81,3 +81,21 @@ def test_two_gemm_chain_realisation_e4096_shape():
     plan.launch()
     torch.cuda.synchronize()
     _check(y.cpu().numpy(), reference_math.gemm_chain_fp64(x, w1, w2))
+
+
+def test_many_rows_small_e_uses_two_gemms():
+    """N >= 2048: the two-GEMM realisation is chosen (faster on B200) and matches fp64."""
+    from paper_2604_14825_b200.gemm import FUSED_MAX_ROWS, ChainPlan
+
+    N, K, F, E = FUSED_MAX_ROWS, 256, 384, 128
+    g = np.random.default_rng(11)
+    x = round_bf16(g.standard_normal((N, K)))
+    w1 = round_bf16(g.standard_normal((K, F)) / np.sqrt(K))
+    w2 = round_bf16(g.standard_normal((F, E)) / np.sqrt(F))
+    tx, t1, t2 = (torch.from_numpy(v).cuda().bfloat16() for v in (x, w1, w2))
+    y = torch.empty((N, E), dtype=torch.float32, device="cuda")
+    plan = ChainPlan(tx, t1, t2, y)
+    assert not plan.fused and plan.realisation == "gemm x2"
+    plan.launch()
+    torch.cuda.synchronize()
+    _check(y.cpu().numpy(), reference_math.gemm_chain_fp64(x, w1, w2))
