@@ -180,6 +180,12 @@ int nt_module_unload(nt_module* module);
 int nt_cast_f32_to_bf16(const float* src, void* dst, int64_t n, void* stream);
 int nt_cast_bf16_to_f32(const void* src, float* dst, int64_t n, void* stream);
 
+/* strided host<->device block copy (cudaMemcpy2DAsync, any direction): `height`
+ * rows of `width` bytes, row pitches in bytes.  Used by the streamed execution
+ * path to move (batch x head) x rows slices of [B, H, S, D] tensors in one call. */
+int nt_memcpy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width, int64_t height,
+                      void* stream);
+
 /* introspection */
 int nt_abi_version(void);
 const char* nt_last_error(void);

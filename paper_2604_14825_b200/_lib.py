@@ -24,6 +24,7 @@ EXPORTED = (
     "nt_gemm_chain", "nt_gemm_chain_workspace_bytes",
     "nt_cast_f32_to_bf16", "nt_cast_bf16_to_f32", "nt_abi_version", "nt_last_error", "nt_launch_count",
     "nt_module_load", "nt_module_function", "nt_launch", "nt_module_unload", "nt_attn_decode_paged",
+    "nt_memcpy2d_async",
 )
 
 
@@ -107,6 +108,9 @@ def lib():
             L.nt_launch.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(C.c_void_p),
                                     C.c_void_p]
             L.nt_module_unload.argtypes = [C.c_void_p]
+            L.nt_memcpy2d_async.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
+                                            C.c_void_p]
+            L.nt_memcpy2d_async.restype = C.c_int
             L.nt_last_error.restype = C.c_char_p
             L.nt_launch_count.restype = C.c_int64
             for name in ("nt_attn_fwd", "nt_attn_decode", "nt_attn_decode_paged", "nt_gemm", "nt_gemm_chain",

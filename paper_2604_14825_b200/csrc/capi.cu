@@ -236,6 +236,14 @@ extern "C" int nt_debug_set_trace(unsigned long long* buf, int cta) {
 }
 #endif
 
+extern "C" int nt_memcpy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width,
+                                 int64_t height, void* stream) {
+  if (width <= 0 || height <= 0) return NT_OK;
+  return check_cuda(cudaMemcpy2DAsync(dst, (size_t)dpitch, src, (size_t)spitch, (size_t)width, (size_t)height,
+                                      cudaMemcpyDefault, static_cast<cudaStream_t>(stream)),
+                    "cudaMemcpy2DAsync");
+}
+
 extern "C" int nt_abi_version(void) { return NT_ABI_VERSION; }
 extern "C" const char* nt_last_error(void) { return g_last_error.c_str(); }
 extern "C" int64_t nt_launch_count(void) { return g_launches.load(); }

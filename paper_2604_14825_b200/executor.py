@@ -188,6 +188,12 @@ def _attention_streamed(spec: AttentionSpec, inputs: dict, outer, mask_kind, out
     s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
     s_in.wait_stream(comp)  # device buffers were allocated on the compute stream
     err = torch.zeros(1, dtype=torch.int32, device=dev)
+    # too few (batch, kv-head) groups to pipeline: chunk the query rows instead
+    # (at Llama 8K, B=1, 4 chunks both ways are PCIe-bound: groups 2.76 ms, rows 2.85 ms)
+    if (kind == "causal" and spec.m == spec.n and B * Hkv < chunks and not cast
+            and all(t.is_contiguous() for t in (q_h, k_h, v_h, o_h))):
+        return _causal_rows_streamed(spec, q_h, k_h, v_h, o_h, q_d, k_d, v_d, o_d, out, comp, s_in, s_out, err,
+                                     chunks)
     units = B * Hkv
     n = max(1, min(chunks, units))
     bounds = [units * i // n for i in range(n + 1)]
@@ -241,6 +247,63 @@ def _attention_streamed(spec: AttentionSpec, inputs: dict, outer, mask_kind, out
         raise RuntimeError(f"device pipeline timeout (code {flag & 0xff})")
     info = {"kernel": type(plans[0]).__name__, "streamed": True, "chunks": n, "mask": kind,
             "launches": launches, "ma_tile": (spec.block_m, spec.block_n)}
+    return out, ev0.elapsed_time(ev1), flops, info
+
+
+def _causal_rows_streamed(spec, q_h, k_h, v_h, o_h, q_d, k_d, v_d, o_d, out, comp, s_in, s_out, err, chunks):
+    """Causal prefill with few (batch, kv-head) groups: chunk the QUERY ROWS.
+
+    Chunk c holds rows [r0, r1) of every head; its kernel needs keys [0, r1), so
+    K/V arrive incrementally (rows [r_prev, r1) per chunk) and every chunk
+    launch keeps all heads -- a full persistent grid -- with
+    ``causal_offset = r0`` (key j visible to row r0 + i iff j <= r0 + i).
+    Copies are one cudaMemcpy2DAsync per tensor per chunk.
+    """
+    L = _lib.lib()
+    B, Hq, N, D = q_h.shape
+    Hkv = k_h.shape[1]
+    esz = q_h.element_size()
+    osz = o_h.element_size()
+    n = max(1, min(chunks, -(-N // 256)))
+    bounds = [min(N, -(-(N * c // n) // 256) * 256) for c in range(n)] + [N]
+    bounds = sorted(set(bounds))
+
+    def copy2d(dst, src, rows0, rows1, total_rows, height, elem, stream):
+        pitch = total_rows * D * elem
+        off = rows0 * D * elem
+        _lib.check(L.nt_memcpy2d_async(dst.data_ptr() + off, pitch, src.data_ptr() + off, pitch,
+                                       (rows1 - rows0) * D * elem, height, stream.cuda_stream),
+                   "nt_memcpy2d_async")
+
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(comp)
+    plans, flops, kv_done = [], 0.0, 0
+    for r0, r1 in zip(bounds[:-1], bounds[1:]):
+        copy2d(q_d, q_h, r0, r1, N, B * Hq, esz, s_in)
+        copy2d(k_d, k_h, kv_done, r1, N, B * Hkv, esz, s_in)
+        copy2d(v_d, v_h, kv_done, r1, N, B * Hkv, esz, s_in)
+        kv_done = r1
+        comp.wait_stream(s_in)
+        plan = AttentionPlan(q_d[:, :, r0:r1], k_d[:, :, :r1], v_d[:, :, :r1], o_d[:, :, r0:r1], spec.scale,
+                             "causal", causal_offset=r0, err_flag=err)
+        plan.launch(comp)
+        plans.append(plan)
+        flops += plan.flops()
+        s_out.wait_stream(comp)
+        copy2d(o_h, o_d, r0, r1, N, B * Hq, osz, s_out)
+    comp.wait_stream(s_out)
+    ev1.record(comp)
+    ev1.synchronize()
+    for t in (q_d, k_d, v_d, o_d):
+        t.record_stream(s_in)
+        t.record_stream(s_out)
+    flag = int(err.item())
+    if flag & 1:
+        raise DivisionByZero("tile divide: softmax denominator is zero (row fully masked)")
+    if flag & 0x100:
+        raise RuntimeError(f"device pipeline timeout (code {flag & 0xff})")
+    info = {"kernel": "AttentionPlan", "streamed": True, "chunks": len(bounds) - 1, "chunking": "query rows",
+            "mask": "causal", "launches": len(plans), "ma_tile": (spec.block_m, spec.block_n)}
     return out, ev0.elapsed_time(ev1), flops, info
 
 

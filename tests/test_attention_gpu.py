@@ -174,6 +174,7 @@ def test_exp2_poly_no_nan_on_masked_tiles():
 
 
 @pytest.mark.parametrize("case,outer,dtype", [("causal512", (2, 8, 2), torch.bfloat16),
+                                              ("causal512", (1, 8, 2), torch.bfloat16),
                                               ("bert512", (3, 4, 4), torch.float32),
                                               ("decode4", (2, 8, 4), torch.bfloat16)])
 def test_streamed_host_execution_matches_resident(case, outer, dtype):
@@ -197,6 +198,8 @@ def test_streamed_host_execution_matches_resident(case, outer, dtype):
     out = torch.empty(tuple(ref[mod.output].shape), dtype=torch.bfloat16).pin_memory()
     got, rep = execute_ma(mod, host, out=out, chunks=3, **kw)
     assert got[mod.output] is out and rep.realisation[0]["streamed"]
+    if outer[0] * outer[2] < 3 and "Mask" in [b.name for b in mod.inputs()]:
+        assert rep.realisation[0]["chunking"] == "query rows"
     if rep.realisation[0]["kernel"] == "DecodePlan":
         # split-KV counts depend on the launch's (batch x kv-head) size: same math, other fp order
         _check(out.float().numpy(), ref[mod.output].float().cpu().numpy())

@@ -11,7 +11,7 @@ host = {"Q": torch.randn(B, Hq, N, D, generator=g).to(torch.bfloat16).pin_memory
         "V": torch.randn(B, Hkv, N, D, generator=g).to(torch.bfloat16).pin_memory()}
 out = torch.empty(B, Hq, N, D, dtype=torch.bfloat16).pin_memory()
 kw = dict(outer=(B, Hq, Hkv), mask_kind="causal", out_dtype="bf16", return_torch=True, out=out)
-for chunks in (1, 2, 4, 8, 16, 32):
+for chunks in (1, 2, 3, 4, 6, 8, 16):
     for _ in range(3):
         execute_ma(mod, host, chunks=chunks, **kw)
     ts, hs = [], []
