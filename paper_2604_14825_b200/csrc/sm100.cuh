@@ -64,7 +64,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, int* e
     for (int i = 0; i < 64; ++i)
       if (mbar_try_wait(bar, parity)) return;
     if (globaltimer() - t0 > NT_WAIT_TIMEOUT_NS) {
-      if (err) atomicOr(err, 0x100 | code);
+      if (err) atomicOr(err, 1 << (8 + (code & 15)));  // bit 8 + code: which wait timed out
       __threadfence_system();
       asm volatile("trap;");
     }
@@ -114,6 +114,9 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 // ------------------------------------------------------------------ tcgen05

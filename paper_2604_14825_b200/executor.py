@@ -243,8 +243,8 @@ def _attention_streamed(spec: AttentionSpec, inputs: dict, outer, mask_kind, out
     flag = int(err.item())
     if flag & 1:
         raise DivisionByZero("tile divide: softmax denominator is zero (row fully masked)")
-    if flag & 0x100:
-        raise RuntimeError(f"device pipeline timeout (code {flag & 0xff})")
+    if flag >> 8:
+        raise RuntimeError(f"device pipeline timeout (wait codes {[c for c in range(16) if flag >> (8 + c) & 1]})")
     info = {"kernel": type(plans[0]).__name__, "streamed": True, "chunks": n, "mask": kind,
             "launches": launches, "ma_tile": (spec.block_m, spec.block_n)}
     return out, ev0.elapsed_time(ev1), flops, info
@@ -300,8 +300,8 @@ def _causal_rows_streamed(spec, q_h, k_h, v_h, o_h, q_d, k_d, v_d, o_d, out, com
     flag = int(err.item())
     if flag & 1:
         raise DivisionByZero("tile divide: softmax denominator is zero (row fully masked)")
-    if flag & 0x100:
-        raise RuntimeError(f"device pipeline timeout (code {flag & 0xff})")
+    if flag >> 8:
+        raise RuntimeError(f"device pipeline timeout (wait codes {[c for c in range(16) if flag >> (8 + c) & 1]})")
     info = {"kernel": "AttentionPlan", "streamed": True, "chunks": len(bounds) - 1, "chunking": "query rows",
             "mask": "causal", "launches": len(plans), "ma_tile": (spec.block_m, spec.block_n)}
     return out, ev0.elapsed_time(ev1), flops, info

@@ -101,8 +101,8 @@ class AttentionPlan:
         flag = int(self.err.item())
         if flag & 1:
             raise DivisionByZero("tile divide: softmax denominator is zero (row fully masked)")
-        if flag & 0x100:
-            raise RuntimeError(f"device pipeline timeout (code {flag & 0xff})")
+        if flag >> 8:
+            raise RuntimeError(f"device pipeline timeout (wait codes {[c for c in range(16) if flag >> (8 + c) & 1]})")
 
 
 def _causal_pairs(N: int, M: int, off: int) -> int:
