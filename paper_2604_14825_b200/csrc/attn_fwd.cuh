@@ -58,7 +58,7 @@ struct AttnFwdParams {
   long long mask_row_stride;
   void* o;            // output (bf16, or fp32 if OUT_F32), element strides below; D contiguous
   long long o_sb, o_sh, o_sn;
-  int* err;  // bit 0: zero denominator (fully masked row); 0x100|k: pipeline timeout
+  int* err;  // bit 0: zero denominator (fully masked row); bit 8+k: wait k timed out
   int* work;  // [next, done] dynamic item counter (zero at launch, reset by the last CTA) or null
 };
 
