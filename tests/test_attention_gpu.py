@@ -205,3 +205,33 @@ def test_streamed_host_execution_matches_resident(case, outer, dtype):
         _check(out.float().numpy(), ref[mod.output].float().cpu().numpy())
     else:
         assert torch.equal(out, ref[mod.output].cpu())
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,N,D,causal", [(3, 16, 4, 1536, 128, True), (16, 12, 12, 512, 64, False),
+                                                 (2, 32, 8, 2048, 128, True)])
+def test_persistent_multi_item_repeated_launches(B, Hq, Hkv, N, D, causal):
+    """More work items than SMs (each CTA walks several, greedy from the device counter);
+    repeated launches of one plan reuse the self-resetting counter and give identical bits."""
+    from paper_2604_14825_b200.runtime import AttentionPlan
+
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(B * N + D)
+    q = torch.randn((B, Hq, N, D), generator=g, device=dev).bfloat16()
+    k = torch.randn((B, Hkv, N, D), generator=g, device=dev).bfloat16()
+    v = torch.randn((B, Hkv, N, D), generator=g, device=dev).bfloat16()
+    o = torch.empty((B, Hq, N, D), dtype=torch.bfloat16, device=dev)
+    plan = AttentionPlan(q, k, v, o, 1.0 / np.sqrt(D), "causal" if causal else "none")
+    assert plan.shape and (N + 255) // 256 * B * Hq > 148
+    plan.launch()
+    torch.cuda.synchronize()
+    first = o.clone()
+    for _ in range(5):
+        plan.launch()
+    torch.cuda.synchronize()
+    plan.check_errors()
+    assert torch.equal(o, first)
+    assert plan.work.tolist() == [0, 0]  # counter reset by the last CTA
+    ref = torch.nn.functional.scaled_dot_product_attention(
+        q.float(), k.float().repeat_interleave(Hq // Hkv, 1), v.float().repeat_interleave(Hq // Hkv, 1),
+        is_causal=causal, scale=1.0 / np.sqrt(D))
+    _check(o.float().cpu().numpy(), ref.cpu().numpy())
