@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 
 #include "../../include/nautilus_b200.h"
@@ -52,6 +53,36 @@ int launch_gemm(const nt_gemm_args* a, cudaStream_t st) {
   kern<<<grid, kGemmThreads, smem, st>>>(ma, mb, p);
   g_launches++;
   return check_cuda(cudaGetLastError(), "gemm launch");
+}
+
+template <bool F32>
+int launch_gemm2(const nt_gemm_args* a, cudaStream_t st) {
+  CUtensorMap ma, mb;
+  int rc;
+  if ((rc = make_map_2d(&ma, a->a, a->k, a->m, a->lda, 64, 128, 2, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+  if ((rc = make_map_2d(&mb, a->b, a->n, a->k, a->ldb, 64, 64, 2, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+  GemmParams p{};
+  p.M = a->m;
+  p.N = a->n;
+  p.K = a->k;
+  p.tiles_m = (a->m + 255) / 256;
+  p.tiles_n = (a->n + 255) / 256;
+  p.c = a->c;
+  p.ldc = a->ldc;
+  auto kern = gemm2_kernel<F32>;
+  const int smem = Gemm2Cfg::SMEM_BYTES;
+  static bool configured = false;
+  if (!configured) {
+    if ((rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+                         "cudaFuncSetAttribute(gemm2)")))
+      return rc;
+    configured = true;
+  }
+  const int tiles = p.tiles_m * p.tiles_n;
+  const int grid = 2 * std::min(tiles, sm_count() / 2);  // one CTA pair per tile, persistent
+  kern<<<grid, kGemmThreads, smem, st>>>(ma, mb, p);
+  g_launches++;
+  return check_cuda(cudaGetLastError(), "gemm2 launch");
 }
 
 // F split so that row_blocks x splits ~ fills the SMs
@@ -117,6 +148,13 @@ extern "C" int nt_gemm(const nt_gemm_args* a, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool f32 = a->out_dtype == NT_DTYPE_F32;
   if (a->n <= 128) return f32 ? launch_gemm<128, true>(a, st) : launch_gemm<128, false>(a, st);
+  // CTA pairs when there are enough 256x256 tiles to give every pair one (B200 A/B,
+  // tools/gemm_ab.py: 4096^3 1-SM 103.8 us -> pairs 96.3 us, 8192^3 784 -> 752 us;
+  // 4096x1024x4096 (64 pair tiles) stays faster on single CTAs)
+  static const bool one_sm = getenv("NT_GEMM_1SM") != nullptr;  // A/B switch
+  const long long pair_tiles = (long long)((a->m + 255) / 256) * ((a->n + 255) / 256);
+  if (!one_sm && pair_tiles >= sm_count() / 2)
+    return f32 ? launch_gemm2<true>(a, st) : launch_gemm2<false>(a, st);
   return f32 ? launch_gemm<256, true>(a, st) : launch_gemm<256, false>(a, st);
 }
 

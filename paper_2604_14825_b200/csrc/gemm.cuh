@@ -5,6 +5,10 @@
 // `xY = dot(xT, W2[128*j0:+128, 0:E], acc=Y[...])`, which interpret_ma runs as
 // sequential rank-1 updates (tilecc/ma/interp.py:241-251).
 //
+// Two variants: gemm_kernel (one CTA, M=128 x N=BN tiles) and gemm2_kernel
+// (a CTA pair with tcgen05.mma.cta_group::2, M=256 x N=256 tiles, below),
+// chosen by nt_gemm from the tile count.
+//
 // Persistent, warp-specialised:
 //   warp 0      TMA producer (A K-major panels, B MN-major panels, SWIZZLE_128B)
 //   warp 1      MMA issuer: tcgen05.mma.cta_group::1.kind::f16 M=128 N=BN K=16
@@ -174,6 +178,177 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+}  // namespace nt
+
+namespace nt {
+
+// ---------------------------------------------------------------------------
+// K3 v2: CTA-pair GEMM (tcgen05.mma.cta_group::2, M = 256 x N = 256 per pair).
+// Each CTA of a 2-CTA cluster stages its own 128 rows of A and its own half
+// (128 columns) of B per k-block; the pair leader issues one M=256 x N=256
+// MMA that reads both CTAs' shared memory and accumulates each CTA's 128 rows
+// in its own TMEM.  Per SM the shared-memory traffic per FLOP is 2/3 of the
+// single-CTA 128x256 kernel (TMA writes 32 KB + MMA reads 32 KB per 512
+// tensor clocks = 125 B/clk against 188 B/clk), which is what bounds the
+// single-CTA kernel.
+//   warp 0      TMA producer (both CTAs; bytes counted on the leader's barrier)
+//   warp 1      MMA issuer (leader CTA only)
+//   warps 2-5   epilogue (both CTAs): TMEM -> registers -> global
+struct Gemm2Cfg {
+  static constexpr int BM = 128, BN = 256, BNH = 128, BK = 64;
+  static constexpr int A_BYTES = BM * BK * 2;   // 16 KB: this CTA's 128 rows
+  static constexpr int B_BYTES = BK * BNH * 2;  // 16 KB: this CTA's 128 columns
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int STAGES = 6;
+  static constexpr int SMEM_BAR = STAGES * STAGE;
+  static constexpr int NBAR = 2 * STAGES + 4;
+  static constexpr int SMEM_BYTES = SMEM_BAR + NBAR * 8 + 16 + 1024;
+};
+
+template <bool OUT_F32>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
+    gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                 const GemmParams p) {
+  using C = Gemm2Cfg;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_u32 = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw_u32 + 1023u) & ~1023u) - raw_u32);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::SMEM_BAR);
+  uint64_t* full = bars;                        // [STAGES] (leader's counts both CTAs' bytes)
+  uint64_t* empty = bars + C::STAGES;           // [STAGES] (multicast commit to both CTAs)
+  uint64_t* tfull = bars + 2 * C::STAGES;       // [2]
+  uint64_t* tempty = bars + 2 * C::STAGES + 2;  // [2] leader: 4 epilogue warps x 2 CTAs
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBAR);
+
+  const int warp = __shfl_sync(0xffffffffu, threadIdx.x / 32, 0);
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int pair = (int)cluster_id_x(), npairs = (int)nclusters_x();
+  const int num_tiles = p.tiles_m * p.tiles_n;  // tiles of 256 x 256
+  const int k_blocks = (p.K + C::BK - 1) / C::BK;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);
+    }
+    fence_barrier_init();
+  }
+  cluster_sync_all();  // both CTAs' barriers exist before any remote arrive / complete_tx
+  if (warp == 1) tmem_alloc_pair(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int it = 0;
+      for (int tile = pair; tile < num_tiles; tile += npairs) {
+        const int mb = tile % p.tiles_m, nb = tile / p.tiles_m;
+        for (int kb = 0; kb < k_blocks; ++kb, ++it) {
+          const int s = it % C::STAGES;
+          mbar_wait(&empty[s], ((it / C::STAGES) & 1) ^ 1);
+          if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * C::STAGE);
+          uint8_t* sa = smem + s * C::STAGE;
+          uint8_t* sb = sa + C::A_BYTES;
+          tma_load_2d_pair(sa, &tmA, &full[s], kb * C::BK, mb * 256 + (int)rank * 128);
+#pragma unroll
+          for (int c = 0; c < C::BNH / 64; ++c)
+            tma_load_2d_pair(sb + c * (C::BK * 128), &tmB, &full[s], nb * 256 + (int)rank * 128 + c * 64,
+                             kb * C::BK);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = idesc_bf16(256, 256, 0, 1);
+      const uint32_t sbase = smem_u32(smem);
+      int it = 0, tcount = 0;
+      for (int tile = pair; tile < num_tiles; tile += npairs, ++tcount) {
+        const int acc = tcount & 1;
+        mbar_wait(&tempty[acc], ((tcount >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * 256;
+        for (int kb = 0; kb < k_blocks; ++kb, ++it) {
+          const int s = it % C::STAGES;
+          mbar_wait(&full[s], (it / C::STAGES) & 1);
+          tc_fence_after();
+          const uint32_t sa = sbase + s * C::STAGE;
+          const uint32_t sb = sa + C::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < C::BK / 16; ++k) {
+            const uint64_t ad = sdesc_sw128(sa + k * 32, 16, 1024);
+            const uint64_t bd = sdesc_sw128(sb + k * 2048, C::BK * 128, 1024);
+            umma_ss_pair(d, ad, bd, idesc, (kb | k) ? 1u : 0u);
+          }
+          umma_commit_pair(&empty[s], 0x3);
+        }
+        umma_commit_pair(&tfull[acc], 0x3);
+      }
+    }
+  } else {
+    // epilogue warps 2..5 -> TMEM sub-partitions 2,3,0,1; this CTA's 128 rows x 256 columns
+    const int wq = warp & 3;
+    const int r = wq * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
+    int tcount = 0;
+    for (int tile = pair; tile < num_tiles; tile += npairs, ++tcount) {
+      const int acc = tcount & 1;
+      const int mb = tile % p.tiles_m, nb = tile / p.tiles_m;
+      mbar_wait(&tfull[acc], (tcount >> 1) & 1);
+      tc_fence_after();
+      const int row = mb * 256 + (int)rank * 128 + r;
+      const bool rv = row < p.M;
+#pragma unroll 1
+      for (int c = 0; c < C::BN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tmem + acc * 256 + lane_off + c * 32, v);
+        tmem_wait_ld();
+        const int col0 = nb * C::BN + c * 32;
+        if (rv && col0 < p.N) {
+          if (OUT_F32) {
+            float* cp = static_cast<float*>(p.c) + (long long)row * p.ldc + col0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if (col0 + 4 * i < p.N)
+                *reinterpret_cast<float4*>(cp + 4 * i) =
+                    make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                                __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+          } else {
+            __nv_bfloat16* cp = static_cast<__nv_bfloat16*>(p.c) + (long long)row * p.ldc + col0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              if (col0 + 8 * i < p.N)
+                *reinterpret_cast<uint4*>(cp + 8 * i) = make_uint4(
+                    pack_bf16(__uint_as_float(v[8 * i]), __uint_as_float(v[8 * i + 1])),
+                    pack_bf16(__uint_as_float(v[8 * i + 2]), __uint_as_float(v[8 * i + 3])),
+                    pack_bf16(__uint_as_float(v[8 * i + 4]), __uint_as_float(v[8 * i + 5])),
+                    pack_bf16(__uint_as_float(v[8 * i + 6]), __uint_as_float(v[8 * i + 7])));
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(mapa_shared(&tempty[acc], 0));  // the leader's barrier
+    }
+  }
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // the leader's MMAs and both epilogues are done with TMEM
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem, 512);
   }
 }
 

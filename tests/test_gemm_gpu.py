@@ -99,3 +99,21 @@ def test_many_rows_small_e_uses_two_gemms():
     plan.launch()
     torch.cuda.synchronize()
     _check(y.cpu().numpy(), reference_math.gemm_chain_fp64(x, w1, w2))
+
+
+@pytest.mark.parametrize("M,N,K", [(4096, 4096, 512), (2304, 2816, 320), (4100, 4104, 136)])
+def test_cta_pair_gemm_vs_fp64(M, N, K):
+    """Shapes with >= 74 tiles of 256x256 take the cta_group::2 kernel (incl. ragged M/N edges)."""
+    from paper_2604_14825_b200.gemm import GemmPlan
+
+    g = np.random.default_rng(M + N + K)
+    a = round_bf16(g.standard_normal((M, K)))
+    b = round_bf16(g.standard_normal((K, N)) / np.sqrt(K))
+    ta = torch.from_numpy(a).cuda().bfloat16()
+    tb = torch.from_numpy(b).cuda().bfloat16()
+    c = torch.empty((M, N), dtype=torch.float32, device="cuda")
+    GemmPlan(ta, tb, c).launch()
+    torch.cuda.synchronize()
+    ref = torch.from_numpy(a).double().cuda() @ torch.from_numpy(b).double().cuda()
+    err = (c.double() - ref).abs()
+    assert float(err.max()) <= 2e-2 and float(err.norm() / ref.norm()) <= 1e-2
