@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 
 #include "../../include/nautilus_b200.h"
 #include "common_host.h"
@@ -23,9 +24,24 @@ int sms() {
 
 int choose_splits(int groups, int M, int requested) {
   if (requested > 0) return std::min(requested, std::max(1, (M + 63) / 64));
-  const int by_occupancy = (8 * sms() + groups - 1) / groups;  // ~8 waves of 1-CTA/SM
-  const int by_length = std::max(1, (M + 1023) / 1024);  // >= 16 tiles per split
-  return std::max(1, std::min(by_occupancy, by_length));
+  // one CTA per SM at a time: pick the split count whose last wave is fullest
+  // (wave quantization is the loss of a streaming kernel), among counts that give
+  // at least ~2 waves and keep >= 8 key tiles per split
+  const int n_sm = sms();
+  const int by_length = std::max(1, (M + 511) / 512);
+  const int lo = std::max(1, std::min(by_length, (2 * n_sm + groups - 1) / groups));
+  const int hi = std::max(lo, std::min(by_length, (16 * n_sm + groups - 1) / groups));
+  int best = lo;
+  double best_eff = -1.0;
+  for (int s = lo; s <= hi; ++s) {
+    const double waves = (double)groups * s / n_sm;
+    const double eff = waves / std::ceil(waves);
+    if (eff > best_eff + 1e-3) {
+      best_eff = eff;
+      best = s;
+    }
+  }
+  return best;
 }
 
 template <int R, bool PAGED>
