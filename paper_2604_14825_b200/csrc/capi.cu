@@ -90,6 +90,28 @@ int make_map_2d(CUtensorMap* m, const void* ptr, int64_t inner, int64_t outer, i
   return NT_OK;
 }
 
+// bf16 page pool viewed as 5-D (d_lo 64, token, d_hi 2, head, page): one box
+// {64, rows, 2, 1, 1} brings both 64-dim panels of `rows` tokens of one page
+int make_map_pages_5d(CUtensorMap* m, const void* ptr, int64_t page_size, int64_t heads, int64_t pages,
+                      int64_t token_stride, int64_t head_stride, int64_t page_stride, int rows) {
+  EncodeFn enc = get_encode();
+  if (!enc) return set_error(NT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if (reinterpret_cast<uintptr_t>(ptr) % 16) return set_error(NT_ERR_INVALID, "page pool base not 16B aligned");
+  cuuint64_t dims[5] = {64, (cuuint64_t)page_size, 2, (cuuint64_t)heads, (cuuint64_t)pages};
+  cuuint64_t strides[4] = {(cuuint64_t)(token_stride * 2), 128, (cuuint64_t)(head_stride * 2),
+                           (cuuint64_t)(page_stride * 2)};
+  for (int i = 0; i < 4; ++i)
+    if (strides[i] % 16) return set_error(NT_ERR_INVALID, "page pool strides must be multiples of 16 bytes");
+  cuuint32_t box[5] = {64, (cuuint32_t)rows, 2, 1, 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return set_error(NT_ERR_INVALID, "cuTensorMapEncodeTiled(pages 5d) failed (" + std::to_string((int)r) + ")");
+  return NT_OK;
+}
+
 // ----------------------------------------------------------------- attention
 template <int D, int MASK, bool F32>
 static int launch_attn(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const AttnFwdParams& p,

@@ -44,10 +44,10 @@ int choose_splits(int groups, int M, int requested) {
   return best;
 }
 
-template <int R, bool PAGED>
+template <int R, int PG>
 int launch(const CUtensorMap& mk, const CUtensorMap& mv, DecodeParams& p, cudaStream_t st) {
   int rc;
-  auto kern = decode_split_kernel<R, PAGED>;
+  auto kern = decode_split_kernel<R, PG>;
   static bool configured = false;
   if (!configured) {
     if ((rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kDecodeSmem),
@@ -64,13 +64,13 @@ int launch(const CUtensorMap& mk, const CUtensorMap& mv, DecodeParams& p, cudaSt
   g_launches++;
   return check_cuda(cudaGetLastError(), "decode_combine launch");
 }
-template <bool PAGED>
+template <int PG>
 int dispatch(int R, const CUtensorMap& mk, const CUtensorMap& mv, DecodeParams& p, cudaStream_t st) {
   switch (R) {
-    case 1: return launch<1, PAGED>(mk, mv, p, st);
-    case 2: return launch<2, PAGED>(mk, mv, p, st);
-    case 4: return launch<4, PAGED>(mk, mv, p, st);
-    default: return launch<8, PAGED>(mk, mv, p, st);
+    case 1: return launch<1, PG>(mk, mv, p, st);
+    case 2: return launch<2, PG>(mk, mv, p, st);
+    case 4: return launch<4, PG>(mk, mv, p, st);
+    default: return launch<8, PG>(mk, mv, p, st);
   }
 }
 }  // namespace
@@ -120,7 +120,7 @@ extern "C" int nt_attn_decode(const nt_decode_args* a, void* stream) {
   if ((rc = make_map_4d(&mv, a->v.ptr, kDecodeD, a->seq_kv, a->heads_kv, a->batch, a->v.stride_s, a->v.stride_h,
                         a->v.stride_b, kDecodeTile, 2)))
     return rc;
-  return dispatch<false>(R, mk, mv, p, st);
+  return dispatch<0>(R, mk, mv, p, st);
 }
 
 extern "C" int nt_attn_decode_paged(const nt_decode_paged_args* a, void* stream) {
@@ -158,13 +158,23 @@ extern "C" int nt_attn_decode_paged(const nt_decode_paged_args* a, void* stream)
   CUtensorMap mk, mv;
   int rc;
   const int rows = std::min(ps, kDecodeTile);
-  if ((rc = make_map_4d(&mk, a->k_pages, kDecodeD, ps, a->heads_kv, a->num_pages, a->token_stride, a->head_stride,
-                        a->page_stride, rows, 2)))
-    return rc;
-  if ((rc = make_map_4d(&mv, a->v_pages, kDecodeD, ps, a->heads_kv, a->num_pages, a->token_stride, a->head_stride,
-                        a->page_stride, rows, 2)))
-    return rc;
-  return dispatch<true>(R, mk, mv, p, static_cast<cudaStream_t>(stream));
+  if (rows < kDecodeTile) {  // small pages: one 5-D box per page slice (both 64-dim panels)
+    if ((rc = make_map_pages_5d(&mk, a->k_pages, ps, a->heads_kv, a->num_pages, a->token_stride, a->head_stride,
+                                a->page_stride, rows)))
+      return rc;
+    if ((rc = make_map_pages_5d(&mv, a->v_pages, ps, a->heads_kv, a->num_pages, a->token_stride, a->head_stride,
+                                a->page_stride, rows)))
+      return rc;
+  } else {
+    if ((rc = make_map_4d(&mk, a->k_pages, kDecodeD, ps, a->heads_kv, a->num_pages, a->token_stride,
+                          a->head_stride, a->page_stride, rows, 2)))
+      return rc;
+    if ((rc = make_map_4d(&mv, a->v_pages, kDecodeD, ps, a->heads_kv, a->num_pages, a->token_stride,
+                          a->head_stride, a->page_stride, rows, 2)))
+      return rc;
+  }
+  return rows < kDecodeTile ? dispatch<2>(R, mk, mv, p, static_cast<cudaStream_t>(stream))
+                            : dispatch<1>(R, mk, mv, p, static_cast<cudaStream_t>(stream));
 }
 
 extern "C" int nt_decode_num_splits(int32_t batch, int32_t heads_kv, int32_t seq_kv, int32_t requested) {

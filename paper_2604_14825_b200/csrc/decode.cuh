@@ -83,12 +83,15 @@ struct DecodeShape {
 // One CTA = (split, batch x kv-head group).  Warp 0 streams K/V tiles with TMA into a
 // kDecodeStages-deep ring; warpgroups 1-2 (256 threads) consume them from shared memory.
 // setmaxnreg moves the idle registers of warpgroup 0 to the consumers.
-template <int R, bool PAGED = false>
+// PG: 0 dense KV, 1 paged (pages of >= 64 tokens), 2 paged with small pages (one
+// 5-D TMA box per page slice)
+template <int R, int PG = 0>
 __global__ void __launch_bounds__(kDecodeCTAThreads, 1)
     decode_split_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                         const DecodeParams p) {
   constexpr int D = kDecodeD;
   using SH = DecodeShape<R>;
+  constexpr bool PAGED = PG != 0;
   constexpr int TPK = SH::TPK, DPT = SH::DPT, KPS = SH::KPS, NCH = SH::NCH;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_u32 = smem_u32(smem_raw);
@@ -157,10 +160,17 @@ __global__ void __launch_bounds__(kDecodeCTAThreads, 1)
             const int lp = min(tok / p.page_size, last_page);
             const int page = (lp - first < n_pages) ? sbt[lp - first] : __ldg(bt + lp);
             const int in_page = tok % p.page_size;
+            if constexpr (PG == 2) {
+              // one 5-D box = both 64-dim panels of `rows` tokens: the tile is laid out
+              // [sub][panel][rows][128 B] (see the consumer's address below)
+              tma_load_5d(sk + sub * 2 * rows * 128, &tmK, &full[slot], 0, in_page, 0, hkv, page);
+              tma_load_5d(sv + sub * 2 * rows * 128, &tmV, &full[slot], 0, in_page, 0, hkv, page);
+            } else {
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              tma_load_4d(sk + h * kDecodePanel + sub * rows * 128, &tmK, &full[slot], h * 64, in_page, hkv, page);
-              tma_load_4d(sv + h * kDecodePanel + sub * rows * 128, &tmV, &full[slot], h * 64, in_page, hkv, page);
+              for (int h = 0; h < 2; ++h) {
+                tma_load_4d(sk + h * kDecodePanel, &tmK, &full[slot], h * 64, in_page, hkv, page);
+                tma_load_4d(sv + h * kDecodePanel, &tmV, &full[slot], h * 64, in_page, hkv, page);
+              }
             }
           }
         }
@@ -185,6 +195,7 @@ __global__ void __launch_bounds__(kDecodeCTAThreads, 1)
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 232;");
     const int tc = threadIdx.x - 128;
+    const int rows_log2 = (PG == 2) ? (31 - __clz(min(kDecodeTile, p.page_size))) : 6;
     const int kg = tc / TPK, ds = tc % TPK;
     const int d0 = ds * DPT;
     const int panel = d0 / 64, chunk = (d0 % 64) / 8;
@@ -214,7 +225,7 @@ __global__ void __launch_bounds__(kDecodeCTAThreads, 1)
     for (int t = 0; t < ntiles; ++t) {
       const int slot = t % kDecodeStages;
       mbar_wait(&full[slot], (t / kDecodeStages) & 1, p.err, 12);
-      const uint8_t* sk = smem + slot * 2 * kDecodeTileBytes + panel * kDecodePanel;
+      const uint8_t* sk = smem + slot * 2 * kDecodeTileBytes;
       const uint8_t* sv = sk + kDecodeTileBytes;
 #pragma unroll 2
       for (int u = 0; u < kDecodeTile / KPS; ++u) {
@@ -222,8 +233,14 @@ __global__ void __launch_bounds__(kDecodeCTAThreads, 1)
         const bool valid = j0 + t * kDecodeTile + kr < j1;
         float kf[DPT], vf[DPT];
 #pragma unroll
+        // key kr, 16-byte chunk: panel-major tile ([panel][64 keys][128 B]), or for
+        // small pages [sub][panel][rows][128 B] with rows = 1 << rows_log2
+        const int kbase = (PG == 2)
+                              ? (((kr >> rows_log2) * 2 + panel) << (rows_log2 + 7)) + ((kr & ((1 << rows_log2) - 1)) << 7)
+                              : panel * kDecodePanel + kr * 128;
+#pragma unroll
         for (int c = 0; c < NCH; ++c) {
-          const int off = kr * 128 + (((chunk + c) ^ (kr & 7)) << 4);
+          const int off = kbase + (((chunk + c) ^ (kr & 7)) << 4);
           bf16x8_to_f32(*reinterpret_cast<const uint4*>(sk + off), &kf[8 * c]);
           bf16x8_to_f32(*reinterpret_cast<const uint4*>(sv + off), &vf[8 * c]);
         }
