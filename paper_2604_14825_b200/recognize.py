@@ -28,7 +28,7 @@ The GPU kernels' tiles are unions of consecutive MA tiles (see
 from __future__ import annotations
 
 import math
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 from typing import Optional
 
 from . import ma_ir as ir

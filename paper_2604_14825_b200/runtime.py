@@ -8,14 +8,12 @@ foreign call.  torch is used purely as the device-memory / stream provider.
 from __future__ import annotations
 
 import ctypes as C
-import math
 from typing import Optional
 
 import torch
 
 from . import _lib
-from .errors import DivisionByZero, InvalidArguments, UnsupportedMA
-from .recognize import AttentionSpec, GemmChainSpec
+from .errors import DivisionByZero, InvalidArguments
 
 
 def _stream_handle(stream) -> int:

@@ -28,10 +28,9 @@ count as tie-breaker.  Here:
 from __future__ import annotations
 
 import json
-import math
 import random
 import statistics
-from typing import Callable, Optional, Sequence
+from typing import Callable, Optional
 
 from . import cost, ma_ir
 from .errors import UnsupportedMA

@@ -1,7 +1,6 @@
 """Tuner restatement parity (CPU) and on-device scoring (GPU)."""
 
 import os
-import sys
 
 import pytest
 
