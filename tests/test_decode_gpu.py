@@ -123,3 +123,49 @@ def test_paged_decode_matches_dense_kernel_bitwise_when_splits_match():
                     0.088, max_seq_kv=M, num_splits=6).launch()
     torch.cuda.synchronize()
     assert torch.equal(o1, o2)
+
+
+@pytest.mark.parametrize("Hq,Hkv,Nq,page_size", [(8, 8, 1, 32), (16, 2, 1, 16), (4, 4, 2, 128), (8, 4, 1, 8)])
+def test_paged_decode_row_packings(Hq, Hkv, Nq, page_size):
+    """R = (Hq/Hkv)*Nq rows per kv group of 1, 8, 2, 2 over paged caches of several page sizes."""
+    from paper_2604_14825_b200.runtime import PagedDecodePlan
+
+    B, M, D = 3, 1300, 128
+    g = np.random.default_rng(Hq * 100 + page_size)
+    q = round_bf16(g.standard_normal((B, Hq, Nq, D)))
+    k = round_bf16(g.standard_normal((B, Hkv, M, D)))
+    v = round_bf16(g.standard_normal((B, Hkv, M, D)))
+    lens = np.array([M, 700, 65], dtype=np.int32)
+    kp, vp, bt = _paged_cache(k, v, page_size, "NHD", seed=page_size)
+    o = torch.empty((B, Hq, Nq, D), dtype=torch.float32, device="cuda")
+    plan = PagedDecodePlan(torch.from_numpy(q).cuda().bfloat16(), torch.from_numpy(kp).cuda().bfloat16(),
+                           torch.from_numpy(vp).cuda().bfloat16(), torch.from_numpy(bt).cuda(),
+                           torch.from_numpy(lens).cuda(), o, 1 / np.sqrt(D), max_seq_kv=M)
+    plan.launch()
+    torch.cuda.synchronize()
+    plan.check_errors()
+    got = o.cpu().numpy()
+    for b in range(B):
+        n = int(lens[b])
+        ref = reference_math.attention_batched_fp64(q[b:b + 1], k[b:b + 1, :, :n], v[b:b + 1, :, :n],
+                                                    1 / np.sqrt(D), False)
+        _check(got[b:b + 1], ref)
+
+
+def test_paged_decode_empty_sequence_raises():
+    """A sequence with no keys has a zero softmax denominator (tilecc/numerics.py:123-126)."""
+    from paper_2604_14825_b200.errors import DivisionByZero
+    from paper_2604_14825_b200.runtime import PagedDecodePlan
+
+    B, Hq, Hkv, M, D, ps = 2, 4, 1, 256, 128, 64
+    g = np.random.default_rng(0)
+    q = torch.from_numpy(round_bf16(g.standard_normal((B, Hq, 1, D)))).cuda().bfloat16()
+    pool = torch.from_numpy(round_bf16(g.standard_normal((8, ps, Hkv, D)))).cuda().bfloat16()
+    bt = torch.arange(8, dtype=torch.int32, device="cuda").reshape(2, 4)
+    lens = torch.tensor([256, 0], dtype=torch.int32, device="cuda")
+    o = torch.empty((B, Hq, 1, D), dtype=torch.float32, device="cuda")
+    plan = PagedDecodePlan(q, pool, pool, bt, lens, o, 0.088, max_seq_kv=M)
+    plan.launch()
+    torch.cuda.synchronize()
+    with pytest.raises(DivisionByZero):
+        plan.check_errors()
