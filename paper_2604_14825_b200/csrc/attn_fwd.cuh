@@ -426,17 +426,18 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         }
         float mx;
         {
-          // tree max with 3-input FMNMX3, 4 independent chains
+          // tree max with 3-input FMNMX3, 4 independent chains over s[0..128)
           float a0 = __uint_as_float(s[0]), a1 = __uint_as_float(s[1]);
           float a2 = __uint_as_float(s[2]), a3 = __uint_as_float(s[3]);
 #pragma unroll
-          for (int c = 4; c < 128; c += 8) {
+          for (int c = 4; c + 8 <= 128; c += 8) {
             a0 = fmax3(a0, __uint_as_float(s[c]), __uint_as_float(s[c + 1]));
             a1 = fmax3(a1, __uint_as_float(s[c + 2]), __uint_as_float(s[c + 3]));
             a2 = fmax3(a2, __uint_as_float(s[c + 4]), __uint_as_float(s[c + 5]));
-            if (c + 7 < 128) a3 = fmax3(a3, __uint_as_float(s[c + 6]), __uint_as_float(s[c + 7]));
-            else a3 = fmaxf(a3, __uint_as_float(s[c + 6]));
+            a3 = fmax3(a3, __uint_as_float(s[c + 6]), __uint_as_float(s[c + 7]));
           }
+          a0 = fmax3(a0, __uint_as_float(s[124]), __uint_as_float(s[125]));
+          a1 = fmax3(a1, __uint_as_float(s[126]), __uint_as_float(s[127]));
           mx = fmaxf(fmax3(a0, a1, a2), a3);
         }
         if (li == 0 && lane == 0 && wq == 0) NT_STAMP(1 + t, j, 3);
