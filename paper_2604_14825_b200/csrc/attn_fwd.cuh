@@ -164,6 +164,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 
   const int warp = __shfl_sync(0xffffffffu, threadIdx.x / 32, 0);
   const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) NT_STAMP(3, 63, 7);  // kernel entry (trace builds)
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmQ);

@@ -53,7 +53,8 @@ for role, name in enumerate(["mma", "softmax0", "softmax1", "producer"]):
     res[name] = rows
 os.makedirs(os.path.dirname(a.out), exist_ok=True)
 json.dump(res, open(a.out, "w"))
-for name in ("mma", "softmax0", "softmax1"):
+print("kernel entry", int(t[3, 63, 7] - base) if t[3, 63, 7] > 0 else None)
+for name in ("mma", "softmax0", "softmax1", "producer"):
     print(name)
     for i, r in enumerate(res[name][:12]):
         print(i, r)
