@@ -72,6 +72,9 @@ typedef struct nt_attn_args {
    * greedily in LPT order and the last CTA resets it, so one counter serves
    * every launch ordered on one stream.  NULL = static round-robin items. */
   int32_t* work_counter;
+  /* the MA kernel's `stages` tunable (0 = the scheduler default 2): K/V tiles
+   * kept in flight -- 1 -> one K/V pair (D=128) / two (D=64), >= 2 -> two / four */
+  int32_t kv_stages;
 } nt_attn_args;
 int nt_attn_fwd(const nt_attn_args* args, void* stream);
 

@@ -39,7 +39,8 @@ class AttnArgs(C.Structure):
                 ("seq_q", C.c_int32), ("seq_kv", C.c_int32), ("head_dim", C.c_int32),
                 ("scale", C.c_float), ("mask_kind", C.c_int32), ("causal_offset", C.c_int32),
                 ("mask", C.c_void_p), ("mask_stride_row", C.c_int64),
-                ("out_dtype", C.c_int32), ("err_flag", C.c_void_p), ("work_counter", C.c_void_p)]
+                ("out_dtype", C.c_int32), ("err_flag", C.c_void_p), ("work_counter", C.c_void_p),
+                ("kv_stages", C.c_int32)]
 
 
 class DecodeArgs(C.Structure):

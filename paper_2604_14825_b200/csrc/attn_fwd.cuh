@@ -73,13 +73,22 @@ constexpr float kRescaleLog2 = 8.0f;
 constexpr bool kPolyExp = NT_POLY_EVERY > 0;
 constexpr int kPolyEvery = NT_POLY_EVERY > 0 ? NT_POLY_EVERY : 1;
 
+// KV ring depth in 128-key K or V tiles.  The MA kernel's `stages` tunable
+// (SetParam stages, tilecc/autosched/scheduler.py:116-124) picks it: stages = 1
+// keeps one K/V tile pair (D=128) / two pairs (D=64) in flight, stages >= 2 the
+// most shared memory allows (64 KB of K/V per stage).
 template <int D>
+constexpr int attn_kv_slots(int ma_stages) {
+  return (D == 128) ? (ma_stages <= 1 ? 2 : 4) : (ma_stages <= 1 ? 4 : 8);
+}
+
+template <int D, int KVS = attn_kv_slots<D>(2)>
 struct AttnCfg {
   static constexpr int BM = 128, BN = 128;
   static constexpr int HALF = 128 * 64 * 2;  // one 128-row x 64-col bf16 swizzle-128B panel
   static constexpr int TQ = BM * D * 2;
   static constexpr int TKV = BN * D * 2;
-  static constexpr int STAGES = (D == 128) ? 4 : 8;
+  static constexpr int STAGES = KVS;
   // D = 64: O_t needs only 64 TMEM columns, so P_t gets its own 64 columns
   // next to it instead of aliasing S_t.  S_t(j+1) can then be computed as soon
   // as the softmax warps have loaded S_t(j) into registers, i.e. while they
@@ -136,11 +145,11 @@ __device__ __forceinline__ AttnItem attn_item(const AttnFwdParams& p, int w) {
   return it;
 }
 
-template <int D, int MASK, bool OUT_F32>
+template <int D, int MASK, bool OUT_F32, int KVS>
 __global__ void __launch_bounds__(kAttnThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const AttnFwdParams p) {
-  using C = AttnCfg<D>;
+  using C = AttnCfg<D, KVS>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_u32 = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_u32 + 1023u) & ~1023u) - raw_u32);

@@ -113,11 +113,11 @@ int make_map_pages_5d(CUtensorMap* m, const void* ptr, int64_t page_size, int64_
 }
 
 // ----------------------------------------------------------------- attention
-template <int D, int MASK, bool F32>
+template <int D, int MASK, bool F32, int KVS>
 static int launch_attn(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const AttnFwdParams& p,
                        cudaStream_t st) {
-  auto kern = attn_fwd_kernel<D, MASK, F32>;
-  const int smem = AttnCfg<D>::SMEM_BYTES;
+  auto kern = attn_fwd_kernel<D, MASK, F32, KVS>;
+  const int smem = AttnCfg<D, KVS>::SMEM_BYTES;
   static bool configured = false;
   if (!configured) {
     int rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
@@ -132,20 +132,29 @@ static int launch_attn(const CUtensorMap& mq, const CUtensorMap& mk, const CUten
   return check_cuda(cudaGetLastError(), "attn_fwd launch");
 }
 
+template <int D, int MASK, bool F32>
+static int launch_attn_stages(int ma_stages, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
+                              const AttnFwdParams& p, cudaStream_t st) {
+  constexpr int kShallow = attn_kv_slots<D>(1), kDeep = attn_kv_slots<D>(2);
+  return attn_kv_slots<D>(ma_stages) == kShallow ? launch_attn<D, MASK, F32, kShallow>(mq, mk, mv, p, st)
+                                                 : launch_attn<D, MASK, F32, kDeep>(mq, mk, mv, p, st);
+}
+
 template <int D>
 static int dispatch_attn(const nt_attn_args* a, const CUtensorMap& mq, const CUtensorMap& mk,
                          const CUtensorMap& mv, const AttnFwdParams& p, cudaStream_t st) {
   const bool f32 = a->out_dtype == NT_DTYPE_F32;
+  const int sg = a->kv_stages > 0 ? a->kv_stages : 2;  // the MA default (VirtualDevice.stage_default)
   switch (a->mask_kind) {
     case NT_MASK_NONE:
-      return f32 ? launch_attn<D, MASK_NONE, true>(mq, mk, mv, p, st)
-                 : launch_attn<D, MASK_NONE, false>(mq, mk, mv, p, st);
+      return f32 ? launch_attn_stages<D, MASK_NONE, true>(sg, mq, mk, mv, p, st)
+                 : launch_attn_stages<D, MASK_NONE, false>(sg, mq, mk, mv, p, st);
     case NT_MASK_CAUSAL:
-      return f32 ? launch_attn<D, MASK_CAUSAL, true>(mq, mk, mv, p, st)
-                 : launch_attn<D, MASK_CAUSAL, false>(mq, mk, mv, p, st);
+      return f32 ? launch_attn_stages<D, MASK_CAUSAL, true>(sg, mq, mk, mv, p, st)
+                 : launch_attn_stages<D, MASK_CAUSAL, false>(sg, mq, mk, mv, p, st);
     case NT_MASK_TENSOR:
-      return f32 ? launch_attn<D, MASK_TENSOR, true>(mq, mk, mv, p, st)
-                 : launch_attn<D, MASK_TENSOR, false>(mq, mk, mv, p, st);
+      return f32 ? launch_attn_stages<D, MASK_TENSOR, true>(sg, mq, mk, mv, p, st)
+                 : launch_attn_stages<D, MASK_TENSOR, false>(sg, mq, mk, mv, p, st);
   }
   return set_error(NT_ERR_INVALID, "unknown mask_kind");
 }

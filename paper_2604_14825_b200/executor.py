@@ -146,7 +146,7 @@ def _prepare_attention(spec: AttentionSpec, module: ir.Module, inputs: dict, out
         # short query block over a long KV range: K2 split-KV decode
         plan = DecodePlan(q, k, v, o, spec.scale)
     else:
-        plan = AttentionPlan(q, k, v, o, spec.scale, kind, mask_t)
+        plan = AttentionPlan(q, k, v, o, spec.scale, kind, mask_t, kv_stages=spec.stages)
     return plan, o, outer
 
 
@@ -225,7 +225,7 @@ def _attention_streamed(spec: AttentionSpec, inputs: dict, outer, mask_kind, out
             if decode_eligible(rows, spec.d, kind) and spec.m >= 1024:
                 plan = DecodePlan(qv, kv, vv, ov, spec.scale, err_flag=err)
             else:
-                plan = AttentionPlan(qv, kv, vv, ov, spec.scale, kind, err_flag=err)
+                plan = AttentionPlan(qv, kv, vv, ov, spec.scale, kind, err_flag=err, kv_stages=spec.stages)
             plan.launch(comp)
             plans.append(plan)  # keep argument structs / workspaces alive until the sync
             flops += plan.flops()
@@ -285,7 +285,7 @@ def _causal_rows_streamed(spec, q_h, k_h, v_h, o_h, q_d, k_d, v_d, o_d, out, com
         kv_done = r1
         comp.wait_stream(s_in)
         plan = AttentionPlan(q_d[:, :, r0:r1], k_d[:, :, :r1], v_d[:, :, :r1], o_d[:, :, r0:r1], spec.scale,
-                             "causal", causal_offset=r0, err_flag=err)
+                             "causal", causal_offset=r0, err_flag=err, kv_stages=spec.stages)
         plan.launch(comp)
         plans.append(plan)
         flops += plan.flops()

@@ -45,7 +45,7 @@ class AttentionPlan:
 
     def __init__(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor,
                  scale: Optional[float], mask_kind: str = "none", mask: Optional[torch.Tensor] = None,
-                 causal_offset: int = 0, err_flag: Optional[torch.Tensor] = None):
+                 causal_offset: int = 0, err_flag: Optional[torch.Tensor] = None, kv_stages: int = 0):
         q, k, v, o = _as4(q), _as4(k), _as4(v), _as4(o)
         for name, t in (("q", q), ("k", k), ("v", v)):
             if t.dtype != torch.bfloat16 or not t.is_cuda:
@@ -76,6 +76,8 @@ class AttentionPlan:
         # dynamic (greedy LPT) item counter of the persistent kernel; reset on device by the last CTA
         self.work = torch.zeros(2, dtype=torch.int32, device=q.device)
         a.work_counter = self.work.data_ptr()
+        a.kv_stages = int(kv_stages)  # the MA `stages` tunable (0 = scheduler default)
+        self.kv_slots = attn_kv_slots(D, kv_stages)
         self.args = a
         self.shape = (B, Hq, Hkv, N, M, D)
         self._fn = _lib.lib().nt_attn_fwd
@@ -101,6 +103,14 @@ class AttentionPlan:
             raise DivisionByZero("tile divide: softmax denominator is zero (row fully masked)")
         if flag >> 8:
             raise RuntimeError(f"device pipeline timeout (wait codes {[c for c in range(16) if flag >> (8 + c) & 1]})")
+
+
+def attn_kv_slots(d: int, ma_stages: int) -> int:
+    """K/V ring slots K1 uses for an MA `stages` value (csrc/attn_fwd.cuh attn_kv_slots)."""
+    st = ma_stages if ma_stages > 0 else 2
+    if d == 128:
+        return 2 if st <= 1 else 4
+    return 4 if st <= 1 else 8
 
 
 def _causal_pairs(N: int, M: int, off: int) -> int:

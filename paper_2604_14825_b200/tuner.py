@@ -53,7 +53,10 @@ def _lower(base, schedule, assignment, device):
 def realisation_key(spec, outer, mask_kind) -> tuple:
     """Fields that determine the sm_100a launch (MA tile sizes do not: the GPU tile is fixed)."""
     if isinstance(spec, AttentionSpec):
-        return ("attn", spec.n, spec.m, spec.d, spec.scale, spec.mask is not None, mask_kind, outer)
+        from .runtime import attn_kv_slots
+        # the MA tile sizes do not change the GPU tiles; `stages` picks the K/V ring depth
+        return ("attn", spec.n, spec.m, spec.d, spec.scale, spec.mask is not None, mask_kind, outer,
+                attn_kv_slots(spec.d, spec.stages))
     if isinstance(spec, GemmChainSpec):
         return ("chain", spec.n, spec.k, spec.f, spec.e)
     return (type(spec).__name__,)

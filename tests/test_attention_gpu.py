@@ -235,3 +235,27 @@ def test_persistent_multi_item_repeated_launches(B, Hq, Hkv, N, D, causal):
         q.float(), k.float().repeat_interleave(Hq // Hkv, 1), v.float().repeat_interleave(Hq // Hkv, 1),
         is_causal=causal, scale=1.0 / np.sqrt(D))
     _check(o.float().cpu().numpy(), ref.cpu().numpy())
+
+
+@pytest.mark.parametrize("D,causal", [(64, False), (128, True)])
+def test_ma_stages_pick_the_kv_ring_depth_without_changing_bits(D, causal):
+    """The MA `stages` tunable selects the K/V ring depth (one vs two/four tile pairs in flight);
+    the arithmetic and its order are the same, so the outputs are bit-identical."""
+    from paper_2604_14825_b200.runtime import AttentionPlan, attn_kv_slots
+
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(D)
+    B, Hq, Hkv, N = 2, 8, 2, 1280
+    q = torch.randn((B, Hq, N, D), generator=g, device=dev).bfloat16()
+    k = torch.randn((B, Hkv, N, D), generator=g, device=dev).bfloat16()
+    v = torch.randn((B, Hkv, N, D), generator=g, device=dev).bfloat16()
+    outs = []
+    for st in (1, 2, 4):
+        o = torch.empty((B, Hq, N, D), dtype=torch.float32, device=dev)
+        plan = AttentionPlan(q, k, v, o, D ** -0.5, "causal" if causal else "none", kv_stages=st)
+        plan.launch()
+        torch.cuda.synchronize()
+        plan.check_errors()
+        outs.append(o)
+    assert attn_kv_slots(D, 1) < attn_kv_slots(D, 2) == attn_kv_slots(D, 4)
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2])
