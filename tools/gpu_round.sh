@@ -16,6 +16,6 @@ cap attn_llama8k attn_fwd 3 llama8k_causal
 cap attn_bert512 attn_fwd 3 bert512
 cap decode32k decode_split 3 decode32k
 cap decode32k_paged16 decode_split 3 decode32k_paged16
-cap gemm4k gemm_kernel 6 gemm_chain_e4096
+cap gemm4k gemm2_kernel 6 gemm_chain_e4096
 cap chain_e128 chain_kernel 3 gemm_chain_e128
 ls -la gpurun_out/round | head -40
