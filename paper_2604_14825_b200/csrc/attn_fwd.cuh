@@ -109,6 +109,7 @@ __device__ __forceinline__ float f_ninf() { return __int_as_float(0xff800000); }
 // 1/2 softmax tile 0/1, 3 producer.
 __device__ unsigned long long* g_nt_trace = nullptr;
 __device__ int g_nt_trace_cta = 0;
+__device__ unsigned long long* g_nt_cta_times = nullptr;  // [cta][entry, exit, items] (globaltimer ns)
 #define NT_STAMP(role, iter, ev)                                                               \
   do {                                                                                         \
     if (g_nt_trace && blockIdx.x == g_nt_trace_cta && (iter) < 64)                             \
@@ -174,6 +175,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   const int warp = __shfl_sync(0xffffffffu, threadIdx.x / 32, 0);
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) NT_STAMP(3, 63, 7);  // kernel entry (trace builds)
+#ifdef NT_TRACE
+  if (threadIdx.x == 0 && g_nt_cta_times) g_nt_cta_times[blockIdx.x * 3] = globaltimer();
+#endif
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmQ);
@@ -400,6 +404,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       const AttnItem itm = attn_item<MASK>(p, w);
       const int qi = itm.q_row0 + t * 128 + r;
       float m_run = NINF, l_run = 0.f;
+      if (t == 0 && wq == 0 && lane == 0 && li < 16) NT_STAMP(3, 32 + li, 6);  // item start (trace)
 
       for (int j = 0; j < itm.n_kv; ++j) {
         if (li == 0 && lane == 0 && wq == 0) NT_STAMP(1 + t, j, 0);
@@ -541,6 +546,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       // O_t is read out: the next item's first PV_t (issued after this warp's
       // next p_full arrival) may overwrite it
       tc_fence_before();
+      if (t == 0 && wq == 0 && lane == 0 && li < 16) NT_STAMP(3, 32 + li, 7);  // item end (trace)
     }
   }
 
@@ -551,6 +557,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
+#ifdef NT_TRACE
+  if (threadIdx.x == 0 && g_nt_cta_times) g_nt_cta_times[blockIdx.x * 3 + 1] = globaltimer();
+#endif
   if (threadIdx.x == 0 && p.work) {
     // every CTA has drawn its terminal item before arriving here: the last one
     // resets the counter for the next launch on this stream

@@ -265,6 +265,10 @@ extern "C" int nt_debug_set_trace(unsigned long long* buf, int cta) {
   cudaMemcpyToSymbol(nt::g_nt_trace_cta, &cta, sizeof(cta));
   return check_cuda(cudaGetLastError(), "nt_debug_set_trace");
 }
+extern "C" int nt_debug_set_cta_times(unsigned long long* buf) {
+  cudaMemcpyToSymbol(nt::g_nt_cta_times, &buf, sizeof(buf));
+  return check_cuda(cudaGetLastError(), "nt_debug_set_cta_times");
+}
 #endif
 
 extern "C" int nt_memcpy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width,

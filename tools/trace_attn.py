@@ -54,6 +54,8 @@ for role, name in enumerate(["mma", "softmax0", "softmax1", "producer"]):
 os.makedirs(os.path.dirname(a.out), exist_ok=True)
 json.dump(res, open(a.out, "w"))
 print("kernel entry", int(t[3, 63, 7] - base) if t[3, 63, 7] > 0 else None)
+print("items (start, end) of tile 0:", [(int(t[3, 32 + i, 6] - base), int(t[3, 32 + i, 7] - base))
+                                       for i in range(16) if t[3, 32 + i, 6] > 0])
 for name in ("mma", "softmax0", "softmax1", "producer"):
     print(name)
     for i, r in enumerate(res[name][:12]):
