@@ -307,6 +307,19 @@ def _causal_rows_streamed(spec, q_h, k_h, v_h, o_h, q_d, k_d, v_d, o_d, out, com
     return out, ev0.elapsed_time(ev1), flops, info
 
 
+def tcgen05_unsupported(spec) -> Optional[str]:
+    """Why a recognised family member has no tensor-core realisation (None if it has one)."""
+    if isinstance(spec, AttentionSpec):
+        if spec.d != spec.dv or spec.d not in (64, 128):
+            return f"attention head dim {spec.d}/{spec.dv}: the K1/K2 kernels are built for 64 and 128"
+        if spec.scale is not None and not spec.scale > 0:
+            return "non-positive score scale"
+    elif isinstance(spec, GemmChainSpec):
+        if spec.k % 8 or spec.f % 8 or spec.e % 8:
+            return "GEMM chain K, F, E must be multiples of 8 (16-byte TMA rows)"
+    return None
+
+
 _SPEC_CACHE: dict = {}
 _COST_CACHE: dict = {}
 
@@ -389,6 +402,9 @@ def execute_ma(module, inputs: dict, device=None, precision=None, *, outer=None,
         raise UnsupportedMA(f"precision {eff!r}: the tcgen05 families compute in bf16 / fp32")
     try:
         specs = _recognize_cached(module, mod)
+        why = [r for r in (tcgen05_unsupported(sp) for sp in specs) if r]
+        if why:
+            raise UnsupportedMA("; ".join(why))
     except UnsupportedMA:
         if backend == "auto" and outer is None:
             return _execute_simt(module, mod, inputs, prec, stream, return_torch)

@@ -227,3 +227,23 @@ def test_simt_runs_the_baseline_families_exactly(case):
     got = np.asarray(bufs[mod.output])
     np.testing.assert_allclose(got, interp32, rtol=FP32_RTOL, atol=FP32_ATOL)
     assert float(np.max(np.abs(got - oracle64))) < 1e-4
+
+
+def test_unrealisable_family_members_are_reported():
+    """An attention MA with head dim 32 is recognised but has no tcgen05 kernel (auto -> SIMT)."""
+    from paper_2604_14825_b200.executor import tcgen05_unsupported
+    from paper_2604_14825_b200.recognize import recognize
+
+    case = [c for c in CASES if c["name"] == "attention64"][0]
+    specs = recognize(_module(case))
+    assert "head dim 32" in tcgen05_unsupported(specs[0])
+
+
+@pytest.mark.gpu
+def test_auto_backend_falls_back_to_simt_for_unsupported_head_dim():
+    from paper_2604_14825_b200 import execute_ma
+
+    case = [c for c in CASES if c["name"] == "attention64"][0]
+    bufs, rep = execute_ma(_module(case), _inputs(case))
+    assert rep.realisation[0]["kernel"] == "simt"
+    np.testing.assert_allclose(bufs[case["output"]], ARR[f"{case['case']}_ref32"], rtol=FP32_RTOL, atol=FP32_ATOL)
