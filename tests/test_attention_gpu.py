@@ -259,3 +259,55 @@ def test_ma_stages_pick_the_kv_ring_depth_without_changing_bits(D, causal):
         outs.append(o)
     assert attn_kv_slots(D, 1) < attn_kv_slots(D, 2) == attn_kv_slots(D, 4)
     assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2])
+
+
+def test_full_size_llama8k_properties():
+    """BASELINE config 4 at full size (B=1, Hq=32, Hkv=8, 8K, causal) through size-independent
+    properties: V = 1 gives O = 1 (the output is a convex combination of V rows); the first
+    query row sees only key 0, so O[0] = V[0] exactly; O is linear in V."""
+    from paper_2604_14825_b200.runtime import AttentionPlan
+
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(8)
+    B, Hq, Hkv, N, D = 1, 32, 8, 8192, 128
+    q = torch.randn((B, Hq, N, D), generator=g, device=dev).bfloat16()
+    k = torch.randn((B, Hkv, N, D), generator=g, device=dev).bfloat16()
+    scale = 0.08838834764831845
+
+    def run(v):
+        o = torch.empty((B, Hq, N, D), dtype=torch.float32, device=dev)
+        plan = AttentionPlan(q, k, v, o, scale, "causal")
+        plan.launch()
+        torch.cuda.synchronize()
+        plan.check_errors()
+        return o
+
+    ones = torch.ones((B, Hkv, N, D), device=dev).bfloat16()
+    o1 = run(ones)
+    assert float((o1 - 1).abs().max()) < 1e-2  # P rounded to bf16 before P.V, l from fp32 P
+    v1 = torch.randn((B, Hkv, N, D), generator=g, device=dev).bfloat16()
+    v2 = torch.randn((B, Hkv, N, D), generator=g, device=dev).bfloat16()
+    oa, ob = run(v1), run(v2)
+    assert torch.equal(oa[:, :, 0], v1.float().repeat_interleave(Hq // Hkv, 1)[:, :, 0])
+    vs = (v1.float() + v2.float()).bfloat16()  # exact in bf16 only up to rounding: compare loosely
+    osum = run(vs)
+    assert float((osum - (oa + ob)).abs().max()) < 3e-2
+    assert float((osum - (oa + ob)).norm() / (oa + ob).norm()) < 1e-2
+
+
+def test_full_size_decode_properties():
+    """BASELINE config 5 at full size (B=64, Hq=32, Hkv=8, KV 32K): V = 1 gives O = 1."""
+    from paper_2604_14825_b200.runtime import DecodePlan
+
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(5)
+    B, Hq, Hkv, M, D = 64, 32, 8, 32768, 128
+    q = torch.randn((B, Hkv, Hq // Hkv, D), generator=g, device=dev).bfloat16()
+    k = torch.randn((B, Hkv, M, D), generator=g, device=dev).bfloat16()
+    v = torch.ones((B, Hkv, M, D), device=dev).bfloat16()
+    o = torch.empty((B, Hkv, Hq // Hkv, D), dtype=torch.float32, device=dev)
+    plan = DecodePlan(q, k, v, o, 0.08838834764831845)
+    plan.launch()
+    torch.cuda.synchronize()
+    plan.check_errors()
+    assert float((o - 1).abs().max()) < 1e-5  # fp32 P on the FMA pipe: O = sum(P)/sum(P)
