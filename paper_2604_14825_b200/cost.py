@@ -166,3 +166,69 @@ def b200_viable(spec) -> list[str]:
             if v % 8:
                 out.append(f"{nm}={v} must be a multiple of 8 (16-byte TMA rows)")
     return out
+
+
+def access_audit(module) -> tuple[int, dict]:
+    """``unique_global_bytes`` and ``read_audit`` of interpret_ma's CostReport, without executing.
+
+    Restates the access accounting of tilecc/ma/interp.py:128-141 and 160-171:
+    every Global slice a kernel reads or writes is stamped into a per-kernel
+    counter of the buffer's shape (unique bytes = touched elements x item
+    size, summed over kernels), and the Global slices each block point reads
+    are counted per block (``reads``, ``unique``, ``blocks``, ``single_pass``).
+    Like the reference it allocates full-buffer counters, so it is computed
+    only when asked for (``ExecReport.read_audit``).
+    """
+    import itertools
+
+    import numpy as np
+
+    module = ir.as_module(module)
+    item = ITEM_BYTES[module.precision]
+    shape = {b.name: tuple(b.shape) for b in module.buffers if b.scope == "Global"}
+    unique = 0
+    audit: dict = {}
+
+    def accesses(body, loops=()):
+        for st in body:
+            if isinstance(st, ir.Loop):
+                yield from accesses(st.body, loops + ((st.var, st.extent),))
+            elif isinstance(st, ir.Copy):
+                yield st.src, st.src_slices, loops, True
+                yield st.dst, st.dst_slices, loops, False
+            else:
+                for n in st.expr.walk():
+                    if isinstance(n, ir.Ref):
+                        yield n.buffer, n.slices, loops, True
+                yield st.dst, st.dst_slices, loops, False
+
+    for k in module.kernels:
+        acc = [a for a in accesses(k.body) if a[0] in shape]
+        touched: dict = {}
+        names = [v for v, _, _ in k.blocks]
+        for point in itertools.product(*[range(e) for _, _, e in k.blocks]):
+            benv = dict(zip(names, point))
+            reads: dict = {}
+            for buf, slices, loops, is_read in acc:
+                lnames = [v for v, _ in loops]
+                for lp in itertools.product(*[range(e) for _, e in loops]):
+                    env = dict(benv, **dict(zip(lnames, lp)))
+                    idx = tuple(slice(s.off.evaluate(env), s.off.evaluate(env) + s.length) for s in slices)
+                    if buf not in touched:
+                        touched[buf] = np.zeros(shape[buf], dtype=np.int32)
+                    touched[buf][idx] += 1
+                    if is_read:
+                        if buf not in reads:
+                            reads[buf] = np.zeros(shape[buf], dtype=np.int32)
+                        reads[buf][idx] += 1
+            for buf, counts in reads.items():
+                a = audit.setdefault(buf, {"reads": 0, "unique": 0, "blocks": 0, "single_pass": True})
+                total, uniq = int(counts.sum()), int((counts > 0).sum())
+                a["reads"] += total
+                a["unique"] += uniq
+                a["blocks"] += 1
+                if total != uniq:
+                    a["single_pass"] = False
+        for mask in touched.values():
+            unique += int((mask > 0).sum()) * item
+    return unique, {b: audit[b] for b in sorted(audit)}

@@ -60,6 +60,38 @@ class ExecReport:
     launches: int = 0
     specs: list = field(default_factory=list)
     realisation: list = field(default_factory=list)
+    module: Optional[object] = field(default=None, repr=False)
+    _audit: Optional[tuple] = field(default=None, repr=False)
+
+    # interpret_ma's dynamic access counters (tilecc/ma/interp.py:128-141, 160-171),
+    # derived from the MA program on first use (cost.access_audit)
+    def _access(self):
+        if self._audit is None:
+            self._audit = cost.access_audit(self.module) if self.module is not None else (0, {})
+        return self._audit
+
+    @property
+    def unique_global_bytes(self) -> int:
+        return self._access()[0]
+
+    @property
+    def read_audit(self) -> dict:
+        return self._access()[1]
+
+    def to_json(self) -> str:
+        """CostReport.to_json layout (tilecc/ma/interp.py:72-83) plus the device time."""
+        import json
+        data = {
+            "bytes": {"Global": self.bytes_global, "Shared": self.bytes_shared, "Register": self.bytes_register},
+            "unique_global_bytes": self.unique_global_bytes,
+            "flops": self.flops,
+            "kernels": self.kernels,
+            "steps": self.steps,
+            "modeled_cost": round(self.modeled_cost, 6),
+            "read_audit": self.read_audit,
+            "device_ms": self.device_ms,
+        }
+        return json.dumps(data, indent=2, sort_keys=False) + "\n"
 
 
 def _to_device(x, dev, name) -> torch.Tensor:
@@ -351,7 +383,7 @@ def _execute_simt(module, mod, inputs, prec, stream, return_torch):
     """Generic MA program on the SIMT lowering (simt.py): interpret_ma semantics in the MA precision."""
     from . import simt
 
-    report = ExecReport(kernels=len(mod.kernels))
+    report = ExecReport(kernels=len(mod.kernels), module=mod)
     static = _static_cached(module, mod)
     for f in ("bytes_global", "bytes_shared", "bytes_register", "flops", "steps", "modeled_cost"):
         setattr(report, f, getattr(static, f))
@@ -410,7 +442,7 @@ def execute_ma(module, inputs: dict, device=None, precision=None, *, outer=None,
             return _execute_simt(module, mod, inputs, prec, stream, return_torch)
         raise
     dev = torch.device("cuda", torch.cuda.current_device())
-    report = ExecReport(kernels=len(mod.kernels))
+    report = ExecReport(kernels=len(mod.kernels), module=mod)
     static = _static_cached(module, mod)
     for f in ("bytes_global", "bytes_shared", "bytes_register", "flops", "steps", "modeled_cost"):
         setattr(report, f, getattr(static, f))

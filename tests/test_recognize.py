@@ -122,3 +122,19 @@ def test_precision_without_device_realisation_raises():
     d["precision"] = "fp64"
     with pytest.raises(UnsupportedMA):
         recognize(ma_ir.from_dict(d))
+
+
+@pytest.mark.parametrize("case", [c for c in __import__("conftest").io_cases()])
+def test_access_audit_equals_reference_cost_report(case):
+    """unique_global_bytes and read_audit of interpret_ma's CostReport, derived statically."""
+    import json
+
+    from conftest import golden_stem, load_golden
+    from paper_2604_14825_b200 import cost
+
+    mod, _, _, _ = load_golden(case)
+    with open(golden_stem(case) + ".interp_cost.json") as f:
+        ref = json.load(f)
+    unique, audit = cost.access_audit(mod)
+    assert unique == ref["unique_global_bytes"]
+    assert audit == ref["read_audit"]
