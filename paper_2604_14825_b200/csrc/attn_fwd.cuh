@@ -103,6 +103,47 @@ struct AttnCfg {
 
 __device__ __forceinline__ float f_ninf() { return __int_as_float(0xff800000); }
 
+// O_t *= alpha in TMEM (one row per thread).
+template <int D>
+__device__ __forceinline__ void attn_rescale_o(uint32_t tO, float alpha) {
+#pragma unroll
+  for (int c = 0; c < D / 16; ++c) {
+    uint32_t o[16];
+    tmem_ld16(tO + c * 16, o);
+    tmem_wait_ld();
+#pragma unroll
+    for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+    tmem_st16(tO + c * 16, o);
+  }
+}
+
+// P = exp2(S*sc - m) for one 128-key row -> bf16 pairs in TMEM at tP; returns
+// the row sum of P (fp32).
+__device__ __forceinline__ float attn_exp_pass(const uint32_t (&s)[128], float sc, float m, uint32_t tP) {
+  const float2 sc2 = make_float2(sc, sc);
+  const float2 nm2 = make_float2(-m, -m);
+  float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+  for (int ch = 0; ch < 4; ++ch) {
+    uint32_t pk[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const float s0 = __uint_as_float(s[ch * 32 + 2 * i]), s1 = __uint_as_float(s[ch * 32 + 2 * i + 1]);
+      const float2 x = ffma2(make_float2(s0, s1), sc2, nm2);
+      float2 e;
+      if (kPolyExp && (i % kPolyEvery) == kPolyEvery - 1) {
+        e = ex2_poly2(x);  // FMA-pipe exp2 for 1/kPolyEvery of the pairs
+      } else {
+        e = make_float2(ex2(x.x), ex2(x.y));
+      }
+      sum2[i & 1] = fadd2(sum2[i & 1], e);
+      pk[i] = pack_bf16(e.x, e.y);
+    }
+    tmem_st16(tP + ch * 16, pk);
+  }
+  return (sum2[0].x + sum2[0].y) + (sum2[1].x + sum2[1].y);
+}
+
 #ifdef NT_TRACE
 // Debug timeline (NT_TRACE builds only): clock64 stamps of one CTA's pipeline
 // for its first work item.  trace[(role * 64 + iter) * 8 + event]; role 0 MMA,
@@ -466,43 +507,12 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         const bool need = m_new > m_run + kRescaleLog2;
         if (__any_sync(0xffffffffu, need)) {
           const float alpha = (m_new == NINF) ? 1.0f : ex2(m_run - m_new);
-          if (j > 0) {
-#pragma unroll
-            for (int c = 0; c < D / 16; ++c) {
-              uint32_t o[16];
-              tmem_ld16(tO + c * 16, o);
-              tmem_wait_ld();
-#pragma unroll
-              for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-              tmem_st16(tO + c * 16, o);
-            }
-          }
+          if (j > 0) attn_rescale_o<D>(tO, alpha);
           l_run *= alpha;
           m_run = m_new;
         }
         const float m_use = (m_run == NINF) ? 0.f : m_run;
-        const float2 sc2 = make_float2(sc, sc);
-        const float2 nm2 = make_float2(-m_use, -m_use);
-        float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-#pragma unroll
-        for (int ch = 0; ch < 4; ++ch) {
-          uint32_t pk[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float2 x = ffma2(make_float2(__uint_as_float(s[ch * 32 + 2 * i]),
-                                               __uint_as_float(s[ch * 32 + 2 * i + 1])), sc2, nm2);
-            float2 e;
-            if (kPolyExp && (i % kPolyEvery) == kPolyEvery - 1) {
-              e = ex2_poly2(x);  // FMA-pipe exp2 for 1/kPolyEvery of the pairs
-            } else {
-              e = make_float2(ex2(x.x), ex2(x.y));
-            }
-            sum2[i & 1] = fadd2(sum2[i & 1], e);
-            pk[i] = pack_bf16(e.x, e.y);
-          }
-          tmem_st16(tP + ch * 16, pk);
-        }
-        const float sum = (sum2[0].x + sum2[0].y) + (sum2[1].x + sum2[1].y);
+        const float sum = attn_exp_pass(s, sc, m_use, tP);
         if (li == 0 && lane == 0 && wq == 0) NT_STAMP(1 + t, j, 4);
         l_run += sum;
         tmem_wait_st();

@@ -173,6 +173,52 @@ def test_exp2_poly_no_nan_on_masked_tiles():
     _check(got, ref)
 
 
+@pytest.mark.parametrize("D", [64, 128])
+@pytest.mark.parametrize("causal", [False, True])
+def test_running_max_jumps_between_kv_tiles(D, causal):
+    """Row maxima that jump between 128-key tiles by < 8, 8..32 and > 32 log2 units.
+
+    Exercises the speculative max (exps against the previous tile's max, the
+    max moved one tile later) and its exact redo when a tile jumps too far.
+    """
+    N = M = 896
+    g = np.random.default_rng(41)
+    w = g.standard_normal(D)
+    w = w / np.linalg.norm(w) * np.sqrt(D)
+    scale = 1.0 / np.sqrt(D)
+    # per-tile key magnitude: log2-unit maxima ~ 1.44*sqrt(D)*c (c in units of |w|^2*scale)
+    c_tiles = [0.0, 0.5, 1.2, 1.25, 4.0, 4.1, 9.0][: M // 128]
+    c = np.repeat(np.array(c_tiles) / np.sqrt(D) * 16.0 / 1.4427, 128)[:M]
+    q = round_bf16((w[None, :] + 0.3 * g.standard_normal((N, D)))[None, None])
+    k = round_bf16((w[None, :] * c[:, None] + 0.3 * g.standard_normal((M, D)))[None, None])
+    v = round_bf16(g.standard_normal((1, 1, M, D)))
+    got = _run_batched(q, k, v, scale, causal)
+    ref = reference_math.attention_batched_fp64(q, k, v, scale, causal)
+    _check(got, ref)
+    # reversed order: the max is reached in the first tile, later tiles are tiny
+    k2, v2 = k[:, :, ::-1].copy(), v[:, :, ::-1].copy()
+    got = _run_batched(q, k2, v2, scale, causal)
+    ref = reference_math.attention_batched_fp64(q, k2, v2, scale, causal)
+    _check(got, ref)
+
+
+def test_running_max_from_fully_masked_first_tile():
+    """Rows whose first tile is fully masked, then large logits (base-0 speculative pass)."""
+    N, M, D = 256, 512, 128
+    g = np.random.default_rng(43)
+    q = _rand((1, 1, N, D), 44, 2.5)
+    k = _rand((1, 1, M, D), 45, 2.5)
+    v = _rand((1, 1, M, D), 46)
+    mask = np.zeros((N, M), np.float32)
+    mask[: N // 2, :128] = -np.inf          # half the rows see nothing in tile 0
+    mask[N // 2:, 128:256] = -np.inf        # the rest lose tile 1
+    mask[g.random((N, M)) < 0.1] = -np.inf
+    mask[:, 300] = 0.0
+    got = _run_batched(q, k, v, 0.0883883, False, mask=mask, mask_kind="tensor")
+    ref = reference_math.attention_fp64(q[0, 0], k[0, 0], v[0, 0], 0.0883883, mask)
+    _check(got[0, 0], ref)
+
+
 @pytest.mark.parametrize("case,outer,dtype", [("causal512", (2, 8, 2), torch.bfloat16),
                                               ("causal512", (1, 8, 2), torch.bfloat16),
                                               ("bert512", (3, 4, 4), torch.float32),
