@@ -71,6 +71,11 @@ constexpr float kRescaleLog2 = 8.0f;
 #define NT_POLY_EVERY 0
 #endif
 constexpr bool kPolyExp = NT_POLY_EVERY > 0;
+// P -> bf16 pack: 0 = cvt.rn.bf16x2.f32 (F2FP, on the XU pipe beside MUFU.EX2),
+// 1 = integer add + byte permute (ALU pipe).
+#ifndef NT_PACK_ALU
+#define NT_PACK_ALU 0
+#endif
 constexpr int kPolyEvery = NT_POLY_EVERY > 0 ? NT_POLY_EVERY : 1;
 
 // KV ring depth in 128-key K or V tiles.  The MA kernel's `stages` tunable
@@ -82,7 +87,7 @@ constexpr int attn_kv_slots(int ma_stages) {
   return (D == 128) ? (ma_stages <= 1 ? 2 : 4) : (ma_stages <= 1 ? 4 : 8);
 }
 
-template <int D, int KVS = attn_kv_slots<D>(2)>
+template <int D, int KVS = attn_kv_slots<D>(2), bool OUT_F32 = false>
 struct AttnCfg {
   static constexpr int BM = 128, BN = 128;
   static constexpr int HALF = 128 * 64 * 2;  // one 128-row x 64-col bf16 swizzle-128B panel
@@ -94,10 +99,18 @@ struct AttnCfg {
   // as the softmax warps have loaded S_t(j) into registers, i.e. while they
   // compute P_t(j), and the tile's GEMMs leave the softmax critical path.
   static constexpr bool SEP_P = (D == 64);
+  // D = 64: Q is double-buffered across work items (the next item's Q lands
+  // while the current one runs); D = 128 has no shared memory left for it
+  static constexpr int QB = (D == 64) ? 2 : 1;
   static constexpr int SMEM_Q = 0;
-  static constexpr int SMEM_KV = 2 * TQ;
-  static constexpr int SMEM_BAR = SMEM_KV + STAGES * TKV;
-  static constexpr int NBAR = 2 + 2 + 2 * STAGES + 2 + 2 + 2 + 2 + 2 + 2 * kItemRing;
+  static constexpr int SMEM_KV = 2 * QB * TQ;
+  // epilogue staging: per softmax warp one 32-row x 32-column O box (TMA store),
+  // 64B-swizzled (bf16) / 128B-swizzled (fp32) so the row-per-thread writes are
+  // bank-conflict free
+  static constexpr int OBOX = 32 * 32 * (OUT_F32 ? 4 : 2);
+  static constexpr int SMEM_O = SMEM_KV + STAGES * TKV;
+  static constexpr int SMEM_BAR = SMEM_O + 8 * OBOX;
+  static constexpr int NBAR = 4 * QB + 2 * STAGES + 2 + 2 + 2 + 2 + 2 + 2 * kItemRing;
   static constexpr int SMEM_BYTES = SMEM_BAR + NBAR * 8 + 16 + 4 * kItemRing + 1024;  // + alignment slack
 };
 
@@ -137,7 +150,7 @@ __device__ __forceinline__ float attn_exp_pass(const uint32_t (&s)[128], float s
         e = make_float2(ex2(x.x), ex2(x.y));
       }
       sum2[i & 1] = fadd2(sum2[i & 1], e);
-      pk[i] = pack_bf16(e.x, e.y);
+      pk[i] = NT_PACK_ALU ? pack_bf16_alu(e.x, e.y) : pack_bf16(e.x, e.y);
     }
     tmem_st16(tP + ch * 16, pk);
   }
@@ -150,14 +163,22 @@ __device__ __forceinline__ float attn_exp_pass(const uint32_t (&s)[128], float s
 // 1/2 softmax tile 0/1, 3 producer.
 __device__ unsigned long long* g_nt_trace = nullptr;
 __device__ int g_nt_trace_cta = 0;
+__device__ int g_nt_trace_li = 0;  // which of the CTA's work items the per-step stamps record
 __device__ unsigned long long* g_nt_cta_times = nullptr;  // [cta][entry, exit, items] (globaltimer ns)
+// The trace controls are read once into registers (nt_tr / nt_tr_li, see
+// NT_TRACE_INIT) so a stamp costs a clock read and a store, not a global load.
+#define NT_TRACE_INIT                                                                          \
+  unsigned long long* const nt_tr = (g_nt_trace && blockIdx.x == g_nt_trace_cta) ? g_nt_trace : nullptr; \
+  const int nt_tr_li = g_nt_trace_li
+#define NT_TRACE_LI nt_tr_li
 #define NT_STAMP(role, iter, ev)                                                               \
   do {                                                                                         \
-    if (g_nt_trace && blockIdx.x == g_nt_trace_cta && (iter) < 64)                             \
-      g_nt_trace[((role) * 64 + (iter)) * 8 + (ev)] = clock64();                               \
+    if (nt_tr && (iter) < 64) nt_tr[((role) * 64 + (iter)) * 8 + (ev)] = clock64();             \
   } while (0)
 #else
 #define NT_STAMP(role, iter, ev) do {} while (0)
+#define NT_TRACE_LI 0
+#define NT_TRACE_INIT do {} while (0)
 #endif
 
 // Work item -> coordinates.  Items are ordered heaviest first for causal masks
@@ -190,8 +211,10 @@ __device__ __forceinline__ AttnItem attn_item(const AttnFwdParams& p, int w) {
 template <int D, int MASK, bool OUT_F32, int KVS>
 __global__ void __launch_bounds__(kAttnThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                    const __grid_constant__ CUtensorMap tmV, const AttnFwdParams p) {
-  using C = AttnCfg<D, KVS>;
+                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
+                    const AttnFwdParams p) {
+  using C = AttnCfg<D, KVS, OUT_F32>;
+  static_assert(C::SMEM_BYTES <= 227 * 1024, "K1 shared memory exceeds the 227 KB opt-in limit");
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_u32 = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_u32 + 1023u) & ~1023u) - raw_u32);
@@ -199,11 +222,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   uint8_t* sQ = smem + C::SMEM_Q;
   uint8_t* sKV = smem + C::SMEM_KV;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::SMEM_BAR);
-  uint64_t* bar_q = bars;                            // [2] Q_t landed
-  uint64_t* bar_q_empty = bars + 2;                  // [2] last S_t of the item done (Q_t reusable)
-  uint64_t* bar_kv_full = bars + 4;                  // [STAGES]
-  uint64_t* bar_kv_empty = bars + 4 + C::STAGES;     // [STAGES]
-  uint64_t* bar_s_full = bars + 4 + 2 * C::STAGES;   // [2]
+  uint64_t* bar_q = bars;                            // [QB][2] Q_t landed
+  uint64_t* bar_q_empty = bars + 2 * C::QB;          // [QB][2] last S_t of the item done (Q_t reusable)
+  uint64_t* bar_kv_full = bars + 4 * C::QB;          // [STAGES]
+  uint64_t* bar_kv_empty = bar_kv_full + C::STAGES;  // [STAGES]
+  uint64_t* bar_s_full = bar_kv_empty + C::STAGES;   // [2]
   uint64_t* bar_p_full = bar_s_full + 2;             // [2]
   uint64_t* bar_o_full = bar_p_full + 2;             // [2]
   uint64_t* bar_s_free = bar_o_full + 2;             // [2] SEP_P: S_t loaded into registers (4 warps)
@@ -215,6 +238,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 
   const int warp = __shfl_sync(0xffffffffu, threadIdx.x / 32, 0);
   const int lane = threadIdx.x & 31;
+  NT_TRACE_INIT;
   if (threadIdx.x == 0) NT_STAMP(3, 63, 7);  // kernel entry (trace builds)
 #ifdef NT_TRACE
   if (threadIdx.x == 0 && g_nt_cta_times) g_nt_cta_times[blockIdx.x * 3] = globaltimer();
@@ -224,14 +248,17 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     prefetch_tmap(&tmQ);
     prefetch_tmap(&tmK);
     prefetch_tmap(&tmV);
+    prefetch_tmap(&tmO);
     for (int t = 0; t < 2; ++t) {
-      mbar_init(&bar_q[t], 1);
-      mbar_init(&bar_q_empty[t], 1);
       mbar_init(&bar_s_full[t], 1);
       mbar_init(&bar_p_full[t], 4);
       mbar_init(&bar_o_full[t], 1);
       mbar_init(&bar_s_free[t], 4);
       mbar_init(&bar_pv_done[t], 1);
+    }
+    for (int q = 0; q < 2 * C::QB; ++q) {
+      mbar_init(&bar_q[q], 1);
+      mbar_init(&bar_q_empty[q], 1);
     }
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&bar_kv_full[s], 1);
@@ -251,8 +278,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 
   if (warp < 4) {
     // setmaxnreg only redistributes the launch allocation (384 x 168 = 64512
-    // registers): 128 x 72 + 256 x 216 = 64512
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
+    // registers): 128 x 104 + 256 x 200 = 64512
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 104;");
     if (warp == 0) {
       // ================= TMA producer
       if (lane == 0) {
@@ -260,6 +287,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         for (int li = 0;; ++li) {
           // ---- schedule: first item static, then greedy (LPT order) from the global counter
           const int slot_i = li % kItemRing;
+          if (li < 15) NT_STAMP(3, 48 + li, 0);  // trace: producer reaches item li
           if (li >= kItemRing) mbar_wait(&bar_item_empty[slot_i], ((li / kItemRing) - 1) & 1, p.err, 12);
           int w;
           if (li == 0) w = blockIdx.x;
@@ -267,23 +295,30 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           else w = blockIdx.x + li * gridDim.x;
           item_ring[slot_i] = w;
           mbar_arrive(&bar_item_full[slot_i]);
+          if (li < 15) NT_STAMP(3, 48 + li, 1);  // trace: item li published
           if (w >= p.n_items) break;
           const AttnItem itm = attn_item<MASK>(p, w);
-          for (int t = 0; t < 2; ++t) {
-            if (li > 0) mbar_wait(&bar_q_empty[t], (li - 1) & 1, p.err, 11);
-            mbar_arrive_expect_tx(&bar_q[t], C::TQ);
+          // Q_t of this item may only land once the previous item's last S_t is
+          // done; K(0) goes first, into the ring, so it is resident when Q is
+          auto load_q = [&]() {
+            const int qb = (li % C::QB) * 2;
+            for (int t = 0; t < 2; ++t) {
+              if (li >= C::QB) mbar_wait(&bar_q_empty[qb + t], ((li / C::QB) - 1) & 1, p.err, 11);
+              mbar_arrive_expect_tx(&bar_q[qb + t], C::TQ);
 #pragma unroll
-            for (int h = 0; h < D / 64; ++h)
-              tma_load_4d(sQ + t * C::TQ + h * C::HALF, &tmQ, &bar_q[t], h * 64, itm.q_row0 + t * 128, itm.hq,
-                          itm.b);
-          }
+              for (int h = 0; h < D / 64; ++h)
+                tma_load_4d(sQ + (qb + t) * C::TQ + h * C::HALF, &tmQ, &bar_q[qb + t], h * 64, itm.q_row0 + t * 128,
+                            itm.hq, itm.b);
+            }
+          };
           for (int it = 0; it < 2 * itm.n_kv; ++it) {
+            if (it == 1) load_q();
             const int g = kv_base + it;
             const int slot = g % C::STAGES;
             const uint32_t ph = (g / C::STAGES) & 1;
-            if (li == 0) NT_STAMP(3, it >> 1, (it & 1) * 2);
+            if (li == NT_TRACE_LI) NT_STAMP(3, it >> 1, (it & 1) * 2);
             mbar_wait(&bar_kv_empty[slot], ph ^ 1, p.err, 1);
-            if (li == 0) NT_STAMP(3, it >> 1, (it & 1) * 2 + 1);
+            if (li == NT_TRACE_LI) NT_STAMP(3, it >> 1, (it & 1) * 2 + 1);
             mbar_arrive_expect_tx(&bar_kv_full[slot], C::TKV);
             const CUtensorMap* m = (it & 1) ? &tmV : &tmK;
             const int row = (it >> 1) * 128;
@@ -291,6 +326,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             for (int h = 0; h < D / 64; ++h)
               tma_load_4d(sKV + slot * C::TKV + h * C::HALF, m, &bar_kv_full[slot], h * 64, row, itm.hkv, itm.b);
           }
+          if (itm.n_kv == 0) load_q();
           kv_base += 2 * itm.n_kv;
         }
       }
@@ -300,11 +336,12 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         constexpr uint32_t idS = idesc_bf16(128, 128, 0, 0);
         constexpr uint32_t idO = idesc_bf16(128, D, 0, 1);
         const uint32_t sQa = smem_u32(sQ), sKVa = smem_u32(sKV);
+        int qb = 0;  // Q buffer pair of the current item
         auto issue_s = [&](int t, int slot) {
 #pragma unroll
           for (int k = 0; k < D / 16; ++k) {
             const uint32_t off = (k >> 2) * C::HALF + (k & 3) * 32;
-            const uint64_t a = sdesc_sw128(sQa + t * C::TQ + off, 16, 1024);
+            const uint64_t a = sdesc_sw128(sQa + (qb + t) * C::TQ + off, 16, 1024);
             const uint64_t bd = sdesc_sw128(sKVa + slot * C::TKV + off, 16, 1024);
             umma_ss(tmem + t * 128, a, bd, idS, k > 0 ? 1u : 0u);
           }
@@ -317,57 +354,110 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             umma_ts(tmem + 256 + t * 128, tmem + pcol + k * 8, bd, idO, (acc || k > 0) ? 1u : 0u);
           }
         };
-        int kv_base = 0;
-        uint32_t p_phase[2] = {0u, 0u};
-        uint32_t sf_phase[2] = {0u, 0u};
-        for (int li = 0;; ++li) {
+        // The issue stream runs across work items: the next item's first score
+        // GEMMs S_t(0) are issued inside the current item's tail (as soon as S_t's
+        // TMEM is free), so the softmax warps find them ready after the epilogue.
+        auto fetch = [&](int li) -> int {  // item index of the CTA's li-th item, -1 at the end
           const int slot_i = li % kItemRing;
           mbar_wait(&bar_item_full[slot_i], (li / kItemRing) & 1, p.err, 13);
           const int w = item_ring[slot_i];
           mbar_arrive(&bar_item_empty[slot_i]);
-          if (w >= p.n_items) break;
-          const int n_kv = attn_item<MASK>(p, w).n_kv;
-          mbar_wait(&bar_q[0], li & 1, p.err, 2);
-          mbar_wait(&bar_q[1], li & 1, p.err, 2);
+          return w < p.n_items ? w : -1;
+        };
+        auto wait_q = [&](int li) {
+          qb = (li % C::QB) * 2;
+          mbar_wait(&bar_q[qb], (li / C::QB) & 1, p.err, 2);
+          mbar_wait(&bar_q[qb + 1], (li / C::QB) & 1, p.err, 2);
+          if (li < 15) NT_STAMP(3, 48 + li, 3);  // trace: MMA has Q of item li
+        };
+        // S_t(0) of an item from its K(0) at ring index g (both tiles)
+        auto first_s = [&](int g, int n_kv) {
+          const int slotK = g % C::STAGES;
+          mbar_wait(&bar_kv_full[slotK], (g / C::STAGES) & 1, p.err, 3);
           tc_fence_after();
-          if constexpr (C::SEP_P) {
-            // stream per tile: S(0), S(1), PV(0), S(2), PV(1), ... -- S(j) waits only
-            // until the softmax warps have read S(j-1) out of TMEM
-            for (int j = 0; j < n_kv; ++j) {
-              const int gK = kv_base + 2 * j;
-              const int slotK = gK % C::STAGES;
-              mbar_wait(&bar_kv_full[slotK], (gK / C::STAGES) & 1, p.err, 3);
-              tc_fence_after();
+          for (int t = 0; t < 2; ++t) {
+            issue_s(t, slotK);
+            umma_commit(&bar_s_full[t]);
+            if (n_kv == 1) umma_commit(&bar_q_empty[qb + t]);
+          }
+          umma_commit(&bar_kv_empty[slotK]);
+        };
+        int kv_base = 0;
+        uint32_t p_phase[2] = {0u, 0u};
+        uint32_t sf_phase[2] = {0u, 0u};
+        int w = fetch(0);
+        int n_kv = w >= 0 ? attn_item<MASK>(p, w).n_kv : 0;
+        if (w >= 0) {
+          wait_q(0);
+          first_s(0, n_kv);
+        }
+        for (int li = 0; w >= 0; ++li) {
+          // ---- steps j = 1 .. n_kv-1: S_t(j) and PV_t(j-1)
+          for (int j = 1; j < n_kv; ++j) {
+            const int gK = kv_base + 2 * j;
+            const int slotK = gK % C::STAGES;
+            const int gV = gK - 1;  // V(j-1)
+            const int slotV = gV % C::STAGES;
+            if (li == NT_TRACE_LI) NT_STAMP(0, j, 0);
+            mbar_wait(&bar_kv_full[slotK], (gK / C::STAGES) & 1, p.err, 3);
+            if (li == NT_TRACE_LI) NT_STAMP(0, j, 1);
+            tc_fence_after();
+            if constexpr (C::SEP_P) {
+              // S_t(j) waits only until the softmax warps have read S_t(j-1) out of TMEM
               for (int t = 0; t < 2; ++t) {
-                if (j > 0) {
-                  mbar_wait(&bar_s_free[t], sf_phase[t], p.err, 15);
-                  sf_phase[t] ^= 1u;
-                  tc_fence_after();
-                }
+                mbar_wait(&bar_s_free[t], sf_phase[t], p.err, 15);
+                sf_phase[t] ^= 1u;
+                tc_fence_after();
+                if (li == NT_TRACE_LI) NT_STAMP(0, j, 2 + t);
                 issue_s(t, slotK);
                 umma_commit(&bar_s_full[t]);
-                if (j == n_kv - 1) umma_commit(&bar_q_empty[t]);
+                if (j == n_kv - 1) umma_commit(&bar_q_empty[qb + t]);
               }
               umma_commit(&bar_kv_empty[slotK]);
-              if (j > 0) {
-                const int gV = gK - 1;
-                const int slotV = gV % C::STAGES;
-                for (int t = 0; t < 2; ++t) {
-                  mbar_wait(&bar_p_full[t], p_phase[t], p.err, 4);
-                  p_phase[t] ^= 1u;
-                  if (t == 0) mbar_wait(&bar_kv_full[slotV], (gV / C::STAGES) & 1, p.err, 5);
-                  tc_fence_after();
-                  issue_pv(t, slotV, j - 1 > 0);
-                  umma_commit(&bar_pv_done[t]);
-                }
-                umma_commit(&bar_kv_empty[slotV]);
+              for (int t = 0; t < 2; ++t) {
+                mbar_wait(&bar_p_full[t], p_phase[t], p.err, 4);
+                p_phase[t] ^= 1u;
+                if (t == 0) mbar_wait(&bar_kv_full[slotV], (gV / C::STAGES) & 1, p.err, 5);
+                tc_fence_after();
+                if (li == NT_TRACE_LI) NT_STAMP(0, j, 4 + t);
+                issue_pv(t, slotV, j - 1 > 0);
+                umma_commit(&bar_pv_done[t]);
               }
+              umma_commit(&bar_kv_empty[slotV]);
+            } else {
+              // P_t(j-1) aliases S_t: PV_t(j-1) then S_t(j), tile 0 then tile 1
+              for (int t = 0; t < 2; ++t) {
+                mbar_wait(&bar_p_full[t], p_phase[t], p.err, 4);
+                p_phase[t] ^= 1u;
+                if (li == NT_TRACE_LI) NT_STAMP(0, j, 2 + 2 * t);
+                if (t == 0) mbar_wait(&bar_kv_full[slotV], (gV / C::STAGES) & 1, p.err, 5);
+                tc_fence_after();
+                issue_pv(t, slotV, j - 1 > 0);
+                if (t == 1) umma_commit(&bar_kv_empty[slotV]);
+                issue_s(t, slotK);
+                umma_commit(&bar_s_full[t]);
+                if (j == n_kv - 1) umma_commit(&bar_q_empty[qb + t]);
+                if (li == NT_TRACE_LI) NT_STAMP(0, j, 3 + 2 * t);
+              }
+              umma_commit(&bar_kv_empty[slotK]);
             }
-            const int gV = kv_base + 2 * (n_kv - 1) + 1;
-            const int slotV = gV % C::STAGES;
+          }
+          // ---- tail: PV_t(n_kv-1) -> O complete, interleaved with the next item's S_t(0)
+          const int wn = fetch(li + 1);
+          const int n_next = wn >= 0 ? attn_item<MASK>(p, wn).n_kv : 0;
+          const int gV = kv_base + 2 * n_kv - 1;
+          const int slotV = gV % C::STAGES;
+          const int gKn = kv_base + 2 * n_kv;  // ring index of the next item's K(0)
+          if constexpr (C::SEP_P) {
             for (int t = 0; t < 2; ++t) {
               mbar_wait(&bar_s_free[t], sf_phase[t], p.err, 16);
               sf_phase[t] ^= 1u;
+            }
+            if (wn >= 0) {
+              wait_q(li + 1);
+              first_s(gKn, n_next);
+            }
+            for (int t = 0; t < 2; ++t) {
               mbar_wait(&bar_p_full[t], p_phase[t], p.err, 6);
               p_phase[t] ^= 1u;
               if (t == 0) mbar_wait(&bar_kv_full[slotV], (gV / C::STAGES) & 1, p.err, 7);
@@ -377,52 +467,37 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
               umma_commit(&bar_o_full[t]);
             }
             umma_commit(&bar_kv_empty[slotV]);
-            kv_base += 2 * n_kv;
-            continue;
-          }
-          for (int j = 0; j < n_kv; ++j) {
-            const int gK = kv_base + 2 * j;
-            const int slotK = gK % C::STAGES;
-            if (li == 0) NT_STAMP(0, j, 0);
-            mbar_wait(&bar_kv_full[slotK], (gK / C::STAGES) & 1, p.err, 3);
-            if (li == 0) NT_STAMP(0, j, 1);
-            tc_fence_after();
-            const int gV = gK - 1;  // V_{j-1}
-            const int slotV = (gV + C::STAGES) % C::STAGES;
+          } else {
+            const int slotKn = gKn % C::STAGES;
             for (int t = 0; t < 2; ++t) {
-              if (j > 0) {
-                mbar_wait(&bar_p_full[t], p_phase[t], p.err, 4);
-                p_phase[t] ^= 1u;
-                if (li == 0) NT_STAMP(0, j, 2 + 2 * t);
-                if (t == 0) mbar_wait(&bar_kv_full[slotV], (gV / C::STAGES) & 1, p.err, 5);
-                tc_fence_after();
-                issue_pv(t, slotV, j - 1 > 0);
-                if (t == 1) umma_commit(&bar_kv_empty[slotV]);
+              mbar_wait(&bar_p_full[t], p_phase[t], p.err, 6);
+              p_phase[t] ^= 1u;
+              if (t == 0) mbar_wait(&bar_kv_full[slotV], (gV / C::STAGES) & 1, p.err, 7);
+              tc_fence_after();
+              issue_pv(t, slotV, n_kv - 1 > 0);
+              umma_commit(&bar_o_full[t]);
+              if (wn >= 0) {
+                if (t == 0) {
+                  wait_q(li + 1);
+                  mbar_wait(&bar_kv_full[slotKn], (gKn / C::STAGES) & 1, p.err, 3);
+                  tc_fence_after();
+                }
+                issue_s(t, slotKn);
+                umma_commit(&bar_s_full[t]);
+                if (n_next == 1) umma_commit(&bar_q_empty[qb + t]);
               }
-              issue_s(t, slotK);
-              umma_commit(&bar_s_full[t]);
-              if (j == n_kv - 1) umma_commit(&bar_q_empty[t]);
-              if (li == 0) NT_STAMP(0, j, 3 + 2 * t);
             }
-            umma_commit(&bar_kv_empty[slotK]);
+            umma_commit(&bar_kv_empty[slotV]);
+            if (wn >= 0) umma_commit(&bar_kv_empty[slotKn]);
           }
-          const int gV = kv_base + 2 * (n_kv - 1) + 1;
-          const int slotV = gV % C::STAGES;
-          for (int t = 0; t < 2; ++t) {
-            mbar_wait(&bar_p_full[t], p_phase[t], p.err, 6);
-            p_phase[t] ^= 1u;
-            if (t == 0) mbar_wait(&bar_kv_full[slotV], (gV / C::STAGES) & 1, p.err, 7);
-            tc_fence_after();
-            issue_pv(t, slotV, n_kv - 1 > 0);
-            umma_commit(&bar_o_full[t]);
-          }
-          umma_commit(&bar_kv_empty[slotV]);
-          kv_base += 2 * n_kv;
+          kv_base = gKn;
+          w = wn;
+          n_kv = n_next;
         }
       }
     }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 216;");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 200;");
     // ================= softmax (+ lazy O correction + epilogue), one thread per query row
     const int t = (warp - 4) / 4;
     const int wq = warp & 3;  // TMEM sub-partition this warp may access
@@ -437,7 +512,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     int pv_base = 0;  // SEP_P: PV_t completions of earlier items
     for (int li = 0;; ++li) {
       const int slot_i = li % kItemRing;
+      if (t == 0 && wq == 0 && lane == 0 && li < 15) NT_STAMP(3, 48 + li, 4);  // trace: softmax asks for item li
       mbar_wait(&bar_item_full[slot_i], (li / kItemRing) & 1, p.err, 14);
+      if (t == 0 && wq == 0 && lane == 0 && li < 15) NT_STAMP(3, 48 + li, 5);
       const int w = item_ring[slot_i];
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_item_empty[slot_i]);
@@ -448,10 +525,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       if (t == 0 && wq == 0 && lane == 0 && li < 16) NT_STAMP(3, 32 + li, 6);  // item start (trace)
 
       for (int j = 0; j < itm.n_kv; ++j) {
-        if (li == 0 && lane == 0 && wq == 0) NT_STAMP(1 + t, j, 0);
+        if (li == NT_TRACE_LI && lane == 0 && wq == 0) NT_STAMP(1 + t, j, 0);
         mbar_wait(&bar_s_full[t], s_phase, p.err, 8);
         s_phase ^= 1u;
-        if (li == 0 && lane == 0 && wq == 0) NT_STAMP(1 + t, j, 1);
+        if (li == NT_TRACE_LI && lane == 0 && wq == 0) NT_STAMP(1 + t, j, 1);
         tc_fence_after();
         uint32_t s[128];
 #pragma unroll
@@ -462,7 +539,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&bar_s_free[t]);
         }
-        if (li == 0 && lane == 0 && wq == 0) NT_STAMP(1 + t, j, 2);
+        if (li == NT_TRACE_LI && lane == 0 && wq == 0) NT_STAMP(1 + t, j, 2);
         const int kv0 = j * 128;
         if (MASK == MASK_TENSOR) {
           const float* mrow = p.mask + (long long)min(qi, p.N - 1) * p.mask_row_stride;
@@ -496,7 +573,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           a1 = fmax3(a1, __uint_as_float(s[126]), __uint_as_float(s[127]));
           mx = fmaxf(fmax3(a0, a1, a2), a3);
         }
-        if (li == 0 && lane == 0 && wq == 0) NT_STAMP(1 + t, j, 3);
+        if (li == NT_TRACE_LI && lane == 0 && wq == 0) NT_STAMP(1 + t, j, 3);
         if (C::SEP_P && j > 0) {
           // PV_t(j-1) must be complete before O_t is rescaled or P_t overwritten;
           // completions up to j-2 were waited for at j-1, so the parity is exact
@@ -513,10 +590,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         }
         const float m_use = (m_run == NINF) ? 0.f : m_run;
         const float sum = attn_exp_pass(s, sc, m_use, tP);
-        if (li == 0 && lane == 0 && wq == 0) NT_STAMP(1 + t, j, 4);
+        if (li == NT_TRACE_LI && lane == 0 && wq == 0) NT_STAMP(1 + t, j, 4);
         l_run += sum;
         tmem_wait_st();
-        if (li == 0 && lane == 0 && wq == 0) NT_STAMP(1 + t, j, 5);
+        if (li == NT_TRACE_LI && lane == 0 && wq == 0) NT_STAMP(1 + t, j, 5);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&bar_p_full[t]);
@@ -524,33 +601,50 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 
       pv_base += itm.n_kv;
 
-      // ---- epilogue: O / l straight from TMEM to global (one row per thread)
+      // ---- epilogue (O_t complete in TMEM)
       mbar_wait(&bar_o_full[t], li & 1, p.err, 9);
+      if (t == 0 && wq == 0 && lane == 0 && li < 15) NT_STAMP(3, 48 + li, 6);  // trace: O of item li complete
       tc_fence_after();
       const bool valid = qi < p.N;
       if (valid && !(l_run > 0.f) && p.err) atomicOr(p.err, 1);
       const float inv = (l_run > 0.f) ? 1.0f / l_run : 0.f;
-      const long long row_off = (long long)itm.b * p.o_sb + (long long)itm.hq * p.o_sh + (long long)qi * p.o_sn;
+      // ---- epilogue: O / l from TMEM -> swizzled smem box (one row per lane) ->
+      // TMA store of 32 rows x 32 columns per warp (rows past N are clipped)
+      uint8_t* stg = smem + C::SMEM_O + (warp - 4) * C::OBOX;
+      const int row0 = itm.q_row0 + t * 128 + wq * 32;
 #pragma unroll
       for (int c = 0; c < D / 32; ++c) {
         uint32_t o[32];
         tmem_ld32(tO + c * 32, o);
         tmem_wait_ld();
-        if (!valid) continue;
+        if (lane == 0) bulk_wait_read0();  // this warp's previous box has left shared memory
+        __syncwarp();
         if (OUT_F32) {
-          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.o) + row_off + c * 32);
+          // 128-byte rows, 16-byte chunk q at q ^ (row & 7) (SWIZZLE_128B)
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
-            dst[i] = make_float4(__uint_as_float(o[4 * i]) * inv, __uint_as_float(o[4 * i + 1]) * inv,
-                                 __uint_as_float(o[4 * i + 2]) * inv, __uint_as_float(o[4 * i + 3]) * inv);
+          for (int q = 0; q < 8; ++q) {
+            const uint4 v = make_uint4(__float_as_uint(__uint_as_float(o[4 * q]) * inv),
+                                       __float_as_uint(__uint_as_float(o[4 * q + 1]) * inv),
+                                       __float_as_uint(__uint_as_float(o[4 * q + 2]) * inv),
+                                       __float_as_uint(__uint_as_float(o[4 * q + 3]) * inv));
+            *reinterpret_cast<uint4*>(stg + lane * 128 + ((q ^ (lane & 7)) << 4)) = v;
+          }
         } else {
-          uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.o) + row_off + c * 32);
+          // 64-byte rows, 16-byte chunk q at q ^ ((row >> 1) & 3) (SWIZZLE_64B)
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            dst[q] = make_uint4(pack_bf16(__uint_as_float(o[8 * q]) * inv, __uint_as_float(o[8 * q + 1]) * inv),
-                                pack_bf16(__uint_as_float(o[8 * q + 2]) * inv, __uint_as_float(o[8 * q + 3]) * inv),
-                                pack_bf16(__uint_as_float(o[8 * q + 4]) * inv, __uint_as_float(o[8 * q + 5]) * inv),
-                                pack_bf16(__uint_as_float(o[8 * q + 6]) * inv, __uint_as_float(o[8 * q + 7]) * inv));
+          for (int q = 0; q < 4; ++q) {
+            const uint4 v = make_uint4(pack_bf16(__uint_as_float(o[8 * q]) * inv, __uint_as_float(o[8 * q + 1]) * inv),
+                                       pack_bf16(__uint_as_float(o[8 * q + 2]) * inv, __uint_as_float(o[8 * q + 3]) * inv),
+                                       pack_bf16(__uint_as_float(o[8 * q + 4]) * inv, __uint_as_float(o[8 * q + 5]) * inv),
+                                       pack_bf16(__uint_as_float(o[8 * q + 6]) * inv, __uint_as_float(o[8 * q + 7]) * inv));
+            *reinterpret_cast<uint4*>(stg + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)) = v;
+          }
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_4d(&tmO, stg, c * 32, row0, itm.hq, itm.b);
+          bulk_commit();
         }
       }
       // O_t is read out: the next item's first PV_t (issued after this warp's
@@ -558,6 +652,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       tc_fence_before();
       if (t == 0 && wq == 0 && lane == 0 && li < 16) NT_STAMP(3, 32 + li, 7);  // item end (trace)
     }
+    if (lane == 0) bulk_wait0();  // the last O boxes are written before the CTA exits
   }
 
   __syncwarp();

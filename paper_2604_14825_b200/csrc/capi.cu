@@ -51,9 +51,10 @@ static EncodeFn get_encode() {
   return fn;
 }
 
-// rank-4 bf16 map over [B, H, S, D] (dims innermost-first), box {64, box_rows, 1, 1}, 128B swizzle
+// rank-4 map over [B, H, S, D] (dims innermost-first), box {box_inner (default one
+// 128-byte row), box_rows, 1, 1}, 128B swizzle unless given
 int make_map_4d(CUtensorMap* m, const void* ptr, int64_t D, int64_t S, int64_t H, int64_t B, int64_t sS,
-                int64_t sH, int64_t sB, int box_rows, size_t elem) {
+                int64_t sH, int64_t sB, int box_rows, size_t elem, int box_inner, CUtensorMapSwizzle swz) {
   EncodeFn enc = get_encode();
   if (!enc) return set_error(NT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   if (reinterpret_cast<uintptr_t>(ptr) % 16) return set_error(NT_ERR_INVALID, "tensor base not 16B aligned");
@@ -63,11 +64,11 @@ int make_map_4d(CUtensorMap* m, const void* ptr, int64_t D, int64_t S, int64_t H
     if (strides[i] % 16) return set_error(NT_ERR_INVALID, "tensor strides must be multiples of 16 bytes");
     if (strides[i] == 0) strides[i] = 16;  // broadcast dims of extent 1
   }
-  cuuint32_t box[4] = {(cuuint32_t)(128 / elem), (cuuint32_t)box_rows, 1, 1};
+  cuuint32_t box[4] = {(cuuint32_t)(box_inner ? box_inner : 128 / elem), (cuuint32_t)box_rows, 1, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = enc(m, elem == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
                    const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(NT_ERR_INVALID, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
   return NT_OK;
@@ -114,10 +115,10 @@ int make_map_pages_5d(CUtensorMap* m, const void* ptr, int64_t page_size, int64_
 
 // ----------------------------------------------------------------- attention
 template <int D, int MASK, bool F32, int KVS>
-static int launch_attn(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const AttnFwdParams& p,
-                       cudaStream_t st) {
+static int launch_attn(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mo,
+                       const AttnFwdParams& p, cudaStream_t st) {
   auto kern = attn_fwd_kernel<D, MASK, F32, KVS>;
-  const int smem = AttnCfg<D, KVS>::SMEM_BYTES;
+  const int smem = AttnCfg<D, KVS, F32>::SMEM_BYTES;
   static bool configured = false;
   if (!configured) {
     int rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
@@ -127,34 +128,34 @@ static int launch_attn(const CUtensorMap& mq, const CUtensorMap& mk, const CUten
   }
   // persistent: at most one CTA per SM, each walking items blockIdx.x + k * gridDim.x
   const int grid = std::min(p.n_items, num_sms());
-  kern<<<grid, kAttnThreads, smem, st>>>(mq, mk, mv, p);
+  kern<<<grid, kAttnThreads, smem, st>>>(mq, mk, mv, mo, p);
   g_launches++;
   return check_cuda(cudaGetLastError(), "attn_fwd launch");
 }
 
 template <int D, int MASK, bool F32>
 static int launch_attn_stages(int ma_stages, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
-                              const AttnFwdParams& p, cudaStream_t st) {
+                              const CUtensorMap& mo, const AttnFwdParams& p, cudaStream_t st) {
   constexpr int kShallow = attn_kv_slots<D>(1), kDeep = attn_kv_slots<D>(2);
-  return attn_kv_slots<D>(ma_stages) == kShallow ? launch_attn<D, MASK, F32, kShallow>(mq, mk, mv, p, st)
-                                                 : launch_attn<D, MASK, F32, kDeep>(mq, mk, mv, p, st);
+  return attn_kv_slots<D>(ma_stages) == kShallow ? launch_attn<D, MASK, F32, kShallow>(mq, mk, mv, mo, p, st)
+                                                 : launch_attn<D, MASK, F32, kDeep>(mq, mk, mv, mo, p, st);
 }
 
 template <int D>
 static int dispatch_attn(const nt_attn_args* a, const CUtensorMap& mq, const CUtensorMap& mk,
-                         const CUtensorMap& mv, const AttnFwdParams& p, cudaStream_t st) {
+                         const CUtensorMap& mv, const CUtensorMap& mo, const AttnFwdParams& p, cudaStream_t st) {
   const bool f32 = a->out_dtype == NT_DTYPE_F32;
   const int sg = a->kv_stages > 0 ? a->kv_stages : 2;  // the MA default (VirtualDevice.stage_default)
   switch (a->mask_kind) {
     case NT_MASK_NONE:
-      return f32 ? launch_attn_stages<D, MASK_NONE, true>(sg, mq, mk, mv, p, st)
-                 : launch_attn_stages<D, MASK_NONE, false>(sg, mq, mk, mv, p, st);
+      return f32 ? launch_attn_stages<D, MASK_NONE, true>(sg, mq, mk, mv, mo, p, st)
+                 : launch_attn_stages<D, MASK_NONE, false>(sg, mq, mk, mv, mo, p, st);
     case NT_MASK_CAUSAL:
-      return f32 ? launch_attn_stages<D, MASK_CAUSAL, true>(sg, mq, mk, mv, p, st)
-                 : launch_attn_stages<D, MASK_CAUSAL, false>(sg, mq, mk, mv, p, st);
+      return f32 ? launch_attn_stages<D, MASK_CAUSAL, true>(sg, mq, mk, mv, mo, p, st)
+                 : launch_attn_stages<D, MASK_CAUSAL, false>(sg, mq, mk, mv, mo, p, st);
     case NT_MASK_TENSOR:
-      return f32 ? launch_attn_stages<D, MASK_TENSOR, true>(sg, mq, mk, mv, p, st)
-                 : launch_attn_stages<D, MASK_TENSOR, false>(sg, mq, mk, mv, p, st);
+      return f32 ? launch_attn_stages<D, MASK_TENSOR, true>(sg, mq, mk, mv, mo, p, st)
+                 : launch_attn_stages<D, MASK_TENSOR, false>(sg, mq, mk, mv, mo, p, st);
   }
   return set_error(NT_ERR_INVALID, "unknown mask_kind");
 }
@@ -184,12 +185,17 @@ extern "C" int nt_attn_fwd(const nt_attn_args* a, void* stream) {
   if ((rc = make_map_4d(&mv, a->v.ptr, D, a->seq_kv, a->heads_kv, a->batch, a->v.stride_s, a->v.stride_h,
                         a->v.stride_b, 128, 2)))
     return rc;
-  // the epilogue stores O rows straight from registers (16-byte vectors)
-  if (reinterpret_cast<uintptr_t>(a->o.ptr) % 16 ||
-      (a->o.stride_s * (a->out_dtype == NT_DTYPE_F32 ? 4 : 2)) % 16 ||
-      (a->o.stride_h * (a->out_dtype == NT_DTYPE_F32 ? 4 : 2)) % 16 ||
-      (a->o.stride_b * (a->out_dtype == NT_DTYPE_F32 ? 4 : 2)) % 16)
+  // the epilogue writes O by TMA: 32-row x 32-column boxes, swizzled to match
+  // the row-per-lane staging writes
+  const bool f32 = a->out_dtype == NT_DTYPE_F32;
+  if (reinterpret_cast<uintptr_t>(a->o.ptr) % 16 || (a->o.stride_s * (f32 ? 4 : 2)) % 16 ||
+      (a->o.stride_h * (f32 ? 4 : 2)) % 16 || (a->o.stride_b * (f32 ? 4 : 2)) % 16)
     return set_error(NT_ERR_INVALID, "output must be 16B aligned with 16B-multiple strides");
+  CUtensorMap mo;
+  if ((rc = make_map_4d(&mo, a->o.ptr, D, a->seq_q, a->heads_q, a->batch, a->o.stride_s, a->o.stride_h,
+                        a->o.stride_b, 32, f32 ? 4 : 2, 32,
+                        f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B)))
+    return rc;
   AttnFwdParams p{};
   p.B = a->batch;
   p.Hq = a->heads_q;
@@ -211,7 +217,7 @@ extern "C" int nt_attn_fwd(const nt_attn_args* a, void* stream) {
   p.err = a->err_flag;
   p.work = a->work_counter;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  return D == 64 ? dispatch_attn<64>(a, mq, mk, mv, p, st) : dispatch_attn<128>(a, mq, mk, mv, p, st);
+  return D == 64 ? dispatch_attn<64>(a, mq, mk, mv, mo, p, st) : dispatch_attn<128>(a, mq, mk, mv, mo, p, st);
 }
 
 // ----------------------------------------------------------------- casts
@@ -260,9 +266,10 @@ extern "C" int nt_cast_bf16_to_f32(const void* src, float* dst, int64_t n, void*
 
 #ifdef NT_TRACE
 // debug builds only: route the K1 pipeline timeline stamps of one CTA into `buf`
-extern "C" int nt_debug_set_trace(unsigned long long* buf, int cta) {
+extern "C" int nt_debug_set_trace(unsigned long long* buf, int cta, int item) {
   cudaMemcpyToSymbol(nt::g_nt_trace, &buf, sizeof(buf));
   cudaMemcpyToSymbol(nt::g_nt_trace_cta, &cta, sizeof(cta));
+  cudaMemcpyToSymbol(nt::g_nt_trace_li, &item, sizeof(item));
   return check_cuda(cudaGetLastError(), "nt_debug_set_trace");
 }
 extern "C" int nt_debug_set_cta_times(unsigned long long* buf) {

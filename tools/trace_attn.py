@@ -16,6 +16,7 @@ from paper_2604_14825_b200.runtime import AttentionPlan  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--cta", type=int, default=0)
+ap.add_argument("--item", type=int, default=0, help="which of the CTA's work items to stamp")
 ap.add_argument("--n", type=int, default=8192)
 ap.add_argument("--causal", type=int, default=1)
 ap.add_argument("--out", default="gpurun_out/trace.json")
@@ -26,7 +27,7 @@ ap.add_argument("--hkv", type=int, default=8)
 ap.add_argument("--scale", type=float, default=0.0883883)
 a = ap.parse_args()
 L = _lib.lib()
-L.nt_debug_set_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
+L.nt_debug_set_trace.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
 buf = torch.zeros(4 * 64 * 8, dtype=torch.int64, device="cuda")
 N, D = a.n, a.d
 q = torch.randn(a.b, a.hq, N, D, device="cuda").bfloat16()
@@ -37,10 +38,10 @@ plan = AttentionPlan(q, k, v, o, a.scale, "causal" if a.causal else "none")
 for _ in range(3):
     plan.launch()
 torch.cuda.synchronize()
-L.nt_debug_set_trace(buf.data_ptr(), a.cta)
+L.nt_debug_set_trace(buf.data_ptr(), a.cta, a.item)
 plan.launch()
 torch.cuda.synchronize()
-L.nt_debug_set_trace(None, a.cta)
+L.nt_debug_set_trace(None, a.cta, 0)
 t = buf.view(4, 64, 8).cpu().numpy()
 base = t[t > 0].min()
 res = {}
@@ -56,6 +57,11 @@ json.dump(res, open(a.out, "w"))
 print("kernel entry", int(t[3, 63, 7] - base) if t[3, 63, 7] > 0 else None)
 print("items (start, end) of tile 0:", [(int(t[3, 32 + i, 6] - base), int(t[3, 32 + i, 7] - base))
                                        for i in range(16) if t[3, 32 + i, 6] > 0])
+print("per item [producer reaches, published, -, Q landed, softmax asks, softmax gets, O complete]:")
+for i in range(15):
+    r = t[3, 48 + i, :7]
+    if (r > 0).any():
+        print(i, [int(x - base) if x > 0 else None for x in r])
 for name in ("mma", "softmax0", "softmax1", "producer"):
     print(name)
     for i, r in enumerate(res[name][:12]):
