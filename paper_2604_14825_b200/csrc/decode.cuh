@@ -232,7 +232,6 @@ __global__ void __launch_bounds__(kDecodeCTAThreads, 1)
         const int kr = u * KPS + kg;
         const bool valid = j0 + t * kDecodeTile + kr < j1;
         float kf[DPT], vf[DPT];
-#pragma unroll
         // key kr, 16-byte chunk: panel-major tile ([panel][64 keys][128 B]), or for
         // small pages [sub][panel][rows][128 B] with rows = 1 << rows_log2
         const int kbase = (PG == 2)

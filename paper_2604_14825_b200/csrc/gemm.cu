@@ -11,6 +11,10 @@
 #include "common_host.h"
 #include "gemm.cuh"
 
+#ifndef NT_GEMM_GROUP
+#define NT_GEMM_GROUP 0  // experiment: raster group rows (0 = default 8)
+#endif
+
 using namespace nt;
 
 namespace {
@@ -67,10 +71,17 @@ int launch_gemm2(const nt_gemm_args* a, cudaStream_t st) {
   p.K = a->k;
   p.tiles_m = (a->m + 255) / 256;
   p.tiles_n = (a->n + 255) / 256;
+  // raster groups only when A's panels would not stay in L2 (~126 MB) next to B's
+  const double a_bytes = 2.0 * a->m * a->k;
+  p.group_m = (a_bytes > 48e6 && p.tiles_m > 8) ? (NT_GEMM_GROUP > 0 ? NT_GEMM_GROUP : 8) : p.tiles_m;
   p.c = a->c;
   p.ldc = a->ldc;
+  CUtensorMap mc;
+  if ((rc = make_map_2d(&mc, a->c, a->n, a->m, a->ldc, 32, 32, F32 ? 4 : 2,
+                        F32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B)))
+    return rc;
   auto kern = gemm2_kernel<F32>;
-  const int smem = Gemm2Cfg::SMEM_BYTES;
+  const int smem = Gemm2Cfg<F32>::SMEM_BYTES;
   static bool configured = false;
   if (!configured) {
     if ((rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
@@ -80,7 +91,7 @@ int launch_gemm2(const nt_gemm_args* a, cudaStream_t st) {
   }
   const int tiles = p.tiles_m * p.tiles_n;
   const int grid = 2 * std::min(tiles, sm_count() / 2);  // one CTA pair per tile, persistent
-  kern<<<grid, kGemmThreads, smem, st>>>(ma, mb, p);
+  kern<<<grid, kGemmThreads, smem, st>>>(ma, mb, mc, p);
   g_launches++;
   return check_cuda(cudaGetLastError(), "gemm2 launch");
 }

@@ -18,11 +18,17 @@
 #pragma once
 #include "sm100.cuh"
 
+// experiment switch: 1 = the CTA-pair epilogue reads TMEM but stores nothing
+#ifndef NT_GEMM_NO_STORE
+#define NT_GEMM_NO_STORE 0
+#endif
+
 namespace nt {
 
 struct GemmParams {
   int M, N, K;
   int tiles_m, tiles_n;
+  int group_m;  // CTA-pair kernel: tile rows per raster group
   void* c;
   long long ldc;
 };
@@ -197,22 +203,39 @@ namespace nt {
 //   warp 0      TMA producer (both CTAs; bytes counted on the leader's barrier)
 //   warp 1      MMA issuer (leader CTA only)
 //   warps 2-5   epilogue (both CTAs): TMEM -> registers -> global
+template <bool OUT_F32>
 struct Gemm2Cfg {
   static constexpr int BM = 128, BN = 256, BNH = 128, BK = 64;
   static constexpr int A_BYTES = BM * BK * 2;   // 16 KB: this CTA's 128 rows
   static constexpr int B_BYTES = BK * BNH * 2;  // 16 KB: this CTA's 128 columns
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int STAGES = 6;
-  static constexpr int SMEM_BAR = STAGES * STAGE;
+  // epilogue staging: one swizzled 32 x 32 C box per epilogue warp (TMA store)
+  static constexpr int OBOX = 32 * 32 * (OUT_F32 ? 4 : 2);
+  static constexpr int SMEM_O = STAGES * STAGE;
+  static constexpr int SMEM_BAR = SMEM_O + 4 * OBOX;
   static constexpr int NBAR = 2 * STAGES + 4;
   static constexpr int SMEM_BYTES = SMEM_BAR + NBAR * 8 + 16 + 1024;
 };
 
+// Pair-tile order: groups of p.group_m tile rows walked column by column.  With
+// group_m = tiles_m this is plain column order (A panels stay L2-resident when
+// A fits); for large A (8192^3: 32 panels = 128 MB) groups of 8 rows keep the
+// ~74 tiles in flight on a few A and B panels.
+__device__ __forceinline__ void gemm_tile_coords(const GemmParams& p, int tile, int& mb, int& nb) {
+  const int per_group = p.group_m * p.tiles_n;
+  const int g = tile / per_group, r = tile - g * per_group;
+  const int m0 = g * p.group_m;
+  const int gm = min(p.tiles_m - m0, p.group_m);
+  mb = m0 + r % gm;
+  nb = r / gm;
+}
+
 template <bool OUT_F32>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                 const GemmParams p) {
-  using C = Gemm2Cfg;
+                 const __grid_constant__ CUtensorMap tmC, const GemmParams p) {
+  using C = Gemm2Cfg<OUT_F32>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_u32 = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_u32 + 1023u) & ~1023u) - raw_u32);
@@ -233,6 +256,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
+    prefetch_tmap(&tmC);
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -254,7 +278,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     if (lane == 0) {
       int it = 0;
       for (int tile = pair; tile < num_tiles; tile += npairs) {
-        const int mb = tile % p.tiles_m, nb = tile / p.tiles_m;
+        int mb, nb;
+        gemm_tile_coords(p, tile, mb, nb);
         for (int kb = 0; kb < k_blocks; ++kb, ++it) {
           const int s = it % C::STAGES;
           mbar_wait(&empty[s], ((it / C::STAGES) & 1) ^ 1);
@@ -299,42 +324,43 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   } else {
     // epilogue warps 2..5 -> TMEM sub-partitions 2,3,0,1; this CTA's 128 rows x 256 columns
     const int wq = warp & 3;
-    const int r = wq * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
     int tcount = 0;
     for (int tile = pair; tile < num_tiles; tile += npairs, ++tcount) {
       const int acc = tcount & 1;
-      const int mb = tile % p.tiles_m, nb = tile / p.tiles_m;
+      int mb, nb;
+      gemm_tile_coords(p, tile, mb, nb);
       mbar_wait(&tfull[acc], (tcount >> 1) & 1);
       tc_fence_after();
-      const int row = mb * 256 + (int)rank * 128 + r;
-      const bool rv = row < p.M;
+      // TMEM -> registers -> swizzled smem box -> TMA store (edges clipped by TMA)
+      uint8_t* stg = smem + C::SMEM_O + (warp - 2) * C::OBOX;
+      const int row0 = mb * 256 + (int)rank * 128 + wq * 32;
 #pragma unroll 1
       for (int c = 0; c < C::BN / 32; ++c) {
         uint32_t v[32];
         tmem_ld32(tmem + acc * 256 + lane_off + c * 32, v);
         tmem_wait_ld();
-        const int col0 = nb * C::BN + c * 32;
-        if (rv && col0 < p.N) {
-          if (OUT_F32) {
-            float* cp = static_cast<float*>(p.c) + (long long)row * p.ldc + col0;
+        if (lane == 0) bulk_wait_read0();  // previous box has left shared memory
+        __syncwarp();
+        if (OUT_F32) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
-              if (col0 + 4 * i < p.N)
-                *reinterpret_cast<float4*>(cp + 4 * i) =
-                    make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
-                                __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
-          } else {
-            __nv_bfloat16* cp = static_cast<__nv_bfloat16*>(p.c) + (long long)row * p.ldc + col0;
+          for (int q = 0; q < 8; ++q)
+            *reinterpret_cast<uint4*>(stg + lane * 128 + ((q ^ (lane & 7)) << 4)) =
+                make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        } else {
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
-              if (col0 + 8 * i < p.N)
-                *reinterpret_cast<uint4*>(cp + 8 * i) = make_uint4(
-                    pack_bf16(__uint_as_float(v[8 * i]), __uint_as_float(v[8 * i + 1])),
-                    pack_bf16(__uint_as_float(v[8 * i + 2]), __uint_as_float(v[8 * i + 3])),
-                    pack_bf16(__uint_as_float(v[8 * i + 4]), __uint_as_float(v[8 * i + 5])),
-                    pack_bf16(__uint_as_float(v[8 * i + 6]), __uint_as_float(v[8 * i + 7])));
-          }
+          for (int q = 0; q < 4; ++q)
+            *reinterpret_cast<uint4*>(stg + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)) = make_uint4(
+                pack_bf16(__uint_as_float(v[8 * q]), __uint_as_float(v[8 * q + 1])),
+                pack_bf16(__uint_as_float(v[8 * q + 2]), __uint_as_float(v[8 * q + 3])),
+                pack_bf16(__uint_as_float(v[8 * q + 4]), __uint_as_float(v[8 * q + 5])),
+                pack_bf16(__uint_as_float(v[8 * q + 6]), __uint_as_float(v[8 * q + 7])));
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0 && !NT_GEMM_NO_STORE) {
+          tma_store_2d(&tmC, stg, nb * C::BN + c * 32, row0);
+          bulk_commit();
         }
       }
       tc_fence_before();
@@ -342,6 +368,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       if (lane == 0) mbar_arrive_cluster(mapa_shared(&tempty[acc], 0));  // the leader's barrier
     }
   }
+  if (warp >= 2 && lane == 0) bulk_wait0();  // the last C boxes are written
   __syncwarp();
   tc_fence_before();
   __syncthreads();
