@@ -42,6 +42,7 @@ extern "C" {
 
 #define NT_DTYPE_BF16 0
 #define NT_DTYPE_F32 1
+#define NT_DTYPE_E4M3 2 /* fp8 e4m3 (attention inputs, with per-tensor descales) */
 
 /* Rank-4 view [batch, heads, seq, dim]; dim is contiguous; strides in elements. */
 typedef struct nt_tensor4 {
@@ -75,6 +76,12 @@ typedef struct nt_attn_args {
   /* the MA kernel's `stages` tunable (0 = the scheduler default 2): K/V tiles
    * kept in flight -- 1 -> one K/V pair (D=128) / two (D=64), >= 2 -> two / four */
   int32_t kv_stages;
+  /* q/k/v element type: NT_DTYPE_BF16 (0) or NT_DTYPE_E4M3 (head_dim 128, no or
+   * causal mask; tcgen05 kind::f8f6f4 with P rounded to e4m3 -- the paper's FP8
+   * regime).  Descales (0 reads as 1): S = (Q K^T) q_descale
+   * k_descale c, O = v_descale P V / l. */
+  int32_t in_dtype;
+  float q_descale, k_descale, v_descale;
 } nt_attn_args;
 int nt_attn_fwd(const nt_attn_args* args, void* stream);
 

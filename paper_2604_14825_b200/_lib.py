@@ -16,7 +16,7 @@ LIB_PATH = os.environ.get("NT_LIB_PATH") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "_native", "libnautilus_b200.so")
 
 NT_MASK_NONE, NT_MASK_CAUSAL, NT_MASK_TENSOR = 0, 1, 2
-NT_DTYPE_BF16, NT_DTYPE_F32 = 0, 1
+NT_DTYPE_BF16, NT_DTYPE_F32, NT_DTYPE_E4M3 = 0, 1, 2
 
 # Every symbol include/nautilus_b200.h declares (checked by tests/test_capi.py).
 EXPORTED = (
@@ -40,7 +40,8 @@ class AttnArgs(C.Structure):
                 ("scale", C.c_float), ("mask_kind", C.c_int32), ("causal_offset", C.c_int32),
                 ("mask", C.c_void_p), ("mask_stride_row", C.c_int64),
                 ("out_dtype", C.c_int32), ("err_flag", C.c_void_p), ("work_counter", C.c_void_p),
-                ("kv_stages", C.c_int32)]
+                ("kv_stages", C.c_int32), ("in_dtype", C.c_int32), ("q_descale", C.c_float),
+                ("k_descale", C.c_float), ("v_descale", C.c_float)]
 
 
 class DecodeArgs(C.Structure):

@@ -60,6 +60,7 @@ struct AttnFwdParams {
   long long o_sb, o_sh, o_sn;
   int* err;  // bit 0: zero denominator (fully masked row); bit 8+k: wait k timed out
   int* work;  // [next, done] dynamic item counter (zero at launch, reset by the last CTA) or null
+  float o_scale;  // e4m3 inputs: V's descale (O = o_scale * P.V / l), else 1
 };
 
 constexpr int kAttnThreads = 384;
@@ -87,12 +88,15 @@ constexpr int attn_kv_slots(int ma_stages) {
   return (D == 128) ? (ma_stages <= 1 ? 2 : 4) : (ma_stages <= 1 ? 4 : 8);
 }
 
-template <int D, int KVS = attn_kv_slots<D>(2), bool OUT_F32 = false>
+template <int D, int KVS = attn_kv_slots<D>(2), bool OUT_F32 = false, bool FP8 = false>
 struct AttnCfg {
   static constexpr int BM = 128, BN = 128;
-  static constexpr int HALF = 128 * 64 * 2;  // one 128-row x 64-col bf16 swizzle-128B panel
-  static constexpr int TQ = BM * D * 2;
-  static constexpr int TKV = BN * D * 2;
+  static constexpr int ESZ = FP8 ? 1 : 2;     // operand bytes (bf16 | e4m3)
+  static constexpr int HALF = 128 * 128;      // one 128-row x 128-byte swizzle-128B panel
+  static constexpr int PANELS = D * ESZ / 128;
+  static constexpr int KSTEP = FP8 ? 32 : 16;  // K per tcgen05.mma (kind::f8f6f4 | kind::f16)
+  static constexpr int TQ = BM * D * ESZ;
+  static constexpr int TKV = BN * D * ESZ;
   static constexpr int STAGES = KVS;
   // D = 64: O_t needs only 64 TMEM columns, so P_t gets its own 64 columns
   // next to it instead of aliasing S_t.  S_t(j+1) can then be computed as soon
@@ -101,7 +105,7 @@ struct AttnCfg {
   static constexpr bool SEP_P = (D == 64);
   // D = 64: Q is double-buffered across work items (the next item's Q lands
   // while the current one runs); D = 128 has no shared memory left for it
-  static constexpr int QB = (D == 64) ? 2 : 1;
+  static constexpr int QB = (D == 64 || FP8) ? 2 : 1;
   static constexpr int SMEM_Q = 0;
   static constexpr int SMEM_KV = 2 * QB * TQ;
   // epilogue staging: per softmax warp one 32-row x 32-column O box (TMA store),
@@ -130,15 +134,17 @@ __device__ __forceinline__ void attn_rescale_o(uint32_t tO, float alpha) {
   }
 }
 
-// P = exp2(S*sc - m) for one 128-key row -> bf16 pairs in TMEM at tP; returns
-// the row sum of P (fp32).
+// P = exp2(S*sc - m) for one 128-key row -> TMEM at tP (bf16 pairs, or e4m3
+// quads when FP8); returns the row sum of P (fp32, before rounding).
+template <bool FP8>
 __device__ __forceinline__ float attn_exp_pass(const uint32_t (&s)[128], float sc, float m, uint32_t tP) {
   const float2 sc2 = make_float2(sc, sc);
   const float2 nm2 = make_float2(-m, -m);
   float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+  uint32_t pk[16];
 #pragma unroll
   for (int ch = 0; ch < 4; ++ch) {
-    uint32_t pk[16];
+    float2 prev = make_float2(0.f, 0.f);
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const float s0 = __uint_as_float(s[ch * 32 + 2 * i]), s1 = __uint_as_float(s[ch * 32 + 2 * i + 1]);
@@ -150,9 +156,15 @@ __device__ __forceinline__ float attn_exp_pass(const uint32_t (&s)[128], float s
         e = make_float2(ex2(x.x), ex2(x.y));
       }
       sum2[i & 1] = fadd2(sum2[i & 1], e);
-      pk[i] = NT_PACK_ALU ? pack_bf16_alu(e.x, e.y) : pack_bf16(e.x, e.y);
+      if (FP8) {
+        if (i & 1) pk[(ch & 1) * 8 + (i >> 1)] = pack_e4m3x4(prev.x, prev.y, e.x, e.y);
+        prev = e;
+      } else {
+        pk[i] = NT_PACK_ALU ? pack_bf16_alu(e.x, e.y) : pack_bf16(e.x, e.y);
+      }
     }
-    tmem_st16(tP + ch * 16, pk);
+    if (!FP8) tmem_st16(tP + ch * 16, pk);
+    else if (ch & 1) tmem_st16(tP + (ch >> 1) * 16, pk);  // 64 keys = 16 columns of e4m3 quads
   }
   return (sum2[0].x + sum2[0].y) + (sum2[1].x + sum2[1].y);
 }
@@ -208,12 +220,12 @@ __device__ __forceinline__ AttnItem attn_item(const AttnFwdParams& p, int w) {
   return it;
 }
 
-template <int D, int MASK, bool OUT_F32, int KVS>
+template <int D, int MASK, bool OUT_F32, int KVS, bool FP8 = false>
 __global__ void __launch_bounds__(kAttnThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
                     const AttnFwdParams p) {
-  using C = AttnCfg<D, KVS, OUT_F32>;
+  using C = AttnCfg<D, KVS, OUT_F32, FP8>;
   static_assert(C::SMEM_BYTES <= 227 * 1024, "K1 shared memory exceeds the 227 KB opt-in limit");
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_u32 = smem_u32(smem_raw);
@@ -306,7 +318,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
               if (li >= C::QB) mbar_wait(&bar_q_empty[qb + t], ((li / C::QB) - 1) & 1, p.err, 11);
               mbar_arrive_expect_tx(&bar_q[qb + t], C::TQ);
 #pragma unroll
-              for (int h = 0; h < D / 64; ++h)
+              for (int h = 0; h < C::PANELS; ++h)
                 tma_load_4d(sQ + (qb + t) * C::TQ + h * C::HALF, &tmQ, &bar_q[qb + t], h * 64, itm.q_row0 + t * 128,
                             itm.hq, itm.b);
             }
@@ -323,7 +335,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             const CUtensorMap* m = (it & 1) ? &tmV : &tmK;
             const int row = (it >> 1) * 128;
 #pragma unroll
-            for (int h = 0; h < D / 64; ++h)
+            for (int h = 0; h < C::PANELS; ++h)
               tma_load_4d(sKV + slot * C::TKV + h * C::HALF, m, &bar_kv_full[slot], h * 64, row, itm.hkv, itm.b);
           }
           if (itm.n_kv == 0) load_q();
@@ -333,25 +345,29 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     } else if (warp == 1) {
       // ================= MMA issuer
       if (lane == 0) {
-        constexpr uint32_t idS = idesc_bf16(128, 128, 0, 0);
-        constexpr uint32_t idO = idesc_bf16(128, D, 0, 1);
+        constexpr uint32_t idS = FP8 ? idesc_e4m3(128, 128, 0, 0) : idesc_bf16(128, 128, 0, 0);
+        constexpr uint32_t idO = FP8 ? idesc_e4m3(128, D, 0, 1) : idesc_bf16(128, D, 0, 1);
         const uint32_t sQa = smem_u32(sQ), sKVa = smem_u32(sKV);
         int qb = 0;  // Q buffer pair of the current item
         auto issue_s = [&](int t, int slot) {
 #pragma unroll
-          for (int k = 0; k < D / 16; ++k) {
+          for (int k = 0; k < D / C::KSTEP; ++k) {
+            // 32 bytes of K per instruction, 4 per 128-byte panel row
             const uint32_t off = (k >> 2) * C::HALF + (k & 3) * 32;
             const uint64_t a = sdesc_sw128(sQa + (qb + t) * C::TQ + off, 16, 1024);
             const uint64_t bd = sdesc_sw128(sKVa + slot * C::TKV + off, 16, 1024);
-            umma_ss(tmem + t * 128, a, bd, idS, k > 0 ? 1u : 0u);
+            if (FP8) umma_ss_f8(tmem + t * 128, a, bd, idS, k > 0 ? 1u : 0u);
+            else umma_ss(tmem + t * 128, a, bd, idS, k > 0 ? 1u : 0u);
           }
         };
         auto issue_pv = [&](int t, int slot, bool acc) {
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const uint64_t bd = sdesc_sw128(sKVa + slot * C::TKV + k * 2048, C::HALF, 1024);
+          for (int k = 0; k < 128 / C::KSTEP; ++k) {
+            // KSTEP keys of V (MN-major, 128-byte rows) x P's 8 TMEM columns
+            const uint64_t bd = sdesc_sw128(sKVa + slot * C::TKV + k * C::KSTEP * 128, C::HALF, 1024);
             const uint32_t pcol = C::SEP_P ? (256 + t * 128 + 64) : (t * 128);
-            umma_ts(tmem + 256 + t * 128, tmem + pcol + k * 8, bd, idO, (acc || k > 0) ? 1u : 0u);
+            if (FP8) umma_ts_f8(tmem + 256 + t * 128, tmem + pcol + k * 8, bd, idO, (acc || k > 0) ? 1u : 0u);
+            else umma_ts(tmem + 256 + t * 128, tmem + pcol + k * 8, bd, idO, (acc || k > 0) ? 1u : 0u);
           }
         };
         // The issue stream runs across work items: the next item's first score
@@ -589,7 +605,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           m_run = m_new;
         }
         const float m_use = (m_run == NINF) ? 0.f : m_run;
-        const float sum = attn_exp_pass(s, sc, m_use, tP);
+        const float sum = attn_exp_pass<FP8>(s, sc, m_use, tP);
         if (li == NT_TRACE_LI && lane == 0 && wq == 0) NT_STAMP(1 + t, j, 4);
         l_run += sum;
         tmem_wait_st();
@@ -607,7 +623,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       tc_fence_after();
       const bool valid = qi < p.N;
       if (valid && !(l_run > 0.f) && p.err) atomicOr(p.err, 1);
-      const float inv = (l_run > 0.f) ? 1.0f / l_run : 0.f;
+      const float inv = (l_run > 0.f) ? p.o_scale / l_run : 0.f;
       // ---- epilogue: O / l from TMEM -> swizzled smem box (one row per lane) ->
       // TMA store of 32 rows x 32 columns per warp (rows past N are clipped)
       uint8_t* stg = smem + C::SMEM_O + (warp - 4) * C::OBOX;

@@ -66,7 +66,10 @@ int make_map_4d(CUtensorMap* m, const void* ptr, int64_t D, int64_t S, int64_t H
   }
   cuuint32_t box[4] = {(cuuint32_t)(box_inner ? box_inner : 128 / elem), (cuuint32_t)box_rows, 1, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUresult r = enc(m, elem == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+  const CUtensorMapDataType dt = elem == 1   ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                                 : elem == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                             : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  CUresult r = enc(m, dt, 4,
                    const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -114,11 +117,11 @@ int make_map_pages_5d(CUtensorMap* m, const void* ptr, int64_t page_size, int64_
 }
 
 // ----------------------------------------------------------------- attention
-template <int D, int MASK, bool F32, int KVS>
+template <int D, int MASK, bool F32, int KVS, bool FP8 = false>
 static int launch_attn(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mo,
                        const AttnFwdParams& p, cudaStream_t st) {
-  auto kern = attn_fwd_kernel<D, MASK, F32, KVS>;
-  const int smem = AttnCfg<D, KVS, F32>::SMEM_BYTES;
+  auto kern = attn_fwd_kernel<D, MASK, F32, KVS, FP8>;
+  const int smem = AttnCfg<D, KVS, F32, FP8>::SMEM_BYTES;
   static bool configured = false;
   if (!configured) {
     int rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
@@ -139,6 +142,26 @@ static int launch_attn_stages(int ma_stages, const CUtensorMap& mq, const CUtens
   constexpr int kShallow = attn_kv_slots<D>(1), kDeep = attn_kv_slots<D>(2);
   return attn_kv_slots<D>(ma_stages) == kShallow ? launch_attn<D, MASK, F32, kShallow>(mq, mk, mv, mo, p, st)
                                                  : launch_attn<D, MASK, F32, kDeep>(mq, mk, mv, mo, p, st);
+}
+
+// e4m3 Q/K/V (head_dim 128, no / causal mask): 16 KB K/V tiles, ring depth as at D=64
+template <int MASK, bool F32>
+static int launch_attn_e4m3(int ma_stages, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
+                            const CUtensorMap& mo, const AttnFwdParams& p, cudaStream_t st) {
+  constexpr int kShallow = attn_kv_slots<64>(1), kDeep = attn_kv_slots<64>(2);
+  return attn_kv_slots<64>(ma_stages) == kShallow ? launch_attn<128, MASK, F32, kShallow, true>(mq, mk, mv, mo, p, st)
+                                                  : launch_attn<128, MASK, F32, kDeep, true>(mq, mk, mv, mo, p, st);
+}
+
+static int dispatch_attn_e4m3(const nt_attn_args* a, const CUtensorMap& mq, const CUtensorMap& mk,
+                              const CUtensorMap& mv, const CUtensorMap& mo, const AttnFwdParams& p, cudaStream_t st) {
+  const bool f32 = a->out_dtype == NT_DTYPE_F32;
+  const int sg = a->kv_stages > 0 ? a->kv_stages : 2;
+  if (a->mask_kind == NT_MASK_NONE)
+    return f32 ? launch_attn_e4m3<MASK_NONE, true>(sg, mq, mk, mv, mo, p, st)
+               : launch_attn_e4m3<MASK_NONE, false>(sg, mq, mk, mv, mo, p, st);
+  return f32 ? launch_attn_e4m3<MASK_CAUSAL, true>(sg, mq, mk, mv, mo, p, st)
+             : launch_attn_e4m3<MASK_CAUSAL, false>(sg, mq, mk, mv, mo, p, st);
 }
 
 template <int D>
@@ -173,17 +196,22 @@ extern "C" int nt_attn_fwd(const nt_attn_args* a, void* stream) {
   if (a->heads_q % a->heads_kv) return set_error(NT_ERR_INVALID, "heads_q must be a multiple of heads_kv");
   if (!(a->scale > 0.f)) return set_error(NT_ERR_UNSUPPORTED, "scale must be positive");
   if (a->mask_kind == NT_MASK_TENSOR && !a->mask) return set_error(NT_ERR_INVALID, "tensor mask missing");
+  const bool e4m3 = a->in_dtype == NT_DTYPE_E4M3;
+  if (a->in_dtype != NT_DTYPE_BF16 && !e4m3) return set_error(NT_ERR_UNSUPPORTED, "q/k/v must be bf16 or e4m3");
+  if (e4m3 && (a->head_dim != 128 || a->mask_kind == NT_MASK_TENSOR))
+    return set_error(NT_ERR_UNSUPPORTED, "e4m3 attention: head_dim 128, no or causal mask");
   const int D = a->head_dim;
+  const size_t in_elem = e4m3 ? 1 : 2;
   CUtensorMap mq, mk, mv;
   int rc;
   if ((rc = make_map_4d(&mq, a->q.ptr, D, a->seq_q, a->heads_q, a->batch, a->q.stride_s, a->q.stride_h,
-                        a->q.stride_b, 128, 2)))
+                        a->q.stride_b, 128, in_elem)))
     return rc;
   if ((rc = make_map_4d(&mk, a->k.ptr, D, a->seq_kv, a->heads_kv, a->batch, a->k.stride_s, a->k.stride_h,
-                        a->k.stride_b, 128, 2)))
+                        a->k.stride_b, 128, in_elem)))
     return rc;
   if ((rc = make_map_4d(&mv, a->v.ptr, D, a->seq_kv, a->heads_kv, a->batch, a->v.stride_s, a->v.stride_h,
-                        a->v.stride_b, 128, 2)))
+                        a->v.stride_b, 128, in_elem)))
     return rc;
   // the epilogue writes O by TMA: 32-row x 32-column boxes, swizzled to match
   // the row-per-lane staging writes
@@ -207,7 +235,11 @@ extern "C" int nt_attn_fwd(const nt_attn_args* a, void* stream) {
   p.n_kv_total = (a->seq_kv + 127) / 128;
   p.n_items = p.n_mblocks * a->batch * a->heads_q;
   p.causal_offset = a->causal_offset;
-  p.scale_log2 = a->scale * 1.4426950408889634f;
+  // e4m3: S = (Q.K^T) q_descale k_descale, O = v_descale P.V / l (a descale of 0 reads as 1)
+  const float qd = (e4m3 && a->q_descale != 0.f) ? a->q_descale : 1.f;
+  const float kd = (e4m3 && a->k_descale != 0.f) ? a->k_descale : 1.f;
+  p.scale_log2 = a->scale * qd * kd * 1.4426950408889634f;
+  p.o_scale = (e4m3 && a->v_descale != 0.f) ? a->v_descale : 1.f;
   p.mask = a->mask;
   p.mask_row_stride = a->mask_stride_row;
   p.o = a->o.ptr;
@@ -217,6 +249,7 @@ extern "C" int nt_attn_fwd(const nt_attn_args* a, void* stream) {
   p.err = a->err_flag;
   p.work = a->work_counter;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (e4m3) return dispatch_attn_e4m3(a, mq, mk, mv, mo, p, st);
   return D == 64 ? dispatch_attn<64>(a, mq, mk, mv, mo, p, st) : dispatch_attn<128>(a, mq, mk, mv, mo, p, st);
 }
 

@@ -41,15 +41,25 @@ def _t4(t: torch.Tensor) -> _lib.Tensor4:
 
 
 class AttentionPlan:
-    """K1 fused attention over a [B, H, N, D] outer grid (bf16 in, bf16/fp32 out)."""
+    """K1 fused attention over a [B, H, N, D] outer grid (bf16 or e4m3 in, bf16/fp32 out).
+
+    e4m3 inputs (``torch.float8_e4m3fn``, head_dim 128, no/causal mask) run the
+    tcgen05 kind::f8f6f4 variant -- the paper's FP8 regime (PAPER.md:778-780),
+    beyond the reference's MA precisions -- with per-tensor descales:
+    S = (Q K^T) q_descale k_descale scale, O = v_descale softmax(S) V, P rounded
+    to e4m3 before P.V.
+    """
 
     def __init__(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor,
                  scale: Optional[float], mask_kind: str = "none", mask: Optional[torch.Tensor] = None,
-                 causal_offset: int = 0, err_flag: Optional[torch.Tensor] = None, kv_stages: int = 0):
+                 causal_offset: int = 0, err_flag: Optional[torch.Tensor] = None, kv_stages: int = 0,
+                 q_descale: float = 1.0, k_descale: float = 1.0, v_descale: float = 1.0):
         q, k, v, o = _as4(q), _as4(k), _as4(v), _as4(o)
+        e4m3 = q.dtype == torch.float8_e4m3fn
+        want = torch.float8_e4m3fn if e4m3 else torch.bfloat16
         for name, t in (("q", q), ("k", k), ("v", v)):
-            if t.dtype != torch.bfloat16 or not t.is_cuda:
-                raise InvalidArguments(f"{name} must be a CUDA bf16 tensor")
+            if t.dtype != want or not t.is_cuda:
+                raise InvalidArguments(f"{name} must be a CUDA bf16 tensor (or q, k, v all float8_e4m3fn)")
         if o.dtype not in (torch.bfloat16, torch.float32) or not o.is_cuda:
             raise InvalidArguments("o must be a CUDA bf16/fp32 tensor")
         B, Hq, N, D = q.shape
@@ -77,7 +87,9 @@ class AttentionPlan:
         self.work = torch.zeros(2, dtype=torch.int32, device=q.device)
         a.work_counter = self.work.data_ptr()
         a.kv_stages = int(kv_stages)  # the MA `stages` tunable (0 = scheduler default)
-        self.kv_slots = attn_kv_slots(D, kv_stages)
+        a.in_dtype = _lib.NT_DTYPE_E4M3 if e4m3 else _lib.NT_DTYPE_BF16
+        a.q_descale, a.k_descale, a.v_descale = float(q_descale), float(k_descale), float(v_descale)
+        self.kv_slots = attn_kv_slots(64 if e4m3 else D, kv_stages)  # e4m3 K/V tiles are D=64-sized
         self.args = a
         self.shape = (B, Hq, Hkv, N, M, D)
         self._fn = _lib.lib().nt_attn_fwd
