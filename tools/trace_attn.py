@@ -25,6 +25,7 @@ ap.add_argument("--b", type=int, default=1)
 ap.add_argument("--hq", type=int, default=32)
 ap.add_argument("--hkv", type=int, default=8)
 ap.add_argument("--scale", type=float, default=0.0883883)
+ap.add_argument("--e4m3", action="store_true", help="e4m3 Q/K/V (the kind::f8f6f4 variant)")
 a = ap.parse_args()
 L = _lib.lib()
 L.nt_debug_set_trace.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
@@ -34,6 +35,8 @@ q = torch.randn(a.b, a.hq, N, D, device="cuda").bfloat16()
 k = torch.randn(a.b, a.hkv, N, D, device="cuda").bfloat16()
 v = torch.randn(a.b, a.hkv, N, D, device="cuda").bfloat16()
 o = torch.empty(a.b, a.hq, N, D, device="cuda").bfloat16()
+if a.e4m3:
+    q, k, v = (t.float().to(torch.float8_e4m3fn) for t in (q, k, v))
 plan = AttentionPlan(q, k, v, o, a.scale, "causal" if a.causal else "none")
 for _ in range(3):
     plan.launch()
