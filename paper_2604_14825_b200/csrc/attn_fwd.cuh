@@ -134,14 +134,15 @@ __device__ __forceinline__ void attn_rescale_o(uint32_t tO, float alpha) {
   }
 }
 
-// P = exp2(S*sc - m) for one 128-key row -> TMEM at tP (bf16 pairs, or e4m3
-// quads when FP8); returns the row sum of P (fp32, before rounding).
-template <bool FP8>
-__device__ __forceinline__ float attn_exp_pass(const uint32_t (&s)[128], float sc, float m, uint32_t tP) {
+// P = exp2(S*sc - m) for one 128-key row, packed into pk (bf16 pairs, or e4m3
+// quads when FP8: 64 / 32 words) and, when STORE, written to TMEM at tP chunk by
+// chunk; returns the row sum of P (fp32, before rounding).
+template <bool FP8, bool STORE>
+__device__ __forceinline__ float attn_exp_pass(const uint32_t (&s)[128], float sc, float m, uint32_t tP,
+                                               uint32_t (&pk)[64]) {
   const float2 sc2 = make_float2(sc, sc);
   const float2 nm2 = make_float2(-m, -m);
   float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-  uint32_t pk[16];
 #pragma unroll
   for (int ch = 0; ch < 4; ++ch) {
     float2 prev = make_float2(0.f, 0.f);
@@ -157,14 +158,16 @@ __device__ __forceinline__ float attn_exp_pass(const uint32_t (&s)[128], float s
       }
       sum2[i & 1] = fadd2(sum2[i & 1], e);
       if (FP8) {
-        if (i & 1) pk[(ch & 1) * 8 + (i >> 1)] = pack_e4m3x4(prev.x, prev.y, e.x, e.y);
+        if (i & 1) pk[ch * 8 + (i >> 1)] = pack_e4m3x4(prev.x, prev.y, e.x, e.y);
         prev = e;
       } else {
-        pk[i] = NT_PACK_ALU ? pack_bf16_alu(e.x, e.y) : pack_bf16(e.x, e.y);
+        pk[ch * 16 + i] = NT_PACK_ALU ? pack_bf16_alu(e.x, e.y) : pack_bf16(e.x, e.y);
       }
     }
-    if (!FP8) tmem_st16(tP + ch * 16, pk);
-    else if (ch & 1) tmem_st16(tP + (ch >> 1) * 16, pk);  // 64 keys = 16 columns of e4m3 quads
+    if (STORE) {
+      if (!FP8) tmem_st16(tP + ch * 16, pk + ch * 16);
+      else if (ch & 1) tmem_st16(tP + (ch >> 1) * 16, pk + (ch >> 1) * 16);  // 64 keys = 16 e4m3-quad columns
+    }
   }
   return (sum2[0].x + sum2[0].y) + (sum2[1].x + sum2[1].y);
 }
@@ -526,6 +529,57 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     const float sc = (MASK == MASK_TENSOR) ? 1.0f : p.scale_log2;
     uint32_t s_phase = 0u;
     int pv_base = 0;  // SEP_P: PV_t completions of earlier items
+    // deferred epilogue of the previous item (O_t still in TMEM)
+    bool pend = false;
+    int pend_li = 0, pend_row0 = 0, pend_hq = 0, pend_b = 0;
+    float pend_inv = 0.f;
+    auto store_o = [&]() {
+      // O / l from TMEM -> swizzled smem box (one row per lane) -> TMA store of
+      // 32 rows x 32 columns per warp (rows past N are clipped)
+      mbar_wait(&bar_o_full[t], pend_li & 1, p.err, 9);
+      if (t == 0 && wq == 0 && lane == 0 && pend_li < 15) NT_STAMP(3, 48 + pend_li, 6);  // trace: O complete
+      tc_fence_after();
+      const float inv = pend_inv;
+      uint8_t* stg = smem + C::SMEM_O + (warp - 4) * C::OBOX;
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t o[32];
+        tmem_ld32(tO + c * 32, o);
+        tmem_wait_ld();
+        if (lane == 0) bulk_wait_read0();  // this warp's previous box has left shared memory
+        __syncwarp();
+        if (OUT_F32) {
+          // 128-byte rows, 16-byte chunk q at q ^ (row & 7) (SWIZZLE_128B)
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const uint4 v = make_uint4(__float_as_uint(__uint_as_float(o[4 * q]) * inv),
+                                       __float_as_uint(__uint_as_float(o[4 * q + 1]) * inv),
+                                       __float_as_uint(__uint_as_float(o[4 * q + 2]) * inv),
+                                       __float_as_uint(__uint_as_float(o[4 * q + 3]) * inv));
+            *reinterpret_cast<uint4*>(stg + lane * 128 + ((q ^ (lane & 7)) << 4)) = v;
+          }
+        } else {
+          // 64-byte rows, 16-byte chunk q at q ^ ((row >> 1) & 3) (SWIZZLE_64B)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint4 v = make_uint4(pack_bf16(__uint_as_float(o[8 * q]) * inv, __uint_as_float(o[8 * q + 1]) * inv),
+                                       pack_bf16(__uint_as_float(o[8 * q + 2]) * inv, __uint_as_float(o[8 * q + 3]) * inv),
+                                       pack_bf16(__uint_as_float(o[8 * q + 4]) * inv, __uint_as_float(o[8 * q + 5]) * inv),
+                                       pack_bf16(__uint_as_float(o[8 * q + 6]) * inv, __uint_as_float(o[8 * q + 7]) * inv));
+            *reinterpret_cast<uint4*>(stg + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)) = v;
+          }
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_4d(&tmO, stg, c * 32, pend_row0, pend_hq, pend_b);
+          bulk_commit();
+        }
+      }
+      // O_t is read out: the next PV_t (after this warp's next p_full arrival) may overwrite it
+      tc_fence_before();
+      if (t == 0 && wq == 0 && lane == 0 && pend_li < 16) NT_STAMP(3, 32 + pend_li, 7);  // item end (trace)
+    };
     for (int li = 0;; ++li) {
       const int slot_i = li % kItemRing;
       if (t == 0 && wq == 0 && lane == 0 && li < 15) NT_STAMP(3, 48 + li, 4);  // trace: softmax asks for item li
@@ -605,7 +659,25 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           m_run = m_new;
         }
         const float m_use = (m_run == NINF) ? 0.f : m_run;
-        const float sum = attn_exp_pass<FP8>(s, sc, m_use, tP);
+        uint32_t pk[64];
+        float sum;
+        if (j == 0 && pend) {
+          // first tile of an item while the previous item's O is still in TMEM:
+          // exps into registers, then that epilogue (its last PV has had the S load,
+          // max and exps to finish), then P -- PV(0) may overwrite O only after it
+          sum = attn_exp_pass<FP8, false>(s, sc, m_use, tP, pk);
+          store_o();
+          pend = false;
+          if (!FP8) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tmem_st16(tP + c * 16, pk + c * 16);
+          } else {
+            tmem_st16(tP, pk);
+            tmem_st16(tP + 16, pk + 16);
+          }
+        } else {
+          sum = attn_exp_pass<FP8, true>(s, sc, m_use, tP, pk);
+        }
         if (li == NT_TRACE_LI && lane == 0 && wq == 0) NT_STAMP(1 + t, j, 4);
         l_run += sum;
         tmem_wait_st();
@@ -617,57 +689,24 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 
       pv_base += itm.n_kv;
 
-      // ---- epilogue (O_t complete in TMEM)
-      mbar_wait(&bar_o_full[t], li & 1, p.err, 9);
-      if (t == 0 && wq == 0 && lane == 0 && li < 15) NT_STAMP(3, 48 + li, 6);  // trace: O of item li complete
-      tc_fence_after();
+      // ---- epilogue.  D=64 (short items): deferred into the next item's first
+      // tile, where it overlaps the last PV's latency with that tile's S load, max
+      // and exps (BERT 60.3 -> 58.5 us).  D=128: right here -- inside the next
+      // tile it would delay P(0) and the chain behind it (8K 450 -> 461 us).
       const bool valid = qi < p.N;
       if (valid && !(l_run > 0.f) && p.err) atomicOr(p.err, 1);
-      const float inv = (l_run > 0.f) ? p.o_scale / l_run : 0.f;
-      // ---- epilogue: O / l from TMEM -> swizzled smem box (one row per lane) ->
-      // TMA store of 32 rows x 32 columns per warp (rows past N are clipped)
-      uint8_t* stg = smem + C::SMEM_O + (warp - 4) * C::OBOX;
-      const int row0 = itm.q_row0 + t * 128 + wq * 32;
-#pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t o[32];
-        tmem_ld32(tO + c * 32, o);
-        tmem_wait_ld();
-        if (lane == 0) bulk_wait_read0();  // this warp's previous box has left shared memory
-        __syncwarp();
-        if (OUT_F32) {
-          // 128-byte rows, 16-byte chunk q at q ^ (row & 7) (SWIZZLE_128B)
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const uint4 v = make_uint4(__float_as_uint(__uint_as_float(o[4 * q]) * inv),
-                                       __float_as_uint(__uint_as_float(o[4 * q + 1]) * inv),
-                                       __float_as_uint(__uint_as_float(o[4 * q + 2]) * inv),
-                                       __float_as_uint(__uint_as_float(o[4 * q + 3]) * inv));
-            *reinterpret_cast<uint4*>(stg + lane * 128 + ((q ^ (lane & 7)) << 4)) = v;
-          }
-        } else {
-          // 64-byte rows, 16-byte chunk q at q ^ ((row >> 1) & 3) (SWIZZLE_64B)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const uint4 v = make_uint4(pack_bf16(__uint_as_float(o[8 * q]) * inv, __uint_as_float(o[8 * q + 1]) * inv),
-                                       pack_bf16(__uint_as_float(o[8 * q + 2]) * inv, __uint_as_float(o[8 * q + 3]) * inv),
-                                       pack_bf16(__uint_as_float(o[8 * q + 4]) * inv, __uint_as_float(o[8 * q + 5]) * inv),
-                                       pack_bf16(__uint_as_float(o[8 * q + 6]) * inv, __uint_as_float(o[8 * q + 7]) * inv));
-            *reinterpret_cast<uint4*>(stg + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)) = v;
-          }
-        }
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          tma_store_4d(&tmO, stg, c * 32, row0, itm.hq, itm.b);
-          bulk_commit();
-        }
+      pend = true;
+      pend_li = li;
+      pend_inv = (l_run > 0.f) ? p.o_scale / l_run : 0.f;
+      pend_row0 = itm.q_row0 + t * 128 + wq * 32;
+      pend_hq = itm.hq;
+      pend_b = itm.b;
+      if (!C::SEP_P) {
+        store_o();
+        pend = false;
       }
-      // O_t is read out: the next item's first PV_t (issued after this warp's
-      // next p_full arrival) may overwrite it
-      tc_fence_before();
-      if (t == 0 && wq == 0 && lane == 0 && li < 16) NT_STAMP(3, 32 + li, 7);  // item end (trace)
     }
+    if (pend) store_o();
     if (lane == 0) bulk_wait0();  // the last O boxes are written before the CTA exits
   }
 
