@@ -152,8 +152,14 @@ typedef struct nt_gemm_args {
   void* c; int64_t ldc;         /* out */
   int32_t m, n, k;
   int32_t out_dtype;            /* NT_DTYPE_BF16 | NT_DTYPE_F32 */
+  /* split K over CTAs (N <= 128 shapes with few output tiles): fp32 partials in
+   * `workspace` (nt_gemm_workspace_bytes), then one reduce launch.  1 / NULL = off. */
+  int32_t k_splits;
+  void* workspace;
 } nt_gemm_args;
 int nt_gemm(const nt_gemm_args* args, void* stream);
+int32_t nt_gemm_k_splits(int32_t m, int32_t n, int32_t k);
+int64_t nt_gemm_workspace_bytes(int32_t m, int32_t n, int32_t k);
 
 /* Fused chain Y = (X . W1) . W2 with the T tile kept on chip (E <= 256).
  * F is split over CTAs; fp32 partials go to `workspace`

@@ -21,7 +21,7 @@ NT_DTYPE_BF16, NT_DTYPE_F32, NT_DTYPE_E4M3 = 0, 1, 2
 # Every symbol include/nautilus_b200.h declares (checked by tests/test_capi.py).
 EXPORTED = (
     "nt_attn_fwd", "nt_attn_decode", "nt_decode_workspace_bytes", "nt_decode_num_splits", "nt_gemm",
-    "nt_gemm_chain", "nt_gemm_chain_workspace_bytes",
+    "nt_gemm_chain", "nt_gemm_chain_workspace_bytes", "nt_gemm_k_splits", "nt_gemm_workspace_bytes",
     "nt_cast_f32_to_bf16", "nt_cast_bf16_to_f32", "nt_abi_version", "nt_last_error", "nt_launch_count",
     "nt_module_load", "nt_module_function", "nt_launch", "nt_module_unload", "nt_attn_decode_paged",
     "nt_memcpy2d_async",
@@ -66,7 +66,7 @@ class DecodePagedArgs(C.Structure):
 class GemmArgs(C.Structure):
     _fields_ = [("a", C.c_void_p), ("lda", C.c_int64), ("b", C.c_void_p), ("ldb", C.c_int64),
                 ("c", C.c_void_p), ("ldc", C.c_int64), ("m", C.c_int32), ("n", C.c_int32),
-                ("k", C.c_int32), ("out_dtype", C.c_int32)]
+                ("k", C.c_int32), ("out_dtype", C.c_int32), ("k_splits", C.c_int32), ("workspace", C.c_void_p)]
 
 
 class ChainArgs(C.Structure):
@@ -103,6 +103,10 @@ def lib():
             L.nt_gemm_chain.argtypes = [C.POINTER(ChainArgs), C.c_void_p]
             L.nt_gemm_chain_workspace_bytes.argtypes = [C.c_int32] * 3
             L.nt_gemm_chain_workspace_bytes.restype = C.c_int64
+            L.nt_gemm_k_splits.argtypes = [C.c_int32] * 3
+            L.nt_gemm_k_splits.restype = C.c_int32
+            L.nt_gemm_workspace_bytes.argtypes = [C.c_int32] * 3
+            L.nt_gemm_workspace_bytes.restype = C.c_int64
             L.nt_cast_f32_to_bf16.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
             L.nt_cast_bf16_to_f32.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
             L.nt_module_load.argtypes = [C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p)]

@@ -41,6 +41,11 @@ int launch_gemm(const nt_gemm_args* a, cudaStream_t st) {
   p.K = a->k;
   p.tiles_m = (a->m + 127) / 128;
   p.tiles_n = (a->n + BN - 1) / BN;
+  const int k_blocks = (a->k + 63) / 64;
+  p.k_splits = (a->k_splits > 1 && a->workspace) ? std::min(a->k_splits, k_blocks) : 1;
+  p.kb_per = (k_blocks + p.k_splits - 1) / p.k_splits;
+  p.k_splits = (k_blocks + p.kb_per - 1) / p.kb_per;  // no empty K range
+  p.ws = static_cast<float*>(a->workspace);
   p.c = a->c;
   p.ldc = a->ldc;
   auto kern = gemm_kernel<BN, F32>;
@@ -52,11 +57,19 @@ int launch_gemm(const nt_gemm_args* a, cudaStream_t st) {
       return rc;
     configured = true;
   }
-  const int tiles = p.tiles_m * p.tiles_n;
+  const int tiles = p.tiles_m * p.tiles_n * p.k_splits;
   const int grid = std::min(tiles, sm_count());
   kern<<<grid, kGemmThreads, smem, st>>>(ma, mb, p);
   g_launches++;
-  return check_cuda(cudaGetLastError(), "gemm launch");
+  if ((rc = check_cuda(cudaGetLastError(), "gemm launch"))) return rc;
+  if (p.k_splits > 1) {
+    const long long n4 = (long long)a->m * a->n / 4;
+    const int blocks = (int)std::min<long long>((n4 + 255) / 256, 4LL * sm_count());
+    gemm_splitk_reduce<<<blocks, 256, 0, st>>>(p.ws, p.k_splits, a->m, a->n, a->c, a->ldc, F32);
+    g_launches++;
+    rc = check_cuda(cudaGetLastError(), "gemm split-K reduce");
+  }
+  return rc;
 }
 
 template <bool F32>
@@ -167,6 +180,21 @@ extern "C" int nt_gemm(const nt_gemm_args* a, void* stream) {
   if (!one_sm && pair_tiles >= sm_count() / 2)
     return f32 ? launch_gemm2<true>(a, st) : launch_gemm2<false>(a, st);
   return f32 ? launch_gemm<256, true>(a, st) : launch_gemm<256, false>(a, st);
+}
+
+// Split K over CTAs when the output tiles (128 x 128) cannot give every SM work:
+// 4096 x 128 x 4096 has 32 tiles -> 4 K ranges of 1024 (the GEMM-chain's T.W2).
+extern "C" int32_t nt_gemm_k_splits(int32_t m, int32_t n, int32_t k) {
+  if (m <= 0 || n <= 0 || k <= 0 || n > 128 || n % 4) return 1;
+  const int tiles = ((m + 127) / 128) * ((n + 127) / 128);
+  const int k_blocks = (k + 63) / 64;
+  if (tiles >= sm_count() / 2) return 1;
+  return std::max(1, std::min(sm_count() / tiles, k_blocks / 8));  // >= 8 k-blocks per range
+}
+
+extern "C" int64_t nt_gemm_workspace_bytes(int32_t m, int32_t n, int32_t k) {
+  const int s = nt_gemm_k_splits(m, n, k);
+  return s > 1 ? (int64_t)s * m * n * (int64_t)sizeof(float) : 0;
 }
 
 extern "C" int64_t nt_gemm_chain_workspace_bytes(int32_t n, int32_t f, int32_t e) {

@@ -29,6 +29,9 @@ struct GemmParams {
   int M, N, K;
   int tiles_m, tiles_n;
   int group_m;  // CTA-pair kernel: tile rows per raster group
+  int k_splits;  // single-CTA kernel: K ranges per output tile (fp32 partials to ws)
+  int kb_per;    // k-blocks per split
+  float* ws;     // [k_splits][M][N] fp32 partials when k_splits > 1
   void* c;
   long long ldc;
 };
@@ -65,7 +68,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   const int warp = __shfl_sync(0xffffffffu, threadIdx.x / 32, 0);
   const int lane = threadIdx.x & 31;
-  const int num_tiles = p.tiles_m * p.tiles_n;
+  const int out_tiles = p.tiles_m * p.tiles_n;
+  const int num_tiles = out_tiles * p.k_splits;  // (output tile, K range) work units
   const int k_blocks = (p.K + C::BK - 1) / C::BK;
 
   if (warp == 0 && lane == 0) {
@@ -91,8 +95,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (lane == 0) {
       int it = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int mb = tile % p.tiles_m, nb = tile / p.tiles_m;
-        for (int kb = 0; kb < k_blocks; ++kb, ++it) {
+        const int ot = tile % out_tiles, ks = tile / out_tiles;
+        const int mb = ot % p.tiles_m, nb = ot / p.tiles_m;
+        const int kb0 = ks * p.kb_per, kb1 = min(k_blocks, kb0 + p.kb_per);
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % C::STAGES;
           mbar_wait(&empty[s], ((it / C::STAGES) & 1) ^ 1);
           mbar_arrive_expect_tx(&full[s], C::STAGE);
@@ -115,7 +121,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         mbar_wait(&tempty[acc], ((tcount >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * BN;
-        for (int kb = 0; kb < k_blocks; ++kb, ++it) {
+        const int kb0 = (tile / out_tiles) * p.kb_per, kb1 = min(k_blocks, kb0 + p.kb_per);
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % C::STAGES;
           mbar_wait(&full[s], (it / C::STAGES) & 1);
           tc_fence_after();
@@ -125,7 +132,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           for (int k = 0; k < C::BK / 16; ++k) {
             const uint64_t ad = sdesc_sw128(sa + k * 32, 16, 1024);
             const uint64_t bd = sdesc_sw128(sb + k * 2048, C::BK * 128, 1024);
-            umma_ss(d, ad, bd, idesc, (kb | k) ? 1u : 0u);
+            umma_ss(d, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           }
           umma_commit(&empty[s]);
         }
@@ -140,11 +147,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     int tcount = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tcount) {
       const int acc = tcount & 1;
-      const int mb = tile % p.tiles_m, nb = tile / p.tiles_m;
+      const int ot = tile % out_tiles, ks = tile / out_tiles;
+      const int mb = ot % p.tiles_m, nb = ot / p.tiles_m;
       mbar_wait(&tfull[acc], (tcount >> 1) & 1);
       tc_fence_after();
       const int row = mb * 128 + r;
       const bool rv = row < p.M;
+      // split K: fp32 partial rows [ks][row][N] for gemm_splitk_reduce
+      float* const part = p.k_splits > 1 ? p.ws + ((long long)ks * p.M + row) * p.N : nullptr;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t v[32];
@@ -152,8 +162,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         tmem_wait_ld();
         const int col0 = nb * BN + c * 32;
         if (rv && col0 < p.N) {
-          if (OUT_F32) {
-            float* cp = static_cast<float*>(p.c) + (long long)row * p.ldc + col0;
+          if (OUT_F32 || part) {
+            float* cp = part ? part + col0 : static_cast<float*>(p.c) + (long long)row * p.ldc + col0;
 #pragma unroll
             for (int i = 0; i < 8; ++i)
               if (col0 + 4 * i < p.N)
@@ -184,6 +194,30 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+// C = sum over k_splits of the fp32 partials (N % 4 == 0), cast to bf16 / fp32
+__global__ void gemm_splitk_reduce(const float* __restrict__ ws, int splits, int M, int N, void* c, long long ldc,
+                                   bool out_f32) {
+  const long long n4 = (long long)M * N / 4;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+    float4 acc = reinterpret_cast<const float4*>(ws)[i];
+    for (int s = 1; s < splits; ++s) {
+      const float4 v = reinterpret_cast<const float4*>(ws + (long long)s * M * N)[i];
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    const long long e = i * 4;
+    const long long row = e / N, col = e % N;
+    if (out_f32) {
+      *reinterpret_cast<float4*>(static_cast<float*>(c) + row * ldc + col) = acc;
+    } else {
+      *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(c) + row * ldc + col) =
+          make_uint2(pack_bf16(acc.x, acc.y), pack_bf16(acc.z, acc.w));
+    }
   }
 }
 

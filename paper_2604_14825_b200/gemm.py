@@ -56,6 +56,14 @@ class GemmPlan:
         g.c, g.ldc = _mat(c, "C")
         g.m, g.n, g.k = M, N, K
         g.out_dtype = _lib.NT_DTYPE_F32 if c.dtype == torch.float32 else _lib.NT_DTYPE_BF16
+        # split K over CTAs for few-tile shapes (fp32 partials + one reduce launch)
+        L = _lib.lib()
+        g.k_splits = int(L.nt_gemm_k_splits(M, N, K)) if c.is_contiguous() else 1
+        ws = int(L.nt_gemm_workspace_bytes(M, N, K)) if g.k_splits > 1 else 0
+        self.ws = torch.empty(max(ws // 4, 1), dtype=torch.float32, device=a.device) if ws else None
+        g.workspace = self.ws.data_ptr() if ws else None
+        if not ws:
+            g.k_splits = 1
         self.args, self.tensors = g, (a, b, c)
         self._ref = C.byref(g)
         self._fn = _lib.lib().nt_gemm

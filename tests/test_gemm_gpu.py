@@ -117,3 +117,28 @@ def test_cta_pair_gemm_vs_fp64(M, N, K):
     ref = torch.from_numpy(a).double().cuda() @ torch.from_numpy(b).double().cuda()
     err = (c.double() - ref).abs()
     assert float(err.max()) <= 2e-2 and float(err.norm() / ref.norm()) <= 1e-2
+
+
+@pytest.mark.parametrize("M,N,K,f32", [(4096, 128, 4096, False), (4096, 128, 4096, True), (1000, 64, 8192, True),
+                                       (256, 128, 2048, False), (4100, 120, 1000, True)])
+def test_split_k_gemm_vs_fp64(M, N, K, f32):
+    """Few-tile shapes split K over CTAs (fp32 partials + reduce): the chain's T.W2 at E=128."""
+    from paper_2604_14825_b200 import _lib
+    from paper_2604_14825_b200.gemm import GemmPlan
+
+    g = np.random.default_rng(M + 3 * N + K)
+    a = round_bf16(g.standard_normal((M, K)))
+    b = round_bf16(g.standard_normal((K, N)) / np.sqrt(K))
+    ta = torch.from_numpy(a).cuda().bfloat16()
+    tb = torch.from_numpy(b).cuda().bfloat16()
+    c = torch.empty((M, N), dtype=torch.float32 if f32 else torch.bfloat16, device="cuda")
+    plan = GemmPlan(ta, tb, c)
+    expect = int(_lib.lib().nt_gemm_k_splits(M, N, K))
+    assert plan.args.k_splits == expect
+    if (M, N, K) == (4096, 128, 4096):
+        assert expect > 1
+    for _ in range(2):  # the workspace is reused across launches
+        plan.launch()
+    torch.cuda.synchronize()
+    ref = a.astype(np.float64) @ b.astype(np.float64)
+    _check(c.float().cpu().numpy(), ref, max_abs=3e-2 if not f32 else 2e-2)
