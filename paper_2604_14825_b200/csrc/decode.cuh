@@ -125,8 +125,8 @@ __global__ void __launch_bounds__(kDecodeCTAThreads, 1)
     asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
     if (PAGED && warp == 0) {
       // the whole warp stages this split's block-table entries in shared memory
-      // (coalesced, 8 independent loads in flight per lane); lane 0 then issues
-      // the page-gather TMAs.  Entries past kDecodeBtChunk are read from global.
+      // (coalesced, 8 independent loads in flight per lane), then issues the
+      // page-gather TMAs.  Entries past kDecodeBtChunk are read from global.
       const int rows = min(kDecodeTile, p.page_size);
       const int last_page = (seq_len - 1) / p.page_size;
       const int* bt = p.block_table + (long long)b * p.bt_stride;
@@ -146,31 +146,48 @@ __global__ void __launch_bounds__(kDecodeCTAThreads, 1)
         }
       }
       __syncwarp();
-      if (lane == 0) {
-        for (int t = 0; t < ntiles; ++t) {
-          const int slot = t % kDecodeStages;
+      // lane 0 claims the ring slot; small pages (PG 2: 64/rows page slices x K,V
+      // boxes per tile) spread the box issues over one lane each -- from one thread
+      // they serialised (16-token pages 0.70 -> 0.81 of HBM); with 4 boxes per tile
+      // (PG 1) one lane issues all of them (spreading measured 0.853 -> 0.84)
+      const int nsub = kDecodeTile / rows;
+      const int per_sub = (PG == 2) ? 2 : 4;  // 5-D box (both panels) x K,V | 4-D panel x K,V
+      const int jobs = (PG == 2) ? nsub * per_sub : 1;
+      const bool pow2 = (p.page_size & (p.page_size - 1)) == 0;
+      const int ps_log2 = 31 - __clz(p.page_size);
+      for (int t = 0; t < ntiles; ++t) {
+        const int slot = t % kDecodeStages;
+        if (lane == 0) {
           mbar_wait(&empty[slot], ((t / kDecodeStages) & 1) ^ 1, p.err, 11);
           mbar_arrive_expect_tx(&full[slot], 2 * kDecodeTileBytes);
+        }
+        __syncwarp();
+        if (lane < jobs) {
           uint8_t* sk = smem + slot * 2 * kDecodeTileBytes;
           uint8_t* sv = sk + kDecodeTileBytes;
-          const int row = j0 + t * kDecodeTile;
-          for (int sub = 0; sub < kDecodeTile / rows; ++sub) {
-            const int tok = row + sub * rows;
+          if constexpr (PG == 2) {
+            const int sub = lane / per_sub;
+            const int tok = j0 + t * kDecodeTile + sub * rows;
             // tokens past the sequence end read its last page; the consumers mask them
-            const int lp = min(tok / p.page_size, last_page);
+            const int pg = pow2 ? (tok >> ps_log2) : tok / p.page_size;
+            const int in_page = pow2 ? (tok & (p.page_size - 1)) : tok - pg * p.page_size;
+            const int lp = min(pg, last_page);
             const int page = (lp - first < n_pages) ? sbt[lp - first] : __ldg(bt + lp);
-            const int in_page = tok % p.page_size;
-            if constexpr (PG == 2) {
-              // one 5-D box = both 64-dim panels of `rows` tokens: the tile is laid out
-              // [sub][panel][rows][128 B] (see the consumer's address below)
-              tma_load_5d(sk + sub * 2 * rows * 128, &tmK, &full[slot], 0, in_page, 0, hkv, page);
-              tma_load_5d(sv + sub * 2 * rows * 128, &tmV, &full[slot], 0, in_page, 0, hkv, page);
-            } else {
+            const bool is_v = lane & 1;
+            // one 5-D box = both 64-dim panels of `rows` tokens: the tile is laid out
+            // [sub][panel][rows][128 B] (see the consumer's address below)
+            tma_load_5d((is_v ? sv : sk) + sub * 2 * rows * 128, is_v ? &tmV : &tmK, &full[slot], 0, in_page, 0,
+                        hkv, page);
+          } else {
+            const int tok = j0 + t * kDecodeTile;
+            const int pg = pow2 ? (tok >> ps_log2) : tok / p.page_size;
+            const int in_page = pow2 ? (tok & (p.page_size - 1)) : tok - pg * p.page_size;
+            const int lp = min(pg, last_page);
+            const int page = (lp - first < n_pages) ? sbt[lp - first] : __ldg(bt + lp);
 #pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                tma_load_4d(sk + h * kDecodePanel, &tmK, &full[slot], h * 64, in_page, hkv, page);
-                tma_load_4d(sv + h * kDecodePanel, &tmV, &full[slot], h * 64, in_page, hkv, page);
-              }
+            for (int h = 0; h < 2; ++h) {
+              tma_load_4d(sk + h * kDecodePanel, &tmK, &full[slot], h * 64, in_page, hkv, page);
+              tma_load_4d(sv + h * kDecodePanel, &tmV, &full[slot], h * 64, in_page, hkv, page);
             }
           }
         }
@@ -183,12 +200,10 @@ __global__ void __launch_bounds__(kDecodeCTAThreads, 1)
         uint8_t* sk = smem + slot * 2 * kDecodeTileBytes;
         uint8_t* sv = sk + kDecodeTileBytes;
         const int row = j0 + t * kDecodeTile;
-        {
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            tma_load_4d(sk + h * kDecodePanel, &tmK, &full[slot], h * 64, row, hkv, b);
-            tma_load_4d(sv + h * kDecodePanel, &tmV, &full[slot], h * 64, row, hkv, b);
-          }
+        for (int h = 0; h < 2; ++h) {
+          tma_load_4d(sk + h * kDecodePanel, &tmK, &full[slot], h * 64, row, hkv, b);
+          tma_load_4d(sv + h * kDecodePanel, &tmV, &full[slot], h * 64, row, hkv, b);
         }
       }
     }
