@@ -229,43 +229,52 @@ def _attention_streamed(spec: AttentionSpec, inputs: dict, outer, mask_kind, out
     units = B * Hkv
     n = max(1, min(chunks, units))
     bounds = [units * i // n for i in range(n + 1)]
-    pieces = []  # (b, h0, h1) kv-head ranges inside one batch entry
+    # pieces: (chunk, b0, b1, h0, h1) = whole batch entries [b0, b1) (h0, h1 = 0, Hkv:
+    # one copy per tensor and one launch), or a kv-head range inside batch entry b0
+    pieces = []
     for c in range(n):
         u, u1 = bounds[c], bounds[c + 1]
         while u < u1:
             b, h0 = divmod(u, Hkv)
+            if h0 == 0 and u1 - u >= Hkv:
+                nb = (u1 - u) // Hkv
+                pieces.append((c, b, b + nb, 0, Hkv))
+                u += nb * Hkv
+                continue
             h1 = min(Hkv, h0 + (u1 - u))
-            pieces.append((c, b, h0, h1))
+            pieces.append((c, b, b + 1, h0, h1))
             u += h1 - h0
+    work = torch.zeros(2, dtype=torch.int32, device=dev)  # shared: every launch is on `comp`
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(comp)
     flops, launches, plans = 0.0, 0, []
     for c in range(n):
         mine = [p for p in pieces if p[0] == c]
         with torch.cuda.stream(s_in):
-            for _, b, h0, h1 in mine:
-                q_d[b, h0 * g:h1 * g].copy_(q_h[b, h0 * g:h1 * g], non_blocking=True)
-                k_d[b, h0:h1].copy_(k_h[b, h0:h1], non_blocking=True)
-                v_d[b, h0:h1].copy_(v_h[b, h0:h1], non_blocking=True)
+            for _, b0, b1, h0, h1 in mine:
+                q_d[b0:b1, h0 * g:h1 * g].copy_(q_h[b0:b1, h0 * g:h1 * g], non_blocking=True)
+                k_d[b0:b1, h0:h1].copy_(k_h[b0:b1, h0:h1], non_blocking=True)
+                v_d[b0:b1, h0:h1].copy_(v_h[b0:b1, h0:h1], non_blocking=True)
         comp.wait_stream(s_in)
-        for _, b, h0, h1 in mine:
-            qv, kv, vv = q_d[b, h0 * g:h1 * g][None], k_d[b, h0:h1][None], v_d[b, h0:h1][None]
+        for _, b0, b1, h0, h1 in mine:
+            qv, kv, vv = q_d[b0:b1, h0 * g:h1 * g], k_d[b0:b1, h0:h1], v_d[b0:b1, h0:h1]
             if cast:
                 qv, kv, vv = to_bf16(qv), to_bf16(kv), to_bf16(vv)
-            ov = o_d[b, h0 * g:h1 * g][None]
+            ov = o_d[b0:b1, h0 * g:h1 * g]
             rows = g * spec.n
             if decode_eligible(rows, spec.d, kind) and spec.m >= 1024:
                 plan = DecodePlan(qv, kv, vv, ov, spec.scale, err_flag=err)
             else:
-                plan = AttentionPlan(qv, kv, vv, ov, spec.scale, kind, err_flag=err, kv_stages=spec.stages)
+                plan = AttentionPlan(qv, kv, vv, ov, spec.scale, kind, err_flag=err, kv_stages=spec.stages,
+                                     work_counter=work)
             plan.launch(comp)
             plans.append(plan)  # keep argument structs / workspaces alive until the sync
             flops += plan.flops()
             launches += 1
         s_out.wait_stream(comp)
         with torch.cuda.stream(s_out):
-            for _, b, h0, h1 in mine:
-                o_h[b, h0 * g:h1 * g].copy_(o_d[b, h0 * g:h1 * g], non_blocking=True)
+            for _, b0, b1, h0, h1 in mine:
+                o_h[b0:b1, h0 * g:h1 * g].copy_(o_d[b0:b1, h0 * g:h1 * g], non_blocking=True)
     comp.wait_stream(s_out)
     ev1.record(comp)
     ev1.synchronize()

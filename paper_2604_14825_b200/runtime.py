@@ -53,7 +53,8 @@ class AttentionPlan:
     def __init__(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor,
                  scale: Optional[float], mask_kind: str = "none", mask: Optional[torch.Tensor] = None,
                  causal_offset: int = 0, err_flag: Optional[torch.Tensor] = None, kv_stages: int = 0,
-                 q_descale: float = 1.0, k_descale: float = 1.0, v_descale: float = 1.0):
+                 q_descale: float = 1.0, k_descale: float = 1.0, v_descale: float = 1.0,
+                 work_counter: Optional[torch.Tensor] = None):
         q, k, v, o = _as4(q), _as4(k), _as4(v), _as4(o)
         e4m3 = q.dtype == torch.float8_e4m3fn
         want = torch.float8_e4m3fn if e4m3 else torch.bfloat16
@@ -83,8 +84,10 @@ class AttentionPlan:
             a.mask_stride_row = mask.stride(0)
         a.out_dtype = _lib.NT_DTYPE_F32 if o.dtype == torch.float32 else _lib.NT_DTYPE_BF16
         a.err_flag = self.err.data_ptr()
-        # dynamic (greedy LPT) item counter of the persistent kernel; reset on device by the last CTA
-        self.work = torch.zeros(2, dtype=torch.int32, device=q.device)
+        # dynamic (greedy LPT) item counter of the persistent kernel; reset on device by the
+        # last CTA, so plans whose launches are ordered on one stream may share one
+        self.work = work_counter if work_counter is not None else torch.zeros(2, dtype=torch.int32,
+                                                                              device=q.device)
         a.work_counter = self.work.data_ptr()
         a.kv_stages = int(kv_stages)  # the MA `stages` tunable (0 = scheduler default)
         a.in_dtype = _lib.NT_DTYPE_E4M3 if e4m3 else _lib.NT_DTYPE_BF16
