@@ -82,8 +82,14 @@ typedef struct nt_attn_args {
    * k_descale c, O = v_descale P V / l. */
   int32_t in_dtype;
   float q_descale, k_descale, v_descale;
+  /* split KV for few, long work items (e.g. one kv-group per GPU): device memory
+   * of nt_attn_workspace_bytes(args) bytes (0 = never split; NULL or smaller =
+   * run unsplit).  The kernel then writes fp32 partials and a merge kernel follows. */
+  void* workspace;
+  int64_t workspace_bytes;
 } nt_attn_args;
 int nt_attn_fwd(const nt_attn_args* args, void* stream);
+int64_t nt_attn_workspace_bytes(const nt_attn_args* args);
 
 /*
  * K2 split-KV decode attention + combine (flash-decoding) for short query

@@ -20,7 +20,7 @@ NT_DTYPE_BF16, NT_DTYPE_F32, NT_DTYPE_E4M3 = 0, 1, 2
 
 # Every symbol include/nautilus_b200.h declares (checked by tests/test_capi.py).
 EXPORTED = (
-    "nt_attn_fwd", "nt_attn_decode", "nt_decode_workspace_bytes", "nt_decode_num_splits", "nt_gemm",
+    "nt_attn_fwd", "nt_attn_workspace_bytes", "nt_attn_decode", "nt_decode_workspace_bytes", "nt_decode_num_splits", "nt_gemm",
     "nt_gemm_chain", "nt_gemm_chain_workspace_bytes", "nt_gemm_k_splits", "nt_gemm_workspace_bytes",
     "nt_cast_f32_to_bf16", "nt_cast_bf16_to_f32", "nt_abi_version", "nt_last_error", "nt_launch_count",
     "nt_module_load", "nt_module_function", "nt_launch", "nt_module_unload", "nt_attn_decode_paged",
@@ -41,7 +41,8 @@ class AttnArgs(C.Structure):
                 ("mask", C.c_void_p), ("mask_stride_row", C.c_int64),
                 ("out_dtype", C.c_int32), ("err_flag", C.c_void_p), ("work_counter", C.c_void_p),
                 ("kv_stages", C.c_int32), ("in_dtype", C.c_int32), ("q_descale", C.c_float),
-                ("k_descale", C.c_float), ("v_descale", C.c_float)]
+                ("k_descale", C.c_float), ("v_descale", C.c_float), ("workspace", C.c_void_p),
+                ("workspace_bytes", C.c_int64)]
 
 
 class DecodeArgs(C.Structure):
@@ -100,6 +101,8 @@ def lib():
             L.nt_decode_num_splits.argtypes = [C.c_int32] * 4
             L.nt_decode_num_splits.restype = C.c_int
             L.nt_gemm.argtypes = [C.POINTER(GemmArgs), C.c_void_p]
+            L.nt_attn_workspace_bytes.argtypes = [C.POINTER(AttnArgs)]
+            L.nt_attn_workspace_bytes.restype = C.c_int64
             L.nt_gemm_chain.argtypes = [C.POINTER(ChainArgs), C.c_void_p]
             L.nt_gemm_chain_workspace_bytes.argtypes = [C.c_int32] * 3
             L.nt_gemm_chain_workspace_bytes.restype = C.c_int64

@@ -61,7 +61,15 @@ struct AttnFwdParams {
   int* err;  // bit 0: zero denominator (fully masked row); bit 8+k: wait k timed out
   int* work;  // [next, done] dynamic item counter (zero at launch, reset by the last CTA) or null
   float o_scale;  // e4m3 inputs: V's descale (O = o_scale * P.V / l), else 1
+  // Split KV (few, long work items -- e.g. one kv-group per GPU at 8 GPUs): an item
+  // whose KV range exceeds kv_split tiles becomes ceil(n_kv / kv_split) work units;
+  // each writes an fp32 partial (O unnormalised, m, l) that attn_combine_kernel
+  // merges with the repair law.  kv_split = 0: one unit per item (n_items units).
+  int kv_split;
+  int* unit_prefix;  // [n_mblocks + 1] units before each m-block position (written by CTA 0)
+  float2* part_ml;   // [unit][256 rows] (m, l)
 };
+constexpr int kMaxSplitMblocks = 384;  // prefix table size in shared memory
 
 constexpr int kAttnThreads = 384;
 constexpr int kItemRing = 4;  // work-item slots handed from the producer to the MMA / softmax warps
@@ -111,11 +119,12 @@ struct AttnCfg {
   // epilogue staging: per softmax warp one 32-row x 32-column O box (TMA store),
   // 64B-swizzled (bf16) / 128B-swizzled (fp32) so the row-per-thread writes are
   // bank-conflict free
-  static constexpr int OBOX = 32 * 32 * (OUT_F32 ? 4 : 2);
+  static constexpr int OBOX = 32 * 32 * 4;  // fp32-sized: split-KV partials are fp32
   static constexpr int SMEM_O = SMEM_KV + STAGES * TKV;
   static constexpr int SMEM_BAR = SMEM_O + 8 * OBOX;
   static constexpr int NBAR = 4 * QB + 2 * STAGES + 2 + 2 + 2 + 2 + 2 + 2 * kItemRing;
-  static constexpr int SMEM_BYTES = SMEM_BAR + NBAR * 8 + 16 + 4 * kItemRing + 1024;  // + alignment slack
+  static constexpr int SMEM_PREFIX = SMEM_BAR + NBAR * 8 + 16 + 4 * kItemRing;
+  static constexpr int SMEM_BYTES = SMEM_PREFIX + 4 * (kMaxSplitMblocks + 1) + 1024;  // + alignment slack
 };
 
 __device__ __forceinline__ float f_ninf() { return __int_as_float(0xff800000); }
@@ -200,7 +209,21 @@ __device__ unsigned long long* g_nt_cta_times = nullptr;  // [cta][entry, exit, 
 // (largest query block first: LPT over the strided CTA assignment).
 struct AttnItem {
   int b, hq, hkv, q_row0, n_kv;
+  int kv_lo;   // first KV tile of this work unit
+  int unit;    // work-unit index (partial slot when split)
+  bool split;  // the item is split over several units: write an fp32 partial
 };
+
+// KV tiles of m-block mb (causal: up to the diagonal of its last row)
+template <int MASK>
+__device__ __forceinline__ int attn_mb_nkv(const AttnFwdParams& p, int mb) {
+  int n_kv = p.n_kv_total;
+  if (MASK == MASK_CAUSAL) {
+    const int last_q = min(mb * 256 + 255, p.N - 1) + p.causal_offset;
+    n_kv = max(min(n_kv, last_q / 128 + 1), 1);
+  }
+  return n_kv;
+}
 
 template <int MASK>
 __device__ __forceinline__ AttnItem attn_item(const AttnFwdParams& p, int w) {
@@ -213,13 +236,39 @@ __device__ __forceinline__ AttnItem attn_item(const AttnFwdParams& p, int w) {
   it.b = bh / p.Hq;
   it.hkv = it.hq / p.q_per_kv;
   it.q_row0 = mb * 256;
-  int n_kv = p.n_kv_total;
-  if (MASK == MASK_CAUSAL) {
-    const int last_q = min(it.q_row0 + 255, p.N - 1) + p.causal_offset;
-    n_kv = min(n_kv, last_q / 128 + 1);
-    n_kv = max(n_kv, 1);
+  it.n_kv = attn_mb_nkv<MASK>(p, mb);
+  it.kv_lo = 0;
+  it.unit = w;
+  it.split = false;
+  return it;
+}
+
+// Work unit w: items in the same LPT order (heaviest m-blocks first); with
+// kv_split, m-block position i holds ceil(n_kv / kv_split) x B x Hq units
+// (chunk-major), located by a binary search of the prefix table.
+template <int MASK>
+__device__ __forceinline__ AttnItem attn_unit(const AttnFwdParams& p, const int* prefix, int w) {
+  if (p.kv_split == 0) return attn_item<MASK>(p, w);
+  int lo = 0, hi = p.n_mblocks;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (prefix[mid] <= w) lo = mid;
+    else hi = mid;
   }
-  it.n_kv = n_kv;
+  const int BH = p.B * p.Hq;
+  const int r = w - prefix[lo];
+  const int c = r / BH, bh = r - c * BH;
+  const int mb = (MASK == MASK_CAUSAL) ? (p.n_mblocks - 1 - lo) : lo;
+  const int n_full = attn_mb_nkv<MASK>(p, mb);
+  AttnItem it;
+  it.hq = bh % p.Hq;
+  it.b = bh / p.Hq;
+  it.hkv = it.hq / p.q_per_kv;
+  it.q_row0 = mb * 256;
+  it.kv_lo = c * p.kv_split;
+  it.n_kv = min(p.kv_split, n_full - it.kv_lo);
+  it.unit = w;
+  it.split = n_full > p.kv_split;
   return it;
 }
 
@@ -227,7 +276,7 @@ template <int D, int MASK, bool OUT_F32, int KVS, bool FP8 = false>
 __global__ void __launch_bounds__(kAttnThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
-                    const AttnFwdParams p) {
+                    const __grid_constant__ CUtensorMap tmP, const AttnFwdParams p) {
   using C = AttnCfg<D, KVS, OUT_F32, FP8>;
   static_assert(C::SMEM_BYTES <= 227 * 1024, "K1 shared memory exceeds the 227 KB opt-in limit");
   extern __shared__ uint8_t smem_raw[];
@@ -250,6 +299,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   uint64_t* bar_item_empty = bar_item_full + kItemRing;  // [kItemRing] read by MMA + 8 softmax warps
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBAR);
   int* item_ring = reinterpret_cast<int*>(tmem_slot + 4);
+  int* unit_prefix = reinterpret_cast<int*>(smem + C::SMEM_PREFIX);
 
   const int warp = __shfl_sync(0xffffffffu, threadIdx.x / 32, 0);
   const int lane = threadIdx.x & 31;
@@ -264,6 +314,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     prefetch_tmap(&tmK);
     prefetch_tmap(&tmV);
     prefetch_tmap(&tmO);
+    if (p.kv_split > 0) prefetch_tmap(&tmP);
     for (int t = 0; t < 2; ++t) {
       mbar_init(&bar_s_full[t], 1);
       mbar_init(&bar_p_full[t], 4);
@@ -286,6 +337,30 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
+  if (warp == 2 && p.kv_split > 0) {
+    // split-KV unit prefix over m-block positions (warp scan, 32 positions per step)
+    const int BH = p.B * p.Hq;
+    int carry = 0;
+    for (int base = 0; base < p.n_mblocks; base += 32) {
+      const int i = base + lane;
+      int cnt = 0;
+      if (i < p.n_mblocks) {
+        const int mb = (MASK == MASK_CAUSAL) ? (p.n_mblocks - 1 - i) : i;
+        cnt = (attn_mb_nkv<MASK>(p, mb) + p.kv_split - 1) / p.kv_split * BH;
+      }
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, cnt, off);
+        if (lane >= off) cnt += v;
+      }
+      if (i < p.n_mblocks) unit_prefix[i + 1] = carry + cnt;
+      carry += __shfl_sync(0xffffffffu, cnt, 31);
+    }
+    if (lane == 0) unit_prefix[0] = 0;
+    __syncwarp();
+    if (blockIdx.x == 0)
+      for (int i = lane; i <= p.n_mblocks; i += 32) p.unit_prefix[i] = unit_prefix[i];
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -312,7 +387,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           mbar_arrive(&bar_item_full[slot_i]);
           if (li < 15) NT_STAMP(3, 48 + li, 1);  // trace: item li published
           if (w >= p.n_items) break;
-          const AttnItem itm = attn_item<MASK>(p, w);
+          const AttnItem itm = attn_unit<MASK>(p, unit_prefix, w);
           // Q_t of this item may only land once the previous item's last S_t is
           // done; K(0) goes first, into the ring, so it is resident when Q is
           auto load_q = [&]() {
@@ -336,7 +411,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             if (li == NT_TRACE_LI) NT_STAMP(3, it >> 1, (it & 1) * 2 + 1);
             mbar_arrive_expect_tx(&bar_kv_full[slot], C::TKV);
             const CUtensorMap* m = (it & 1) ? &tmV : &tmK;
-            const int row = (it >> 1) * 128;
+            const int row = (itm.kv_lo + (it >> 1)) * 128;
 #pragma unroll
             for (int h = 0; h < C::PANELS; ++h)
               tma_load_4d(sKV + slot * C::TKV + h * C::HALF, m, &bar_kv_full[slot], h * 64, row, itm.hkv, itm.b);
@@ -405,7 +480,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         uint32_t p_phase[2] = {0u, 0u};
         uint32_t sf_phase[2] = {0u, 0u};
         int w = fetch(0);
-        int n_kv = w >= 0 ? attn_item<MASK>(p, w).n_kv : 0;
+        int n_kv = w >= 0 ? attn_unit<MASK>(p, unit_prefix, w).n_kv : 0;
         if (w >= 0) {
           wait_q(0);
           first_s(0, n_kv);
@@ -463,7 +538,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           }
           // ---- tail: PV_t(n_kv-1) -> O complete, interleaved with the next item's S_t(0)
           const int wn = fetch(li + 1);
-          const int n_next = wn >= 0 ? attn_item<MASK>(p, wn).n_kv : 0;
+          const int n_next = wn >= 0 ? attn_unit<MASK>(p, unit_prefix, wn).n_kv : 0;
           const int gV = kv_base + 2 * n_kv - 1;
           const int slotV = gV % C::STAGES;
           const int gKn = kv_base + 2 * n_kv;  // ring index of the next item's K(0)
@@ -533,6 +608,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     bool pend = false;
     int pend_li = 0, pend_row0 = 0, pend_hq = 0, pend_b = 0;
     float pend_inv = 0.f;
+    bool pend_part = false;  // split-KV unit: O goes unnormalised to the fp32 partial map (row pend_row0)
     auto store_o = [&]() {
       // O / l from TMEM -> swizzled smem box (one row per lane) -> TMA store of
       // 32 rows x 32 columns per warp (rows past N are clipped)
@@ -548,7 +624,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         tmem_wait_ld();
         if (lane == 0) bulk_wait_read0();  // this warp's previous box has left shared memory
         __syncwarp();
-        if (OUT_F32) {
+        if (OUT_F32 || pend_part) {
           // 128-byte rows, 16-byte chunk q at q ^ (row & 7) (SWIZZLE_128B)
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
@@ -572,7 +648,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          tma_store_4d(&tmO, stg, c * 32, pend_row0, pend_hq, pend_b);
+          if (pend_part) tma_store_2d(&tmP, stg, c * 32, pend_row0);
+          else tma_store_4d(&tmO, stg, c * 32, pend_row0, pend_hq, pend_b);
           bulk_commit();
         }
       }
@@ -589,7 +666,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_item_empty[slot_i]);
       if (w >= p.n_items) break;
-      const AttnItem itm = attn_item<MASK>(p, w);
+      const AttnItem itm = attn_unit<MASK>(p, unit_prefix, w);
       const int qi = itm.q_row0 + t * 128 + r;
       float m_run = NINF, l_run = 0.f;
       if (t == 0 && wq == 0 && lane == 0 && li < 16) NT_STAMP(3, 32 + li, 6);  // item start (trace)
@@ -610,7 +687,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           if (lane == 0) mbar_arrive(&bar_s_free[t]);
         }
         if (li == NT_TRACE_LI && lane == 0 && wq == 0) NT_STAMP(1 + t, j, 2);
-        const int kv0 = j * 128;
+        const int kv0 = (itm.kv_lo + j) * 128;
         if (MASK == MASK_TENSOR) {
           const float* mrow = p.mask + (long long)min(qi, p.N - 1) * p.mask_row_stride;
 #pragma unroll
@@ -694,11 +771,20 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       // and exps (BERT 60.3 -> 58.5 us).  D=128: right here -- inside the next
       // tile it would delay P(0) and the chain behind it (8K 450 -> 461 us).
       const bool valid = qi < p.N;
-      if (valid && !(l_run > 0.f) && p.err) atomicOr(p.err, 1);
       pend = true;
       pend_li = li;
-      pend_inv = (l_run > 0.f) ? p.o_scale / l_run : 0.f;
-      pend_row0 = itm.q_row0 + t * 128 + wq * 32;
+      pend_part = itm.split;
+      if (itm.split) {
+        // partial of a split item: (m, l) per row now, O unnormalised (store_o);
+        // a KV range can legitimately miss a causal row (l = 0): the combine checks
+        p.part_ml[(long long)itm.unit * 256 + t * 128 + r] = make_float2(m_run, l_run);
+        pend_inv = 1.0f;
+        pend_row0 = itm.unit * 256 + t * 128 + wq * 32;
+      } else {
+        if (valid && !(l_run > 0.f) && p.err) atomicOr(p.err, 1);
+        pend_inv = (l_run > 0.f) ? p.o_scale / l_run : 0.f;
+        pend_row0 = itm.q_row0 + t * 128 + wq * 32;
+      }
       pend_hq = itm.hq;
       pend_b = itm.b;
       if (!C::SEP_P) {
@@ -728,6 +814,61 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       atomicExch(p.work, 0);
       atomicExch(p.work + 1, 0);
     }
+  }
+}
+
+// Split-KV merge: O[row] = o_scale * sum_c w_c O_c[row] / sum_c w_c l_c with
+// w_c = exp2(m_c - max m) (the repair law, tilecc/schedule/repair.py:80-88).
+// Block = 8 rows (one warp per row, D/32 columns per lane) of one (m-block
+// position, batch x head); m-blocks with a single unit exit at once.
+template <int D, int MASK, bool OUT_F32>
+__global__ void __launch_bounds__(256) attn_combine_kernel(const float* __restrict__ part_o, const AttnFwdParams p) {
+  const int mbi = blockIdx.z, bh = blockIdx.y;
+  const int mb = (MASK == MASK_CAUSAL) ? (p.n_mblocks - 1 - mbi) : mbi;
+  const int n_full = attn_mb_nkv<MASK>(p, mb);
+  const int nc = (n_full + p.kv_split - 1) / p.kv_split;
+  if (nc <= 1) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 8 + warp;  // 0..255 within the m-block
+  const int qr = mb * 256 + row;
+  if (qr >= p.N) return;
+  const int BH = p.B * p.Hq;
+  const int u0 = p.unit_prefix[mbi] + bh;
+  float m = f_ninf();
+  for (int c = 0; c < nc; ++c) m = fmaxf(m, p.part_ml[(long long)(u0 + c * BH) * 256 + row].x);
+  constexpr int CPL = D / 32;  // columns per lane
+  float acc[CPL];
+#pragma unroll
+  for (int i = 0; i < CPL; ++i) acc[i] = 0.f;
+  float lsum = 0.f;
+  for (int c = 0; c < nc; ++c) {
+    const long long u = u0 + c * BH;
+    const float2 ml = p.part_ml[u * 256 + row];
+    const float wgt = (ml.x == f_ninf()) ? 0.f : ex2(ml.x - m);
+    lsum += wgt * ml.y;
+    const float* src = part_o + (u * 256 + row) * D + lane * CPL;
+#pragma unroll
+    for (int i = 0; i < CPL; i += 2) {
+      const float2 v = *reinterpret_cast<const float2*>(src + i);
+      acc[i] += wgt * v.x;
+      acc[i + 1] += wgt * v.y;
+    }
+  }
+  if (!(lsum > 0.f)) {
+    if (lane == 0 && p.err) atomicOr(p.err, 1);
+    lsum = 0.f;
+  }
+  const float inv = (lsum > 0.f) ? p.o_scale / lsum : 0.f;
+  const int b = bh / p.Hq, hq = bh % p.Hq;
+  const long long off = (long long)b * p.o_sb + (long long)hq * p.o_sh + (long long)qr * p.o_sn + lane * CPL;
+  if (OUT_F32) {
+    float* dst = static_cast<float*>(p.o) + off;
+#pragma unroll
+    for (int i = 0; i < CPL; i += 2) *reinterpret_cast<float2*>(dst + i) = make_float2(acc[i] * inv, acc[i + 1] * inv);
+  } else {
+    __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.o) + off;
+#pragma unroll
+    for (int i = 0; i < CPL; i += 2) *reinterpret_cast<uint32_t*>(dst + i) = pack_bf16(acc[i] * inv, acc[i + 1] * inv);
   }
 }
 

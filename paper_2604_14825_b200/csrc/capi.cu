@@ -117,68 +117,119 @@ int make_map_pages_5d(CUtensorMap* m, const void* ptr, int64_t page_size, int64_
 }
 
 // ----------------------------------------------------------------- attention
+struct AttnMaps {
+  CUtensorMap q, k, v, o;
+  CUtensorMap p;   // split KV: fp32 partial O [units * 256, D]
+  float* part_o;   // its base
+};
+
+// Split-KV plan (host restatement of attn_unit's prefix): kv_split = 0 unless the
+// heaviest item exceeds 2x the per-SM average of KV-tile steps (few, long items:
+// one kv-group per GPU at 8 GPUs); then items are cut into ~avg/3-tile units.
+// Measured (tools/split_probe.py, Llama 8K causal): Hq=4 131 -> 101 us; Hq=8
+// (1.1x) 135 -> 153-185 us -- each unit reloads Q, stores an fp32 partial and
+// refills the pipeline, so splitting only pays when the heaviest item dominates.
+struct AttnSplit {
+  int kv_split = 0, n_units = 0;
+  int64_t bytes = 0, off_ml = 0, off_o = 0;
+};
+static AttnSplit attn_split_plan(const nt_attn_args* a) {
+  AttnSplit sp;
+  const int nmb = (a->seq_q + 255) / 256, nkv_total = (a->seq_kv + 127) / 128;
+  const long long BH = (long long)a->batch * a->heads_q;
+  sp.n_units = (int)(nmb * BH);
+  if (nmb > kMaxSplitMblocks || a->mask_kind == NT_MASK_TENSOR) return sp;
+  auto nkv = [&](int mb) {
+    if (a->mask_kind != NT_MASK_CAUSAL) return nkv_total;
+    const int last_q = std::min(mb * 256 + 255, a->seq_q - 1) + a->causal_offset;
+    return std::max(std::min(nkv_total, last_q / 128 + 1), 1);
+  };
+  long long total = 0;
+  int mx = 0;
+  for (int mb = 0; mb < nmb; ++mb) {
+    total += nkv(mb) * BH;
+    mx = std::max(mx, nkv(mb));
+  }
+  const double avg = (double)total / num_sms();
+  // experiment overrides: NT_ATTN_SPLIT_THRESH (x avg), NT_ATTN_SPLIT_DIV (avg / div tiles per unit)
+  static const double thresh = getenv("NT_ATTN_SPLIT_THRESH") ? atof(getenv("NT_ATTN_SPLIT_THRESH")) : 2.0;
+  static const double div = getenv("NT_ATTN_SPLIT_DIV") ? atof(getenv("NT_ATTN_SPLIT_DIV")) : 3.0;
+  if (mx <= thresh * avg) return sp;
+  const int S = std::max(4, (int)std::ceil(avg / div));
+  if (S >= mx) return sp;
+  long long units = 0;
+  for (int mb = 0; mb < nmb; ++mb) units += (nkv(mb) + S - 1) / S * BH;
+  sp.kv_split = S;
+  sp.n_units = (int)units;
+  const int64_t prefix_bytes = ((int64_t)(nmb + 1) * 4 + 255) / 256 * 256;
+  sp.off_ml = prefix_bytes;
+  sp.off_o = sp.off_ml + ((int64_t)units * 256 * 8 + 255) / 256 * 256;
+  sp.bytes = sp.off_o + (int64_t)units * 256 * a->head_dim * 4;
+  return sp;
+}
+
 template <int D, int MASK, bool F32, int KVS, bool FP8 = false>
-static int launch_attn(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mo,
-                       const AttnFwdParams& p, cudaStream_t st) {
+static int launch_attn(const AttnMaps& m, const AttnFwdParams& p, cudaStream_t st) {
   auto kern = attn_fwd_kernel<D, MASK, F32, KVS, FP8>;
   const int smem = AttnCfg<D, KVS, F32, FP8>::SMEM_BYTES;
   static bool configured = false;
   if (!configured) {
-    int rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                        "cudaFuncSetAttribute(attn_fwd)");
-    if (rc) return rc;
+    const int rc0 = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+                               "cudaFuncSetAttribute(attn_fwd)");
+    if (rc0) return rc0;
     configured = true;
   }
   // persistent: at most one CTA per SM, each walking items blockIdx.x + k * gridDim.x
   const int grid = std::min(p.n_items, num_sms());
-  kern<<<grid, kAttnThreads, smem, st>>>(mq, mk, mv, mo, p);
+  kern<<<grid, kAttnThreads, smem, st>>>(m.q, m.k, m.v, m.o, m.p, p);
   g_launches++;
-  return check_cuda(cudaGetLastError(), "attn_fwd launch");
+  int rc = check_cuda(cudaGetLastError(), "attn_fwd launch");
+  if (rc || p.kv_split == 0) return rc;
+  // split-KV items: merge the fp32 partials
+  attn_combine_kernel<D, MASK, F32><<<dim3(32, p.B * p.Hq, p.n_mblocks), 256, 0, st>>>(m.part_o, p);
+  g_launches++;
+  return check_cuda(cudaGetLastError(), "attn_combine launch");
 }
 
 template <int D, int MASK, bool F32>
-static int launch_attn_stages(int ma_stages, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
-                              const CUtensorMap& mo, const AttnFwdParams& p, cudaStream_t st) {
+static int launch_attn_stages(int ma_stages, const AttnMaps& m, const AttnFwdParams& p, cudaStream_t st) {
   constexpr int kShallow = attn_kv_slots<D>(1), kDeep = attn_kv_slots<D>(2);
-  return attn_kv_slots<D>(ma_stages) == kShallow ? launch_attn<D, MASK, F32, kShallow>(mq, mk, mv, mo, p, st)
-                                                 : launch_attn<D, MASK, F32, kDeep>(mq, mk, mv, mo, p, st);
+  return attn_kv_slots<D>(ma_stages) == kShallow ? launch_attn<D, MASK, F32, kShallow>(m, p, st)
+                                                 : launch_attn<D, MASK, F32, kDeep>(m, p, st);
 }
 
 // e4m3 Q/K/V (head_dim 128, no / causal mask): 16 KB K/V tiles, ring depth as at D=64
 template <int MASK, bool F32>
-static int launch_attn_e4m3(int ma_stages, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
-                            const CUtensorMap& mo, const AttnFwdParams& p, cudaStream_t st) {
+static int launch_attn_e4m3(int ma_stages, const AttnMaps& m, const AttnFwdParams& p, cudaStream_t st) {
   constexpr int kShallow = attn_kv_slots<64>(1), kDeep = attn_kv_slots<64>(2);
-  return attn_kv_slots<64>(ma_stages) == kShallow ? launch_attn<128, MASK, F32, kShallow, true>(mq, mk, mv, mo, p, st)
-                                                  : launch_attn<128, MASK, F32, kDeep, true>(mq, mk, mv, mo, p, st);
+  return attn_kv_slots<64>(ma_stages) == kShallow ? launch_attn<128, MASK, F32, kShallow, true>(m, p, st)
+                                                  : launch_attn<128, MASK, F32, kDeep, true>(m, p, st);
 }
 
-static int dispatch_attn_e4m3(const nt_attn_args* a, const CUtensorMap& mq, const CUtensorMap& mk,
-                              const CUtensorMap& mv, const CUtensorMap& mo, const AttnFwdParams& p, cudaStream_t st) {
+static int dispatch_attn_e4m3(const nt_attn_args* a, const AttnMaps& m, const AttnFwdParams& p, cudaStream_t st) {
   const bool f32 = a->out_dtype == NT_DTYPE_F32;
   const int sg = a->kv_stages > 0 ? a->kv_stages : 2;
   if (a->mask_kind == NT_MASK_NONE)
-    return f32 ? launch_attn_e4m3<MASK_NONE, true>(sg, mq, mk, mv, mo, p, st)
-               : launch_attn_e4m3<MASK_NONE, false>(sg, mq, mk, mv, mo, p, st);
-  return f32 ? launch_attn_e4m3<MASK_CAUSAL, true>(sg, mq, mk, mv, mo, p, st)
-             : launch_attn_e4m3<MASK_CAUSAL, false>(sg, mq, mk, mv, mo, p, st);
+    return f32 ? launch_attn_e4m3<MASK_NONE, true>(sg, m, p, st)
+               : launch_attn_e4m3<MASK_NONE, false>(sg, m, p, st);
+  return f32 ? launch_attn_e4m3<MASK_CAUSAL, true>(sg, m, p, st)
+             : launch_attn_e4m3<MASK_CAUSAL, false>(sg, m, p, st);
 }
 
 template <int D>
-static int dispatch_attn(const nt_attn_args* a, const CUtensorMap& mq, const CUtensorMap& mk,
-                         const CUtensorMap& mv, const CUtensorMap& mo, const AttnFwdParams& p, cudaStream_t st) {
+static int dispatch_attn(const nt_attn_args* a, const AttnMaps& m, const AttnFwdParams& p, cudaStream_t st) {
   const bool f32 = a->out_dtype == NT_DTYPE_F32;
   const int sg = a->kv_stages > 0 ? a->kv_stages : 2;  // the MA default (VirtualDevice.stage_default)
   switch (a->mask_kind) {
     case NT_MASK_NONE:
-      return f32 ? launch_attn_stages<D, MASK_NONE, true>(sg, mq, mk, mv, mo, p, st)
-                 : launch_attn_stages<D, MASK_NONE, false>(sg, mq, mk, mv, mo, p, st);
+      return f32 ? launch_attn_stages<D, MASK_NONE, true>(sg, m, p, st)
+                 : launch_attn_stages<D, MASK_NONE, false>(sg, m, p, st);
     case NT_MASK_CAUSAL:
-      return f32 ? launch_attn_stages<D, MASK_CAUSAL, true>(sg, mq, mk, mv, mo, p, st)
-                 : launch_attn_stages<D, MASK_CAUSAL, false>(sg, mq, mk, mv, mo, p, st);
+      return f32 ? launch_attn_stages<D, MASK_CAUSAL, true>(sg, m, p, st)
+                 : launch_attn_stages<D, MASK_CAUSAL, false>(sg, m, p, st);
     case NT_MASK_TENSOR:
-      return f32 ? launch_attn_stages<D, MASK_TENSOR, true>(sg, mq, mk, mv, mo, p, st)
-                 : launch_attn_stages<D, MASK_TENSOR, false>(sg, mq, mk, mv, mo, p, st);
+      return f32 ? launch_attn_stages<D, MASK_TENSOR, true>(sg, m, p, st)
+                 : launch_attn_stages<D, MASK_TENSOR, false>(sg, m, p, st);
   }
   return set_error(NT_ERR_INVALID, "unknown mask_kind");
 }
@@ -186,6 +237,11 @@ static int dispatch_attn(const nt_attn_args* a, const CUtensorMap& mq, const CUt
 }  // namespace nt
 
 using namespace nt;
+
+extern "C" int64_t nt_attn_workspace_bytes(const nt_attn_args* a) {
+  if (!a || a->seq_q <= 0 || a->seq_kv <= 0 || a->batch <= 0 || a->heads_q <= 0) return 0;
+  return attn_split_plan(a).bytes;
+}
 
 extern "C" int nt_attn_fwd(const nt_attn_args* a, void* stream) {
   if (!a) return set_error(NT_ERR_INVALID, "null args");
@@ -202,7 +258,8 @@ extern "C" int nt_attn_fwd(const nt_attn_args* a, void* stream) {
     return set_error(NT_ERR_UNSUPPORTED, "e4m3 attention: head_dim 128, no or causal mask");
   const int D = a->head_dim;
   const size_t in_elem = e4m3 ? 1 : 2;
-  CUtensorMap mq, mk, mv;
+  AttnMaps m{};
+  CUtensorMap &mq = m.q, &mk = m.k, &mv = m.v, &mo = m.o;
   int rc;
   if ((rc = make_map_4d(&mq, a->q.ptr, D, a->seq_q, a->heads_q, a->batch, a->q.stride_s, a->q.stride_h,
                         a->q.stride_b, 128, in_elem)))
@@ -219,7 +276,6 @@ extern "C" int nt_attn_fwd(const nt_attn_args* a, void* stream) {
   if (reinterpret_cast<uintptr_t>(a->o.ptr) % 16 || (a->o.stride_s * (f32 ? 4 : 2)) % 16 ||
       (a->o.stride_h * (f32 ? 4 : 2)) % 16 || (a->o.stride_b * (f32 ? 4 : 2)) % 16)
     return set_error(NT_ERR_INVALID, "output must be 16B aligned with 16B-multiple strides");
-  CUtensorMap mo;
   if ((rc = make_map_4d(&mo, a->o.ptr, D, a->seq_q, a->heads_q, a->batch, a->o.stride_s, a->o.stride_h,
                         a->o.stride_b, 32, f32 ? 4 : 2, 32,
                         f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B)))
@@ -248,9 +304,23 @@ extern "C" int nt_attn_fwd(const nt_attn_args* a, void* stream) {
   p.o_sn = a->o.stride_s;
   p.err = a->err_flag;
   p.work = a->work_counter;
+  // split KV when the caller provided the workspace nt_attn_workspace_bytes asks for
+  const AttnSplit sp = attn_split_plan(a);
+  if (sp.kv_split > 0 && a->workspace && a->workspace_bytes >= sp.bytes) {
+    char* ws = static_cast<char*>(a->workspace);
+    p.kv_split = sp.kv_split;
+    p.n_items = sp.n_units;
+    p.unit_prefix = reinterpret_cast<int*>(ws);
+    p.part_ml = reinterpret_cast<float2*>(ws + sp.off_ml);
+    m.part_o = reinterpret_cast<float*>(ws + sp.off_o);
+    if ((rc = make_map_2d(&m.p, m.part_o, D, (int64_t)sp.n_units * 256, D, 32, 32, 4, CU_TENSOR_MAP_SWIZZLE_128B)))
+      return rc;
+  } else {
+    m.p = m.o;  // unused (no split)
+  }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (e4m3) return dispatch_attn_e4m3(a, mq, mk, mv, mo, p, st);
-  return D == 64 ? dispatch_attn<64>(a, mq, mk, mv, mo, p, st) : dispatch_attn<128>(a, mq, mk, mv, mo, p, st);
+  if (e4m3) return dispatch_attn_e4m3(a, m, p, st);
+  return D == 64 ? dispatch_attn<64>(a, m, p, st) : dispatch_attn<128>(a, m, p, st);
 }
 
 // ----------------------------------------------------------------- casts

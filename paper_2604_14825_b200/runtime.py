@@ -92,6 +92,11 @@ class AttentionPlan:
         a.kv_stages = int(kv_stages)  # the MA `stages` tunable (0 = scheduler default)
         a.in_dtype = _lib.NT_DTYPE_E4M3 if e4m3 else _lib.NT_DTYPE_BF16
         a.q_descale, a.k_descale, a.v_descale = float(q_descale), float(k_descale), float(v_descale)
+        # split-KV workspace (non-zero only for few, long work items)
+        ws = int(_lib.lib().nt_attn_workspace_bytes(C.byref(a)))
+        self.ws = torch.empty(ws, dtype=torch.uint8, device=q.device) if ws else None
+        a.workspace = self.ws.data_ptr() if ws else None
+        a.workspace_bytes = ws
         self.kv_slots = attn_kv_slots(64 if e4m3 else D, kv_stages)  # e4m3 K/V tiles are D=64-sized
         self.args = a
         self.shape = (B, Hq, Hkv, N, M, D)

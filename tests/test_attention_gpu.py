@@ -433,3 +433,66 @@ def test_e4m3_rejects_unsupported_shapes():
     plan = AttentionPlan(q, q, q, o, 0.125, "none")
     with pytest.raises(Exception, match="e4m3"):
         plan.launch()
+
+
+# ------------------------------------------------------------ split-KV work units
+@pytest.mark.parametrize("B,Hq,Hkv,N,M,D,causal,out_f32", [
+    (1, 4, 1, 8192, 8192, 128, True, True),      # one kv-group: the per-GPU load at 8 GPUs
+    (1, 2, 2, 4096, 4096, 128, False, False),    # few long non-causal items
+    (1, 2, 1, 3000, 3000, 64, True, True),       # D=64 (deferred epilogue), ragged
+    (2, 1, 1, 2048, 5000, 64, False, False),     # N != M, ragged KV
+])
+def test_split_kv_units_vs_fp64(B, Hq, Hkv, N, M, D, causal, out_f32):
+    """Few, long work items are cut into KV ranges whose fp32 partials are merged (repair law)."""
+    from paper_2604_14825_b200.runtime import AttentionPlan
+
+    scale = 1.0 / np.sqrt(D)
+    q = _rand((B, Hq, N, D), 61)
+    k = _rand((B, Hkv, M, D), 62)
+    v = _rand((B, Hkv, M, D), 63)
+    dev = torch.device("cuda")
+    o = torch.empty((B, Hq, N, D), dtype=torch.float32 if out_f32 else torch.bfloat16, device=dev)
+    plan = AttentionPlan(*(torch.from_numpy(x).to(dev).to(torch.bfloat16) for x in (q, k, v)), o, scale,
+                         "causal" if causal else "none")
+    assert plan.ws is not None, "expected the split-KV path for this shape"
+    plan.launch()
+    torch.cuda.synchronize()
+    plan.check_errors()
+    first = o.clone()
+    plan.launch()  # repeated launches reuse the workspace and reproduce the result bit for bit
+    torch.cuda.synchronize()
+    assert torch.equal(o, first)
+    ref = reference_math.attention_batched_fp64(q, k, v, scale, causal)
+    _check(o.float().cpu().numpy(), ref)
+
+
+def test_split_kv_e4m3():
+    from paper_2604_14825_b200.runtime import AttentionPlan
+
+    B, Hq, Hkv, N, D, scale = 1, 4, 1, 8192, 128, 0.08838834764831845
+    g = np.random.default_rng(64)
+    q8, qd, qf = _quant_e4m3(g.standard_normal((B, Hq, N, D)))
+    k8, kd, kf = _quant_e4m3(g.standard_normal((B, Hkv, N, D)))
+    v8, vd, vf = _quant_e4m3(g.standard_normal((B, Hkv, N, D)))
+    dev = torch.device("cuda")
+    o = torch.empty((B, Hq, N, D), dtype=torch.float32, device=dev)
+    plan = AttentionPlan(q8.to(dev), k8.to(dev), v8.to(dev), o, scale, "causal",
+                         q_descale=qd, k_descale=kd, v_descale=vd)
+    assert plan.ws is not None
+    plan.launch()
+    torch.cuda.synchronize()
+    ref = reference_math.attention_batched_fp64(qf, kf, vf, scale, True)
+    mx, rl = _err(o.cpu().numpy(), ref)
+    assert mx <= E4M3_MAX_ABS and rl <= E4M3_REL_L2, (mx, rl)
+
+
+def test_split_kv_not_used_for_full_grids():
+    """The headline shape (32 heads) balances without splitting: no workspace."""
+    from paper_2604_14825_b200 import _lib
+    from paper_2604_14825_b200.runtime import AttentionPlan
+
+    dev = torch.device("cuda")
+    q = torch.zeros((1, 32, 8192, 128), device=dev, dtype=torch.bfloat16)
+    kv = torch.zeros((1, 8, 8192, 128), device=dev, dtype=torch.bfloat16)
+    plan = AttentionPlan(q, kv, kv, torch.empty_like(q), 0.088, "causal")
+    assert plan.ws is None and int(_lib.lib().nt_attn_workspace_bytes(plan._ref)) == 0
