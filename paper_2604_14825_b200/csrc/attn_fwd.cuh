@@ -834,24 +834,45 @@ __global__ void __launch_bounds__(256) attn_combine_kernel(const float* __restri
   if (qr >= p.N) return;
   const int BH = p.B * p.Hq;
   const int u0 = p.unit_prefix[mbi] + bh;
-  float m = f_ninf();
-  for (int c = 0; c < nc; ++c) m = fmaxf(m, p.part_ml[(long long)(u0 + c * BH) * 256 + row].x);
+  // (m, l) of every chunk in one round trip: lane c holds chunk c (nc <= 32 by construction)
+  float mc = f_ninf(), lc = 0.f;
+  if (lane < nc) {
+    const float2 ml = p.part_ml[(long long)(u0 + lane * BH) * 256 + row];
+    mc = ml.x;
+    lc = ml.y;
+  }
+  float m = mc;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+  const float wgt = (lane < nc && mc != f_ninf()) ? ex2(mc - m) : 0.f;
+  float lsum = wgt * lc;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, off);
   constexpr int CPL = D / 32;  // columns per lane
   float acc[CPL];
 #pragma unroll
   for (int i = 0; i < CPL; ++i) acc[i] = 0.f;
-  float lsum = 0.f;
-  for (int c = 0; c < nc; ++c) {
-    const long long u = u0 + c * BH;
-    const float2 ml = p.part_ml[u * 256 + row];
-    const float wgt = (ml.x == f_ninf()) ? 0.f : ex2(ml.x - m);
-    lsum += wgt * ml.y;
-    const float* src = part_o + (u * 256 + row) * D + lane * CPL;
+  const float* base = part_o + ((long long)u0 * 256 + row) * D + lane * CPL;
+  const long long cstride = (long long)BH * 256 * D;
+  for (int c0 = 0; c0 < nc; c0 += 4) {
+    float v[4][CPL];
 #pragma unroll
-    for (int i = 0; i < CPL; i += 2) {
-      const float2 v = *reinterpret_cast<const float2*>(src + i);
-      acc[i] += wgt * v.x;
-      acc[i + 1] += wgt * v.y;
+    for (int k = 0; k < 4; ++k)  // four chunks' loads in flight before the FMAs
+      if (c0 + k < nc) {
+#pragma unroll
+        for (int i = 0; i < CPL; i += 2) {
+          const float2 x = __ldg(reinterpret_cast<const float2*>(base + (c0 + k) * cstride + i));
+          v[k][i] = x.x;
+          v[k][i + 1] = x.y;
+        }
+      }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float w = __shfl_sync(0xffffffffu, wgt, (c0 + k) & 31);
+      if (c0 + k < nc) {
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) acc[i] += w * v[k][i];
+      }
     }
   }
   if (!(lsum > 0.f)) {

@@ -155,7 +155,8 @@ static AttnSplit attn_split_plan(const nt_attn_args* a) {
   static const double thresh = getenv("NT_ATTN_SPLIT_THRESH") ? atof(getenv("NT_ATTN_SPLIT_THRESH")) : 2.0;
   static const double div = getenv("NT_ATTN_SPLIT_DIV") ? atof(getenv("NT_ATTN_SPLIT_DIV")) : 3.0;
   if (mx <= thresh * avg) return sp;
-  const int S = std::max(4, (int)std::ceil(avg / div));
+  // >= 4 tiles per unit; <= 32 units per item (the combine holds one chunk per lane)
+  const int S = std::max(std::max(4, (int)std::ceil(avg / div)), (mx + 31) / 32);
   if (S >= mx) return sp;
   long long units = 0;
   for (int mb = 0; mb < nmb; ++mb) units += (nkv(mb) + S - 1) / S * BH;
