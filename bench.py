@@ -46,6 +46,10 @@ CONFIGS = {
                            golden="causal2k", scale=LLAMA_SCALE),
     "llama16k_causal": dict(prog="llama_causal", B=1, Hq=32, Hkv=8, N=16384, D=128, causal=True,
                             golden="causal16k", scale=LLAMA_SCALE),
+    # one GPU's share at 8 GPUs (batch x head sharding: one kv-group, 4 q-heads): few,
+    # long causal items -> K1 split-KV work units
+    "llama8k_causal_1group": dict(prog="llama_causal", B=1, Hq=4, Hkv=1, N=8192, D=128, causal=True,
+                                  golden="causal8k", scale=LLAMA_SCALE),
     # the paper's FP8 regime: e4m3 Q/K/V with per-tensor descales, kind::f8f6f4
     "llama8k_causal_e4m3": dict(prog="llama_causal", B=1, Hq=32, Hkv=8, N=8192, D=128, causal=True,
                                 golden="causal8k", scale=LLAMA_SCALE, in_dtype="e4m3"),
