@@ -72,6 +72,9 @@ struct AttnFwdParams {
 constexpr int kMaxSplitMblocks = 384;  // prefix table size in shared memory
 
 constexpr int kAttnThreads = 384;
+#ifndef NT_REG_LO64
+#define NT_REG_LO64 104  // D=64 register split (88 / 96 / 104 -> softmax 208 / 204 / 200)
+#endif
 constexpr int kItemRing = 4;  // work-item slots handed from the producer to the MMA / softmax warps
 constexpr float kRescaleLog2 = 8.0f;
 // Fraction of exp2 evaluated by the FMA-pipe polynomial instead of MUFU.EX2
@@ -246,9 +249,9 @@ __device__ __forceinline__ AttnItem attn_item(const AttnFwdParams& p, int w) {
 // Work unit w: items in the same LPT order (heaviest m-blocks first); with
 // kv_split, m-block position i holds ceil(n_kv / kv_split) x B x Hq units
 // (chunk-major), located by a binary search of the prefix table.
-template <int MASK>
+template <int MASK, bool SPLIT>
 __device__ __forceinline__ AttnItem attn_unit(const AttnFwdParams& p, const int* prefix, int w) {
-  if (p.kv_split == 0) return attn_item<MASK>(p, w);
+  if (!SPLIT) return attn_item<MASK>(p, w);
   int lo = 0, hi = p.n_mblocks;
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
@@ -272,12 +275,15 @@ __device__ __forceinline__ AttnItem attn_unit(const AttnFwdParams& p, const int*
   return it;
 }
 
-template <int D, int MASK, bool OUT_F32, int KVS, bool FP8 = false>
+template <int D, int MASK, bool OUT_F32, int KVS, bool FP8 = false, bool SPLIT = false>
 __global__ void __launch_bounds__(kAttnThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
                     const __grid_constant__ CUtensorMap tmP, const AttnFwdParams p) {
   using C = AttnCfg<D, KVS, OUT_F32, FP8>;
+  // register split between warpgroup 0 (producer / MMA issuer) and the softmax
+  // warpgroups: 128 x lo + 256 x hi = 384 x 168
+  constexpr int kRegSplitLo = (D == 64) ? NT_REG_LO64 : 104;
   static_assert(C::SMEM_BYTES <= 227 * 1024, "K1 shared memory exceeds the 227 KB opt-in limit");
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_u32 = smem_u32(smem_raw);
@@ -314,7 +320,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     prefetch_tmap(&tmK);
     prefetch_tmap(&tmV);
     prefetch_tmap(&tmO);
-    if (p.kv_split > 0) prefetch_tmap(&tmP);
+    if (SPLIT) prefetch_tmap(&tmP);
     for (int t = 0; t < 2; ++t) {
       mbar_init(&bar_s_full[t], 1);
       mbar_init(&bar_p_full[t], 4);
@@ -337,7 +343,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
-  if (warp == 2 && p.kv_split > 0) {
+  if (SPLIT && warp == 2) {
     // split-KV unit prefix over m-block positions (warp scan, 32 positions per step)
     const int BH = p.B * p.Hq;
     int carry = 0;
@@ -369,7 +375,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   if (warp < 4) {
     // setmaxnreg only redistributes the launch allocation (384 x 168 = 64512
     // registers): 128 x 104 + 256 x 200 = 64512
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 104;");
+    if constexpr (kRegSplitLo == 104) asm volatile("setmaxnreg.dec.sync.aligned.u32 104;");
+    else if constexpr (kRegSplitLo == 96) asm volatile("setmaxnreg.dec.sync.aligned.u32 96;");
+    else asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
     if (warp == 0) {
       // ================= TMA producer
       if (lane == 0) {
@@ -387,7 +395,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           mbar_arrive(&bar_item_full[slot_i]);
           if (li < 15) NT_STAMP(3, 48 + li, 1);  // trace: item li published
           if (w >= p.n_items) break;
-          const AttnItem itm = attn_unit<MASK>(p, unit_prefix, w);
+          const AttnItem itm = attn_unit<MASK, SPLIT>(p, unit_prefix, w);
           // Q_t of this item may only land once the previous item's last S_t is
           // done; K(0) goes first, into the ring, so it is resident when Q is
           auto load_q = [&]() {
@@ -480,7 +488,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         uint32_t p_phase[2] = {0u, 0u};
         uint32_t sf_phase[2] = {0u, 0u};
         int w = fetch(0);
-        int n_kv = w >= 0 ? attn_unit<MASK>(p, unit_prefix, w).n_kv : 0;
+        int n_kv = w >= 0 ? attn_unit<MASK, SPLIT>(p, unit_prefix, w).n_kv : 0;
         if (w >= 0) {
           wait_q(0);
           first_s(0, n_kv);
@@ -538,7 +546,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           }
           // ---- tail: PV_t(n_kv-1) -> O complete, interleaved with the next item's S_t(0)
           const int wn = fetch(li + 1);
-          const int n_next = wn >= 0 ? attn_unit<MASK>(p, unit_prefix, wn).n_kv : 0;
+          const int n_next = wn >= 0 ? attn_unit<MASK, SPLIT>(p, unit_prefix, wn).n_kv : 0;
           const int gV = kv_base + 2 * n_kv - 1;
           const int slotV = gV % C::STAGES;
           const int gKn = kv_base + 2 * n_kv;  // ring index of the next item's K(0)
@@ -591,7 +599,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       }
     }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 200;");
+    if constexpr (kRegSplitLo == 104) asm volatile("setmaxnreg.inc.sync.aligned.u32 200;");
+    else if constexpr (kRegSplitLo == 96) asm volatile("setmaxnreg.inc.sync.aligned.u32 204;");
+    else asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
     // ================= softmax (+ lazy O correction + epilogue), one thread per query row
     const int t = (warp - 4) / 4;
     const int wq = warp & 3;  // TMEM sub-partition this warp may access
@@ -624,7 +634,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         tmem_wait_ld();
         if (lane == 0) bulk_wait_read0();  // this warp's previous box has left shared memory
         __syncwarp();
-        if (OUT_F32 || pend_part) {
+        if (OUT_F32 || (SPLIT && pend_part)) {
           // 128-byte rows, 16-byte chunk q at q ^ (row & 7) (SWIZZLE_128B)
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
@@ -648,7 +658,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          if (pend_part) tma_store_2d(&tmP, stg, c * 32, pend_row0);
+          if (SPLIT && pend_part) tma_store_2d(&tmP, stg, c * 32, pend_row0);
           else tma_store_4d(&tmO, stg, c * 32, pend_row0, pend_hq, pend_b);
           bulk_commit();
         }
@@ -666,7 +676,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_item_empty[slot_i]);
       if (w >= p.n_items) break;
-      const AttnItem itm = attn_unit<MASK>(p, unit_prefix, w);
+      const AttnItem itm = attn_unit<MASK, SPLIT>(p, unit_prefix, w);
       const int qi = itm.q_row0 + t * 128 + r;
       float m_run = NINF, l_run = 0.f;
       if (t == 0 && wq == 0 && lane == 0 && li < 16) NT_STAMP(3, 32 + li, 6);  // item start (trace)
@@ -773,8 +783,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       const bool valid = qi < p.N;
       pend = true;
       pend_li = li;
-      pend_part = itm.split;
-      if (itm.split) {
+      pend_part = SPLIT && itm.split;
+      if (SPLIT && itm.split) {
         // partial of a split item: (m, l) per row now, O unnormalised (store_o);
         // a KV range can legitimately miss a causal row (l = 0): the combine checks
         p.part_ml[(long long)itm.unit * 256 + t * 128 + r] = make_float2(m_run, l_run);
