@@ -11,12 +11,20 @@ for c in llama8k_causal llama2k_causal llama16k_causal llama8k_causal_1group lla
 done
 timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/round/bench_reference.json.log 2>&1; echo ref=$?
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/round/launches_llama8k.csv python bench.py --steps 5 --warmup 3 --no-cpu-baseline > /dev/null 2>&1; echo launches=$?
-cap() { timeout 600 ncu --set full --clock-control none --import-source on -k regex:$2 -s $3 -c 1 -o gpurun_out/round/$1 python bench.py --config $4 --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/round/ncu_$1.log 2>&1; echo ncu_$1=$?; }
-cap attn_llama8k attn_fwd 3 llama8k_causal
-cap attn_bert512 attn_fwd 3 bert512
-cap decode32k decode_split 3 decode32k
-cap decode32k_paged16 decode_split 3 decode32k_paged16
-cap gemm4k gemm2_kernel 6 gemm_chain_e4096
-cap attn_llama8k_e4m3 attn_fwd 3 llama8k_causal_e4m3
-cap gemm_e128 gemm_kernel 3 gemm_chain_e128
+# cap NAME KERNEL_REGEX SKIP CONFIG [summary args]: one --set full capture, summarised on
+# the box (tools/ncu_summary.py); only the headline report is kept (gpurun_out <= 64 MiB)
+cap() {
+  name=$1; k=$2; skip=$3; cfg=$4; shift 4
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s $skip -c 1 -o gpurun_out/round/$name python bench.py --config $cfg --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/round/ncu_$name.log 2>&1; echo ncu_$name=$?
+  python tools/ncu_summary.py gpurun_out/round/$name.ncu-rep gpurun_out/round/${name}_ncu.json --workload $cfg "$@" > /dev/null 2>&1
+  [ "$name" = attn_llama8k ] || rm -f gpurun_out/round/$name.ncu-rep
+}
+cap attn_llama8k attn_fwd 3 llama8k_causal --algorithmic-bytes 167772160 --algorithmic-flops 549822922752
+cap attn_bert512 attn_fwd 3 bert512 --algorithmic-bytes 100663296 --algorithmic-flops 25769803776
+cap decode32k decode_split 3 decode32k --algorithmic-bytes 8590983168
+cap decode32k_paged16 decode_split 3 decode32k_paged16 --algorithmic-bytes 8590983168
+cap gemm4k gemm2_kernel 6 gemm_chain_e4096 --algorithmic-flops 137438953472
+cap attn_llama8k_e4m3 attn_fwd 3 llama8k_causal_e4m3 --algorithmic-bytes 117440512 --algorithmic-flops 549822922752
+cap gemm_e128 gemm_kernel 3 gemm_chain_e128 --algorithmic-flops 4294967296
+cap attn_1group attn_fwd 3 llama8k_causal_1group --algorithmic-flops 68727865344
 ls -la gpurun_out/round | head -40
