@@ -114,11 +114,13 @@ extern "C" int nt_attn_decode(const nt_decode_args* a, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   CUtensorMap mk, mv;
   int rc;
-  if ((rc = make_map_4d(&mk, a->k.ptr, kDecodeD, a->seq_kv, a->heads_kv, a->batch, a->k.stride_s, a->k.stride_h,
-                        a->k.stride_b, kDecodeTile, 2)))
+  // one 5-D box {64 dims, 64 keys, 2 panels} per K or V tile (a batch entry is a "page"
+  // of seq_kv tokens): both 64-dim panels in one TMA, laid out [panel][64 keys][128 B]
+  if ((rc = make_map_pages_5d(&mk, a->k.ptr, a->seq_kv, a->heads_kv, a->batch, a->k.stride_s, a->k.stride_h,
+                              a->k.stride_b, kDecodeTile)))
     return rc;
-  if ((rc = make_map_4d(&mv, a->v.ptr, kDecodeD, a->seq_kv, a->heads_kv, a->batch, a->v.stride_s, a->v.stride_h,
-                        a->v.stride_b, kDecodeTile, 2)))
+  if ((rc = make_map_pages_5d(&mv, a->v.ptr, a->seq_kv, a->heads_kv, a->batch, a->v.stride_s, a->v.stride_h,
+                              a->v.stride_b, kDecodeTile)))
     return rc;
   return dispatch<0>(R, mk, mv, p, st);
 }

@@ -200,11 +200,8 @@ __global__ void __launch_bounds__(kDecodeCTAThreads, 1)
         uint8_t* sk = smem + slot * 2 * kDecodeTileBytes;
         uint8_t* sv = sk + kDecodeTileBytes;
         const int row = j0 + t * kDecodeTile;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          tma_load_4d(sk + h * kDecodePanel, &tmK, &full[slot], h * 64, row, hkv, b);
-          tma_load_4d(sv + h * kDecodePanel, &tmV, &full[slot], h * 64, row, hkv, b);
-        }
+        tma_load_5d(sk, &tmK, &full[slot], 0, row, 0, hkv, b);  // both panels of 64 keys
+        tma_load_5d(sv, &tmV, &full[slot], 0, row, 0, hkv, b);
       }
     }
   } else {
