@@ -25,6 +25,12 @@
 
 namespace nt {
 
+// K3's waits suspend instead of re-polling (A/B: GEMM +1.5 %, attention -0.5 % -> K3 only)
+#ifndef NT_GEMM_WAIT_HINT
+#define NT_GEMM_WAIT_HINT 1
+#endif
+constexpr bool kGemmWaitHint = NT_GEMM_WAIT_HINT != 0;
+
 struct GemmParams {
   int M, N, K;
   int tiles_m, tiles_n;
@@ -100,7 +106,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int kb0 = ks * p.kb_per, kb1 = min(k_blocks, kb0 + p.kb_per);
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % C::STAGES;
-          mbar_wait(&empty[s], ((it / C::STAGES) & 1) ^ 1);
+          mbar_wait<kGemmWaitHint>(&empty[s], ((it / C::STAGES) & 1) ^ 1);
           mbar_arrive_expect_tx(&full[s], C::STAGE);
           uint8_t* sa = smem + s * C::STAGE;
           uint8_t* sb = sa + C::A_BYTES;
@@ -118,13 +124,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       int it = 0, tcount = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tcount) {
         const int acc = tcount & 1;
-        mbar_wait(&tempty[acc], ((tcount >> 1) & 1) ^ 1);
+        mbar_wait<kGemmWaitHint>(&tempty[acc], ((tcount >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * BN;
         const int kb0 = (tile / out_tiles) * p.kb_per, kb1 = min(k_blocks, kb0 + p.kb_per);
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % C::STAGES;
-          mbar_wait(&full[s], (it / C::STAGES) & 1);
+          mbar_wait<kGemmWaitHint>(&full[s], (it / C::STAGES) & 1);
           tc_fence_after();
           const uint32_t sa = sbase + s * C::STAGE;
           const uint32_t sb = sa + C::A_BYTES;
@@ -149,7 +155,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int acc = tcount & 1;
       const int ot = tile % out_tiles, ks = tile / out_tiles;
       const int mb = ot % p.tiles_m, nb = ot / p.tiles_m;
-      mbar_wait(&tfull[acc], (tcount >> 1) & 1);
+      mbar_wait<kGemmWaitHint>(&tfull[acc], (tcount >> 1) & 1);
       tc_fence_after();
       const int row = mb * 128 + r;
       const bool rv = row < p.M;
@@ -316,7 +322,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         gemm_tile_coords(p, tile, mb, nb);
         for (int kb = 0; kb < k_blocks; ++kb, ++it) {
           const int s = it % C::STAGES;
-          mbar_wait(&empty[s], ((it / C::STAGES) & 1) ^ 1);
+          mbar_wait<kGemmWaitHint>(&empty[s], ((it / C::STAGES) & 1) ^ 1);
           if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * C::STAGE);
           uint8_t* sa = smem + s * C::STAGE;
           uint8_t* sb = sa + C::A_BYTES;
@@ -335,12 +341,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       int it = 0, tcount = 0;
       for (int tile = pair; tile < num_tiles; tile += npairs, ++tcount) {
         const int acc = tcount & 1;
-        mbar_wait(&tempty[acc], ((tcount >> 1) & 1) ^ 1);
+        mbar_wait<kGemmWaitHint>(&tempty[acc], ((tcount >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * 256;
         for (int kb = 0; kb < k_blocks; ++kb, ++it) {
           const int s = it % C::STAGES;
-          mbar_wait(&full[s], (it / C::STAGES) & 1);
+          mbar_wait<kGemmWaitHint>(&full[s], (it / C::STAGES) & 1);
           tc_fence_after();
           const uint32_t sa = sbase + s * C::STAGE;
           const uint32_t sb = sa + C::A_BYTES;
@@ -364,7 +370,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const int acc = tcount & 1;
       int mb, nb;
       gemm_tile_coords(p, tile, mb, nb);
-      mbar_wait(&tfull[acc], (tcount >> 1) & 1);
+      mbar_wait<kGemmWaitHint>(&tfull[acc], (tcount >> 1) & 1);
       tc_fence_after();
       // TMEM -> registers -> swizzled smem box -> TMA store (edges clipped by TMA)
       uint8_t* stg = smem + C::SMEM_O + (warp - 2) * C::OBOX;

@@ -44,9 +44,10 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 #ifndef NT_WAIT_HINT
 #define NT_WAIT_HINT 0
 #endif
+template <bool HINT = (NT_WAIT_HINT != 0)>
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
-  if (NT_WAIT_HINT) {
+  if (HINT) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
@@ -71,14 +72,15 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
 #ifndef NT_WAIT_TIMEOUT_NS
 #define NT_WAIT_TIMEOUT_NS 4000000000ull
 #endif
+template <bool HINT = (NT_WAIT_HINT != 0)>
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, int* err = nullptr,
                                           int code = 0) {
-  if (mbar_try_wait(bar, parity)) return;
+  if (mbar_try_wait<HINT>(bar, parity)) return;
   uint64_t t0 = globaltimer();
   while (true) {
 #pragma unroll 1
     for (int i = 0; i < 64; ++i)
-      if (mbar_try_wait(bar, parity)) return;
+      if (mbar_try_wait<HINT>(bar, parity)) return;
     if (globaltimer() - t0 > NT_WAIT_TIMEOUT_NS) {
       if (err) atomicOr(err, 1 << (8 + (code & 15)));  // bit 8 + code: which wait timed out
       __threadfence_system();
