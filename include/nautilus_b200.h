@@ -28,7 +28,9 @@
 extern "C" {
 #endif
 
-#define NT_ABI_VERSION 1
+/* 2: workspace_bytes in the decode / gemm / chain argument structs (the library
+ *    rejects a workspace smaller than the launch needs instead of writing past it) */
+#define NT_ABI_VERSION 2
 
 /* status codes (mapped by the host onto tilecc.errors CompilerError subclasses) */
 #define NT_OK 0
@@ -107,6 +109,7 @@ typedef struct nt_decode_args {
   int32_t out_dtype;
   void* workspace;
   int32_t* err_flag;
+  int64_t workspace_bytes; /* size of `workspace`; < nt_decode_workspace_bytes(...) -> NT_ERR_INVALID */
 } nt_decode_args;
 /* rows_per_group = (heads_q / heads_kv) * seq_q; workspace = fp32 (O, m, l) per split */
 int64_t nt_decode_workspace_bytes(int32_t batch, int32_t heads_kv, int32_t rows_per_group, int32_t head_dim,
@@ -142,6 +145,7 @@ typedef struct nt_decode_paged_args {
   int32_t out_dtype;
   void* workspace;
   int32_t* err_flag;
+  int64_t workspace_bytes; /* size of `workspace`; too small -> NT_ERR_INVALID */
 } nt_decode_paged_args;
 int nt_attn_decode_paged(const nt_decode_paged_args* args, void* stream);
 
@@ -162,6 +166,7 @@ typedef struct nt_gemm_args {
    * `workspace` (nt_gemm_workspace_bytes), then one reduce launch.  1 / NULL = off. */
   int32_t k_splits;
   void* workspace;
+  int64_t workspace_bytes; /* size of `workspace`; k_splits is clamped to what it holds */
 } nt_gemm_args;
 int nt_gemm(const nt_gemm_args* args, void* stream);
 int32_t nt_gemm_k_splits(int32_t m, int32_t n, int32_t k);
@@ -178,6 +183,7 @@ typedef struct nt_chain_args {
   int32_t n, k, f, e;
   int32_t out_dtype;
   void* workspace;
+  int64_t workspace_bytes; /* size of `workspace`; too small -> NT_ERR_INVALID */
 } nt_chain_args;
 int64_t nt_gemm_chain_workspace_bytes(int32_t n, int32_t f, int32_t e);
 int nt_gemm_chain(const nt_chain_args* args, void* stream);

@@ -50,7 +50,7 @@ class DecodeArgs(C.Structure):
                 ("batch", C.c_int32), ("heads_q", C.c_int32), ("heads_kv", C.c_int32),
                 ("seq_q", C.c_int32), ("seq_kv", C.c_int32), ("head_dim", C.c_int32),
                 ("scale", C.c_float), ("num_splits", C.c_int32), ("out_dtype", C.c_int32),
-                ("workspace", C.c_void_p), ("err_flag", C.c_void_p)]
+                ("workspace", C.c_void_p), ("err_flag", C.c_void_p), ("workspace_bytes", C.c_int64)]
 
 
 class DecodePagedArgs(C.Structure):
@@ -61,20 +61,21 @@ class DecodePagedArgs(C.Structure):
                 ("batch", C.c_int32), ("heads_q", C.c_int32), ("heads_kv", C.c_int32),
                 ("seq_q", C.c_int32), ("max_seq_kv", C.c_int32), ("head_dim", C.c_int32),
                 ("scale", C.c_float), ("num_splits", C.c_int32), ("out_dtype", C.c_int32),
-                ("workspace", C.c_void_p), ("err_flag", C.c_void_p)]
+                ("workspace", C.c_void_p), ("err_flag", C.c_void_p), ("workspace_bytes", C.c_int64)]
 
 
 class GemmArgs(C.Structure):
     _fields_ = [("a", C.c_void_p), ("lda", C.c_int64), ("b", C.c_void_p), ("ldb", C.c_int64),
                 ("c", C.c_void_p), ("ldc", C.c_int64), ("m", C.c_int32), ("n", C.c_int32),
-                ("k", C.c_int32), ("out_dtype", C.c_int32), ("k_splits", C.c_int32), ("workspace", C.c_void_p)]
+                ("k", C.c_int32), ("out_dtype", C.c_int32), ("k_splits", C.c_int32), ("workspace", C.c_void_p),
+                ("workspace_bytes", C.c_int64)]
 
 
 class ChainArgs(C.Structure):
     _fields_ = [("x", C.c_void_p), ("ldx", C.c_int64), ("w1", C.c_void_p), ("ldw1", C.c_int64),
                 ("w2", C.c_void_p), ("ldw2", C.c_int64), ("y", C.c_void_p), ("ldy", C.c_int64),
                 ("n", C.c_int32), ("k", C.c_int32), ("f", C.c_int32), ("e", C.c_int32),
-                ("out_dtype", C.c_int32), ("workspace", C.c_void_p)]
+                ("out_dtype", C.c_int32), ("workspace", C.c_void_p), ("workspace_bytes", C.c_int64)]
 
 
 _lib = None

@@ -171,15 +171,9 @@ static AttnSplit attn_split_plan(const nt_attn_args* a) {
 
 template <int D, int MASK, bool F32, int KVS, bool FP8, bool SPLIT>
 static int launch_attn_kernel(const AttnMaps& m, const AttnFwdParams& p, cudaStream_t st) {
-  auto kern = attn_fwd_kernel<D, MASK, F32, KVS, FP8, SPLIT>;
+  constexpr auto kern = attn_fwd_kernel<D, MASK, F32, KVS, FP8, SPLIT>;
   const int smem = AttnCfg<D, KVS, F32, FP8>::SMEM_BYTES;
-  static bool configured = false;
-  if (!configured) {
-    const int rc0 = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                               "cudaFuncSetAttribute(attn_fwd)");
-    if (rc0) return rc0;
-    configured = true;
-  }
+  if (const int rc0 = configure_smem<kern>(smem, "cudaFuncSetAttribute(attn_fwd)")) return rc0;
   // persistent: at most one CTA per SM, each walking items blockIdx.x + k * gridDim.x
   const int grid = std::min(p.n_items, num_sms());
   kern<<<grid, kAttnThreads, smem, st>>>(m.q, m.k, m.v, m.o, m.p, p);

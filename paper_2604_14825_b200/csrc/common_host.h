@@ -19,4 +19,20 @@ int make_map_pages_5d(CUtensorMap* m, const void* ptr, int64_t page_size, int64_
                       int64_t token_stride, int64_t head_stride, int64_t page_stride, int rows);
 int make_map_2d(CUtensorMap* m, const void* ptr, int64_t inner, int64_t outer, int64_t ld, int box_inner,
                 int box_outer, size_t elem, CUtensorMapSwizzle swz);
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device):
+// the attribute lives in the device's context, so a process that launches on
+// several GPUs must set it on each.  Keyed by the kernel's address (one static
+// per instantiation), a bit per device ordinal.
+template <auto Kern>
+int configure_smem(int smem, const char* what) {
+  static std::atomic<uint64_t> done{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return 0;
+  const int rc = check_cuda(cudaFuncSetAttribute(Kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), what);
+  if (rc == 0) done.fetch_or(bit, std::memory_order_acq_rel);
+  return rc;
+}
 }  // namespace nt

@@ -47,14 +47,8 @@ int choose_splits(int groups, int M, int requested) {
 template <int R, int PG>
 int launch(const CUtensorMap& mk, const CUtensorMap& mv, DecodeParams& p, cudaStream_t st) {
   int rc;
-  auto kern = decode_split_kernel<R, PG>;
-  static bool configured = false;
-  if (!configured) {
-    if ((rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kDecodeSmem),
-                         "cudaFuncSetAttribute(decode)")))
-      return rc;
-    configured = true;
-  }
+  constexpr auto kern = decode_split_kernel<R, PG>;
+  if ((rc = configure_smem<kern>(kDecodeSmem, "cudaFuncSetAttribute(decode)"))) return rc;
   dim3 grid(p.splits, p.B * p.Hkv);
   kern<<<grid, kDecodeCTAThreads, kDecodeSmem, st>>>(mk, mv, p);
   g_launches++;
@@ -88,7 +82,9 @@ extern "C" int nt_attn_decode(const nt_decode_args* a, void* stream) {
   const int R = g * a->seq_q;
   if (R != 1 && R != 2 && R != 4 && R != 8)
     return set_error(NT_ERR_UNSUPPORTED, "decode kernel packs 1, 2, 4 or 8 query rows per kv group");
-  if (!a->workspace) return set_error(NT_ERR_INVALID, "workspace required");
+  if (!a->workspace || a->workspace_bytes < nt_decode_workspace_bytes(a->batch, a->heads_kv, R, a->head_dim,
+                                                                      std::max(1, a->num_splits)))
+    return set_error(NT_ERR_INVALID, "workspace missing or smaller than nt_decode_workspace_bytes(...)");
   for (const nt_tensor4* t : {&a->q, &a->k, &a->v})
     if (reinterpret_cast<uintptr_t>(t->ptr) % 16 || t->stride_s % 8 || t->stride_h % 8 || t->stride_b % 8)
       return set_error(NT_ERR_INVALID, "q/k/v must be 16-byte aligned with strides % 8 == 0");
@@ -137,6 +133,8 @@ extern "C" int nt_attn_decode_paged(const nt_decode_paged_args* a, void* stream)
   if (ps <= 0 || ps % 8 || (ps < kDecodeTile && kDecodeTile % ps) || (ps > kDecodeTile && ps % kDecodeTile))
     return set_error(NT_ERR_UNSUPPORTED, "page_size must be 8, 16, 32, 64 or a multiple of 64");
   if (!a->workspace || !a->block_table || !a->seq_lens) return set_error(NT_ERR_INVALID, "workspace, block_table and seq_lens required");
+  if (a->workspace_bytes < nt_decode_workspace_bytes(a->batch, a->heads_kv, R, a->head_dim, std::max(1, a->num_splits)))
+    return set_error(NT_ERR_INVALID, "workspace smaller than nt_decode_workspace_bytes(...)");
   if (a->max_seq_kv <= 0 || a->num_pages <= 0) return set_error(NT_ERR_INVALID, "empty cache");
   for (const nt_tensor4* t : {&a->q})
     if (reinterpret_cast<uintptr_t>(t->ptr) % 16 || t->stride_s % 8 || t->stride_h % 8 || t->stride_b % 8)

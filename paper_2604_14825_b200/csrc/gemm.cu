@@ -42,21 +42,18 @@ int launch_gemm(const nt_gemm_args* a, cudaStream_t st) {
   p.tiles_m = (a->m + 127) / 128;
   p.tiles_n = (a->n + BN - 1) / BN;
   const int k_blocks = (a->k + 63) / 64;
-  p.k_splits = (a->k_splits > 1 && a->workspace) ? std::min(a->k_splits, k_blocks) : 1;
+  // clamp to what the caller's workspace holds (fp32 M x N partial per split)
+  const int64_t per_split = (int64_t)a->m * a->n * (int64_t)sizeof(float);
+  const int fits = a->workspace ? (int)std::min<int64_t>(a->workspace_bytes / per_split, 1 << 20) : 0;
+  p.k_splits = (a->k_splits > 1 && fits > 1) ? std::min(std::min(a->k_splits, fits), k_blocks) : 1;
   p.kb_per = (k_blocks + p.k_splits - 1) / p.k_splits;
   p.k_splits = (k_blocks + p.kb_per - 1) / p.kb_per;  // no empty K range
   p.ws = static_cast<float*>(a->workspace);
   p.c = a->c;
   p.ldc = a->ldc;
-  auto kern = gemm_kernel<BN, F32>;
+  constexpr auto kern = gemm_kernel<BN, F32>;
   const int smem = GemmCfg<BN>::SMEM_BYTES;
-  static bool configured = false;
-  if (!configured) {
-    if ((rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                         "cudaFuncSetAttribute(gemm)")))
-      return rc;
-    configured = true;
-  }
+  if ((rc = configure_smem<kern>(smem, "cudaFuncSetAttribute(gemm)"))) return rc;
   const int tiles = p.tiles_m * p.tiles_n * p.k_splits;
   const int grid = std::min(tiles, sm_count());
   kern<<<grid, kGemmThreads, smem, st>>>(ma, mb, p);
@@ -93,15 +90,9 @@ int launch_gemm2(const nt_gemm_args* a, cudaStream_t st) {
   if ((rc = make_map_2d(&mc, a->c, a->n, a->m, a->ldc, 32, 32, F32 ? 4 : 2,
                         F32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B)))
     return rc;
-  auto kern = gemm2_kernel<F32>;
+  constexpr auto kern = gemm2_kernel<F32>;
   const int smem = Gemm2Cfg<F32>::SMEM_BYTES;
-  static bool configured = false;
-  if (!configured) {
-    if ((rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                         "cudaFuncSetAttribute(gemm2)")))
-      return rc;
-    configured = true;
-  }
+  if ((rc = configure_smem<kern>(smem, "cudaFuncSetAttribute(gemm2)"))) return rc;
   const int tiles = p.tiles_m * p.tiles_n;
   const int grid = 2 * std::min(tiles, sm_count() / 2);  // one CTA pair per tile, persistent
   kern<<<grid, kGemmThreads, smem, st>>>(ma, mb, mc, p);
@@ -139,17 +130,12 @@ int launch_chain(const nt_chain_args* a, cudaStream_t st) {
   p.ldy = a->ldy;
   p.out_f32 = a->out_dtype == NT_DTYPE_F32;
   float* partial = static_cast<float*>(a->workspace);
-  if (splits > 1 && !partial) return set_error(NT_ERR_INVALID, "chain workspace required (nt_gemm_chain_workspace_bytes)");
+  if (splits > 1 && (!partial || a->workspace_bytes < (int64_t)splits * a->n * a->e * (int64_t)sizeof(float)))
+    return set_error(NT_ERR_INVALID, "chain workspace too small (nt_gemm_chain_workspace_bytes)");
   p.partial = partial;
-  auto kern = chain_kernel<E>;
+  constexpr auto kern = chain_kernel<E>;
   const int smem = ChainCfg<E>::SMEM_BYTES;
-  static bool configured = false;
-  if (!configured) {
-    if ((rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                         "cudaFuncSetAttribute(chain)")))
-      return rc;
-    configured = true;
-  }
+  if ((rc = configure_smem<kern>(smem, "cudaFuncSetAttribute(chain)"))) return rc;
   kern<<<p.row_blocks * splits, kChainThreads, smem, st>>>(mx, mw1, mw2, p);
   g_launches++;
   if ((rc = check_cuda(cudaGetLastError(), "chain launch"))) return rc;

@@ -62,6 +62,7 @@ class GemmPlan:
         ws = int(L.nt_gemm_workspace_bytes(M, N, K)) if g.k_splits > 1 else 0
         self.ws = torch.empty(max(ws // 4, 1), dtype=torch.float32, device=a.device) if ws else None
         g.workspace = self.ws.data_ptr() if ws else None
+        g.workspace_bytes = self.ws.numel() * 4 if ws else 0
         if not ws:
             g.k_splits = 1
         self.args, self.tensors = g, (a, b, c)
@@ -102,6 +103,7 @@ class ChainPlan:
             ws = int(_lib.lib().nt_gemm_chain_workspace_bytes(N, F, E))
             self.ws = torch.empty(max(ws // 4, 1), dtype=torch.float32, device=x.device)
             c.workspace = self.ws.data_ptr() if ws else None
+            c.workspace_bytes = self.ws.numel() * 4
             self.args = c
             self._ref = C.byref(c)
             self._fn = _lib.lib().nt_gemm_chain

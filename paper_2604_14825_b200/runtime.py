@@ -165,6 +165,7 @@ class DecodePlan:
         a.num_splits = splits
         a.out_dtype = _lib.NT_DTYPE_F32 if o.dtype == torch.float32 else _lib.NT_DTYPE_BF16
         a.workspace = self.ws.data_ptr()
+        a.workspace_bytes = self.ws.numel() * 4
         a.err_flag = self.err.data_ptr()
         self.args, self.splits = a, splits
         self.tensors = (q, k, v, o)
@@ -246,6 +247,7 @@ class PagedDecodePlan:
         a.num_splits = splits
         a.out_dtype = _lib.NT_DTYPE_F32 if o.dtype == torch.float32 else _lib.NT_DTYPE_BF16
         a.workspace = self.ws.data_ptr()
+        a.workspace_bytes = self.ws.numel() * 4
         a.err_flag = self.err.data_ptr()
         self.args, self.splits = a, splits
         self.tensors = (q, k_pages, v_pages, bt, seq_lens, o)

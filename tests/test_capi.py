@@ -24,7 +24,7 @@ def test_library_loads_and_exports_all_symbols():
     L = _lib.lib()
     for name in declared_symbols():
         assert hasattr(L, name), name
-    assert L.nt_abi_version() == 1
+    assert L.nt_abi_version() == 2
     assert L.nt_launch_count() >= 0
 
 
@@ -32,7 +32,7 @@ def test_struct_layouts_match_header():
     # sizes computed from the header's field order (x86-64 SysV)
     assert ctypes.sizeof(_lib.Tensor4) == 32
     assert ctypes.sizeof(_lib.AttnArgs) == 4 * 32 + 6 * 4 + 4 + 4 + 4 + 4 + 8 + 8 + 4 + 4 + 8 + 8 + 4 + 4 + 3 * 4 + 4 + 8 + 8
-    assert ctypes.sizeof(_lib.GemmArgs) == 6 * 8 + 4 * 4 + 4 + 4 + 8
+    assert ctypes.sizeof(_lib.GemmArgs) == 6 * 8 + 4 * 4 + 4 + 4 + 8 + 8
 
 
 STRUCTS = [("nt_tensor4", "Tensor4"), ("nt_attn_args", "AttnArgs"), ("nt_decode_args", "DecodeArgs"),

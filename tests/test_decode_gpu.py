@@ -169,3 +169,30 @@ def test_paged_decode_empty_sequence_raises():
     torch.cuda.synchronize()
     with pytest.raises(DivisionByZero):
         plan.check_errors()
+
+
+def test_workspace_smaller_than_required_is_rejected():
+    """ABI v2: a workspace_bytes below what the splits need is NT_ERR_INVALID, not an OOB write."""
+    from paper_2604_14825_b200.errors import InvalidArguments
+    from paper_2604_14825_b200.gemm import GemmPlan
+    from paper_2604_14825_b200.runtime import DecodePlan
+
+    D = 128
+    q = torch.zeros((1, 4, 1, D), dtype=torch.bfloat16, device="cuda")
+    k = torch.zeros((1, 1, 4096, D), dtype=torch.bfloat16, device="cuda")
+    o = torch.empty((1, 4, 1, D), dtype=torch.float32, device="cuda")
+    plan = DecodePlan(q, k, k, o, 0.1, num_splits=8)
+    plan.args.workspace_bytes = 64
+    with pytest.raises(InvalidArguments):
+        plan.launch()
+    # split-K GEMM: k_splits is clamped to what the workspace holds (here: none -> unsplit, still correct)
+    a = torch.randn((256, 4096), device="cuda").bfloat16()
+    b = (torch.randn((4096, 128), device="cuda") / 64).bfloat16()
+    c = torch.empty((256, 128), dtype=torch.float32, device="cuda")
+    g = GemmPlan(a, b, c)
+    assert g.args.k_splits > 1
+    g.args.workspace_bytes = 0
+    g.launch()
+    torch.cuda.synchronize()
+    ref = a.float() @ b.float()
+    assert float((c - ref).abs().max()) < 2e-2
