@@ -293,7 +293,7 @@ def run_reference_arm(args, cfg, rank, world):
            "unit": "TFLOP/s", "impl": "reference", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
-           "config": config_block(cfg, args),
+           "config": config_block(cfg, args, world),
            "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": kind,
                             "sample": f"each step: {cores} processes x 1 MA block of the "
                                       f"{args.config} slice program; extrapolated to {blocks_total} blocks "
@@ -313,12 +313,15 @@ def attention_flops(cfg):
     return 4.0 * B * Hq * N * M * D
 
 
-def config_block(cfg, args):
-    world = args.gpus
+def config_block(cfg, args, world):
+    """The workload keys only (identical in both arms); ``world`` = ranks that actually ran."""
     blk = {"workload": args.config}
     blk.update({k: v for k, v in cfg.items() if k not in ("golden",)})
-    blk["parallelism"] = (f"row-block sharding over {world} GPU(s)" if cfg.get("kind") == "gemm_chain"
-                          else f"(batch, kv-head) group sharding over {world} GPU(s)")
+    if world == 1:
+        blk["parallelism"] = "single GPU"
+    else:
+        blk["parallelism"] = (f"row-block sharding over {world} GPUs" if cfg.get("kind") == "gemm_chain"
+                              else f"(batch, kv-head) group sharding over {world} GPUs")
     blk["l2"] = "flushed between timed steps (256 MiB write)"
     return blk
 
@@ -353,8 +356,10 @@ def build_workload(cfg, spec, rank, world, dev):
     kind = cfg.get("kind", "prefill")
     w = {"kind": kind}
     if kind == "gemm_chain":
+        from paper_2604_14825_b200.shard import plan_row_shard
         N, K, F, E = cfg["N"], cfg["K"], cfg["F"], cfg["E"]
-        rows = N // world
+        rs = plan_row_shard(N, world, rank)
+        rows = rs.r1 - rs.r0
         x = torch.randn((rows, K), generator=gen, device=dev).to(torch.bfloat16)
         w1 = (torch.randn((K, F), generator=gen, device=dev) / K ** 0.5).to(torch.bfloat16)
         w2 = (torch.randn((F, E), generator=gen, device=dev) / F ** 0.5).to(torch.bfloat16)
@@ -362,7 +367,7 @@ def build_workload(cfg, spec, rank, world, dev):
         w.update(plan=ChainPlan(x, w1, w2, y), out=y, local_flops=2.0 * rows * F * (K + E),
                  total_flops=2.0 * N * F * (K + E), bound="tensor",
                  host_inputs={spec.x: x, spec.w1: w1, spec.w2: w2}, outer=None, mask_kind=None,
-                 in_bytes=(x.numel() + w1.numel() + w2.numel()) * 2)
+                 in_bytes=(x.numel() + w1.numel() + w2.numel()) * 2, rows=N)
         return w
     b0, b1, h0, h1 = shard(cfg, rank, world)
     g = cfg["Hq"] // cfg["Hkv"]
@@ -443,6 +448,14 @@ def run_ours(args, cfg, rank, world, dist):
     w = build_workload(cfg, spec, rank, world, dev)
     plan, o = w["plan"], w["out"]
     full = torch.empty((world,) + tuple(o.shape), dtype=o.dtype, device=dev) if world > 1 else None
+    if world > 1 and w["kind"] == "gemm_chain":
+        from paper_2604_14825_b200.shard import gather_rows
+
+        def gather():
+            gather_rows(o, w["rows"], world, dist)
+    elif world > 1:
+        def gather():
+            dist.all_gather_into_tensor(full, o)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
 
@@ -450,7 +463,7 @@ def run_ours(args, cfg, rank, world, dist):
         flush.zero_()
         plan.launch(stream)
         if world > 1:
-            dist.all_gather_into_tensor(full, o)
+            gather()
     torch.cuda.synchronize()
     if hasattr(plan, "check_errors") and not os.environ.get("NT_BENCH_NOCHECK"):
         plan.check_errors()
@@ -467,7 +480,7 @@ def run_ours(args, cfg, rank, world, dist):
             plan.launch(stream)
             ev[i][1].record(stream)
             if world > 1:
-                dist.all_gather_into_tensor(full, o)
+                gather()
             ev[i][2].record(stream)
         torch.cuda.synchronize()
     launches = _lib.launch_count() - l0
@@ -482,6 +495,7 @@ def run_ours(args, cfg, rank, world, dist):
         t = torch.tensor([ms_step, ms_kernel], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_step, ms_kernel = float(t[0]), float(t[1])
+    ms_compute = ms_kernel  # max over ranks of the kernel-only time (no gather)
     total_flops = w["total_flops"]
     value = total_flops / (ms_step * 1e-3) / 1e12
     peaks, peak_src = load_peaks()
@@ -504,7 +518,7 @@ def run_ours(args, cfg, rank, world, dist):
         # host q/k/v in, host O out: execute_ma streams the (batch, kv-head) groups
         # (H2D, kernel and D2H of consecutive chunks overlap on three streams)
         execute_ma(mod, host_in, outer=w["outer"], mask_kind=w["mask_kind"], out_dtype="bf16",
-                   return_torch=True, timing=False, out=host_out)
+                   return_torch=True, out=host_out)
 
     for _ in range(max(1, args.warmup)):
         e2e_step()
@@ -563,7 +577,9 @@ def run_ours(args, cfg, rank, world, dist):
         "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "e4m3" if w.get("e4m3") else "bf16", "data": "synthetic (torch.randn, seeded)",
-        "config": dict(config_block(cfg, args), ma_source=ma_src, kernel_ms=ms_kernel),
+        "config": config_block(cfg, args, world),
+        "ma_source": ma_src, "kernel_ms": ms_kernel,
+        "ms_per_step_compute_only": ms_compute, "ms_per_step_with_gather": ms_step,
         "pct_of_peak": {"measured_burst": value / peak_t,
                         "measured_sustained": value / peaks.get("bf16_tflops_sustained", peak_t),
                         "nominal_2250": value / 2250.0, "peak_source": peak_src},
@@ -580,6 +596,23 @@ def run_ours(args, cfg, rank, world, dist):
     print(json.dumps(out), flush=True)
 
 
+def spawn_ranks(n):
+    """``bench.py --gpus N`` outside torchrun: launch N ranks (one per GPU, NCCL) the way
+    the driver does and return rank 0's exit status; rank 0 prints the JSON line.
+    NCCL's init log (transport, NVLS/NVLink choice) goes to stderr."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT,NVLS")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -591,6 +624,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     args.gpus = world if world > 1 else args.gpus

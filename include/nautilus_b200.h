@@ -92,6 +92,11 @@ typedef struct nt_attn_args {
 } nt_attn_args;
 int nt_attn_fwd(const nt_attn_args* args, void* stream);
 int64_t nt_attn_workspace_bytes(const nt_attn_args* args);
+/* Everything nt_attn_fwd does except the launch: validation, tensor-map encoding,
+ * split plan, kernel choice and the per-device shared-memory attribute (which
+ * loads the lazily loaded kernel image).  Call once per plan so the first
+ * launch costs what every later one does.  No device work is enqueued. */
+int nt_attn_prepare(const nt_attn_args* args);
 
 /*
  * K2 split-KV decode attention + combine (flash-decoding) for short query

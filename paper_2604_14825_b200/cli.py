@@ -110,15 +110,18 @@ def cmd_selftest(args) -> int:
 
 def _context(args):
     import_tilecc()
-    from tilecc.autosched.scheduler import SchedulerOptions, run_autoscheduler
-    from tilecc.ma.device import DEFAULT_DEVICE, load_device
+    from dataclasses import replace
+
+    from tilecc.autosched.scheduler import run_autoscheduler
     from tilecc.pipeline import frontend
+
+    from .frontdoor import resolve_device
 
     text = Path(args.program).read_text()
     binding = _parse_bind(args.bind)
-    device = load_device(args.device) if args.device else DEFAULT_DEVICE
+    device, opts = resolve_device(args.device)  # None | "b200" | profile path
     bound, base = frontend(text, binding)
-    seeds = run_autoscheduler(base, device, SchedulerOptions(max_seeds=args.max_seeds))
+    seeds = run_autoscheduler(base, device, replace(opts, max_seeds=args.max_seeds))
     if not seeds:
         raise SystemExit("error: auto-scheduler produced no viable seeds")
     return text, binding, device, bound, base, seeds
@@ -216,7 +219,9 @@ def build_argparser() -> argparse.ArgumentParser:
     def common(p):
         p.add_argument("program", help="input .te file")
         p.add_argument("--bind", action="append", default=[], help="dimension binding, e.g. --bind N=256,M=256")
-        p.add_argument("--device", default=None, help="reference device profile path")
+        p.add_argument("--device", default=None,
+                       help='device profile: "b200" (b200.device, sm100a backend only) or a profile path '
+                            "(default: the reference's virtual-h100)")
         p.add_argument("--seed", type=int, default=0, help="rng seed")
         p.add_argument("--max-seeds", type=int, default=16)
         p.add_argument("--backend", default="simt", choices=["auto", "simt", "tcgen05"])

@@ -47,6 +47,51 @@ class DeviceProfile:
 
 DEFAULT = DeviceProfile()
 
+_INT_KEYS = {"shared_bytes", "register_bytes", "warp_default", "stage_default"}
+_IGNORED_INT_KEYS = {"inner_cap", "max_tile_elems", "stage_min", "stage_max"}  # scheduler-only
+_FLOAT_KEYS = {"cost_global", "cost_shared", "cost_register", "cost_flop", "launch_cost", "stage_discount"}
+
+
+def parse_profile(text: str) -> DeviceProfile:
+    """``key = value`` device profile -> DeviceProfile (restates parse_device,
+    tilecc/ma/device.py:59-95, for the fields the cost model reads; the
+    scheduler-only keys are accepted and ignored).  Unknown keys raise."""
+    from dataclasses import replace
+
+    dev = DEFAULT
+    factors = dict(dev.backend_factors)
+    for lineno, raw in enumerate(text.splitlines(), start=1):
+        line = raw.split("#", 1)[0].strip()
+        if not line:
+            continue
+        if "=" not in line:
+            raise ValueError(f"device profile line {lineno}: expected key = value")
+        key, _, val = (x.strip() for x in line.partition("="))
+        if key in _INT_KEYS:
+            dev = replace(dev, **{key: int(val)})
+        elif key in _FLOAT_KEYS:
+            dev = replace(dev, **{key: float(val)})
+        elif key in _IGNORED_INT_KEYS:
+            int(val)
+        elif key == "warp_choices":
+            tuple(int(x) for x in val.split(","))
+        elif key == "name":
+            dev = replace(dev, name=val)
+        elif key.startswith("backend.") and key.endswith((".byte_factor", ".flop_factor")):
+            b = key.split(".")[1]
+            bf, ff = factors.get(b, (1.0, 1.0))
+            factors[b] = (float(val), ff) if key.endswith(".byte_factor") else (bf, float(val))
+        else:
+            raise ValueError(f"device profile line {lineno}: unknown key {key!r}")
+    return replace(dev, backend_factors=tuple(sorted(factors.items())))
+
+
+def b200_profile() -> DeviceProfile:
+    """The B200 profile (``b200.device``, also what ``frontdoor.b200_device`` feeds the scheduler)."""
+    import os
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "b200.device")) as f:
+        return parse_profile(f.read())
+
 
 @dataclass(frozen=True)
 class B200:

@@ -17,6 +17,10 @@ namespace nt {
 
 thread_local std::string g_last_error;
 std::atomic<int64_t> g_launches{0};
+// nt_attn_prepare: run the whole launch path (validation, tensor maps, split plan,
+// kernel selection, per-device smem attribute -- which also loads the lazily
+// loaded kernel image) but stop before the launch
+thread_local bool g_prepare_only = false;
 
 int set_error(int code, const std::string& msg) {
   g_last_error = msg;
@@ -174,6 +178,12 @@ static int launch_attn_kernel(const AttnMaps& m, const AttnFwdParams& p, cudaStr
   constexpr auto kern = attn_fwd_kernel<D, MASK, F32, KVS, FP8, SPLIT>;
   const int smem = AttnCfg<D, KVS, F32, FP8>::SMEM_BYTES;
   if (const int rc0 = configure_smem<kern>(smem, "cudaFuncSetAttribute(attn_fwd)")) return rc0;
+  if (g_prepare_only) {
+    cudaFuncAttributes fa;
+    if constexpr (SPLIT) return check_cuda(cudaFuncGetAttributes(&fa, attn_combine_kernel<D, MASK, F32>),
+                                           "cudaFuncGetAttributes(attn_combine)");
+    return NT_OK;
+  }
   // persistent: at most one CTA per SM, each walking items blockIdx.x + k * gridDim.x
   const int grid = std::min(p.n_items, num_sms());
   kern<<<grid, kAttnThreads, smem, st>>>(m.q, m.k, m.v, m.o, m.p, p);
@@ -188,7 +198,7 @@ static int launch_attn(const AttnMaps& m, const AttnFwdParams& p, cudaStream_t s
   if constexpr (MASK != MASK_TENSOR) {
     if (p.kv_split > 0) {
       int rc = launch_attn_kernel<D, MASK, F32, KVS, FP8, true>(m, p, st);
-      if (rc) return rc;
+      if (rc || g_prepare_only) return rc;
       // split-KV items: merge the fp32 partials
       attn_combine_kernel<D, MASK, F32><<<dim3(32, p.B * p.Hq, p.n_mblocks), 256, 0, st>>>(m.part_o, p);
       g_launches++;
@@ -248,6 +258,15 @@ using namespace nt;
 extern "C" int64_t nt_attn_workspace_bytes(const nt_attn_args* a) {
   if (!a || a->seq_q <= 0 || a->seq_kv <= 0 || a->batch <= 0 || a->heads_q <= 0) return 0;
   return attn_split_plan(a).bytes;
+}
+
+extern "C" int nt_attn_fwd(const nt_attn_args* a, void* stream);
+
+extern "C" int nt_attn_prepare(const nt_attn_args* a) {
+  g_prepare_only = true;
+  const int rc = nt_attn_fwd(a, nullptr);
+  g_prepare_only = false;
+  return rc;
 }
 
 extern "C" int nt_attn_fwd(const nt_attn_args* a, void* stream) {

@@ -407,8 +407,19 @@ def _execute_simt(module, mod, inputs, prec, stream, return_torch):
 BACKENDS = ("auto", "tcgen05", "simt")
 
 
+def _launch_stream(stream, cur):
+    """``stream`` argument -> torch stream object (``cur`` itself when it is the current stream)."""
+    if stream is None:
+        return cur
+    if isinstance(stream, int):
+        if stream == cur.cuda_stream:
+            return cur
+        return torch.cuda.ExternalStream(stream, device=cur.device)
+    return cur if stream.cuda_stream == cur.cuda_stream else stream
+
+
 def execute_ma(module, inputs: dict, device=None, precision=None, *, outer=None, mask_kind=None,
-               out_dtype=None, stream=None, timing: bool = True, return_torch: bool = False,
+               out_dtype=None, stream=None, return_torch: bool = False,
                backend: str = "auto", out: Optional[torch.Tensor] = None, chunks: int = 4):
     """Run an MA module on the B200 (see module docstring).
 
@@ -418,6 +429,11 @@ def execute_ma(module, inputs: dict, device=None, precision=None, *, outer=None,
     (fp32 / fp64, interpret_ma's operation order); "auto" (default) uses the
     tensor-core kernels for fp32 programs they recognise and the SIMT lowering
     for every other program and for fp64.
+
+    ``stream``: optional ``torch.cuda.Stream`` (or raw ``cudaStream_t``) to launch on.
+    Input staging runs on the current stream; ``stream`` waits for it before the
+    launch, the device time is taken on ``stream``, and the current stream waits
+    for ``stream`` before the output is read, so results are ordered either way.
 
     ``out``: optional preallocated tensor (host or device) that receives the
     module output.  With host (CPU) q/k/v inputs over an outer grid and a host
@@ -474,10 +490,16 @@ def execute_ma(module, inputs: dict, device=None, precision=None, *, outer=None,
                 report.realisation.append({"kernel": "attn_fwd", "mask": plan.mask_kind,
                                            "grid_ctas": -(-spec.n // 256) * o.shape[0] * o.shape[1],
                                            "gpu_tile": (256, 128), "ma_tile": (spec.block_m, spec.block_n)})
+            cur = torch.cuda.current_stream(dev)
+            st = _launch_stream(stream, cur)
             ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            ev0.record()
-            plan.launch(stream)
-            ev1.record()
+            if st is not cur:
+                st.wait_stream(cur)  # q/k/v staging and casts ran on the current stream
+            ev0.record(st)
+            plan.launch(st)
+            ev1.record(st)
+            if st is not cur:
+                cur.wait_stream(st)  # output reads / error flag below are on the current stream
             ev1.synchronize()
             plan.check_errors()
             report.device_ms += ev0.elapsed_time(ev1)
@@ -514,6 +536,13 @@ def execute_ma(module, inputs: dict, device=None, precision=None, *, outer=None,
     return bufs, report
 
 
-def run_pipeline(ma, inputs: dict, device=None, precision=None):
-    """Drop-in for tilecc.pipeline.run_pipeline (tilecc/pipeline.py:62-64)."""
-    return execute_ma(ma, inputs, device, precision)
+def run_pipeline(ma, inputs: dict, device=None, precision=None, backend: str = "simt"):
+    """Drop-in for tilecc.pipeline.run_pipeline (tilecc/pipeline.py:62-64).
+
+    Defaults to ``backend="simt"``: interpret_ma's own fp32/fp64 arithmetic on the
+    GPU, so the reference's ``check`` gate (exact + RMS <= 1e-5, tilecc/cli.py:196)
+    holds.  ``backend="auto"`` runs recognised attention / GEMM-chain programs on
+    the tensor cores with bf16 operands (max-abs ~1e-3: inside the BASELINE
+    tolerance, outside that gate).
+    """
+    return execute_ma(ma, inputs, device, precision, backend=backend)

@@ -102,6 +102,8 @@ class AttentionPlan:
         self.shape = (B, Hq, Hkv, N, M, D)
         self._fn = _lib.lib().nt_attn_fwd
         self._ref = C.byref(a)
+        # validate + load the kernel now, so the first launch is a plain launch
+        _lib.check(_lib.lib().nt_attn_prepare(self._ref), "nt_attn_prepare")
 
     def launch(self, stream=None) -> None:
         st = self._fn(self._ref, _stream_handle(stream))

@@ -860,8 +860,13 @@ def execute(module, inputs: dict, precision: Optional[str] = None, stream=None, 
             tensors[b.name] = torch.zeros(tuple(b.shape), dtype=tdt, device=dev)
     loaded = load(prog)
     L = _lib.lib()
-    st = torch.cuda.current_stream() if stream is None else stream
-    st_handle = C.c_void_p(st.cuda_stream if hasattr(st, "cuda_stream") else st)
+    cur = torch.cuda.current_stream(dev)
+    if stream is None or (stream if isinstance(stream, int) else stream.cuda_stream) == cur.cuda_stream:
+        st = cur
+    else:
+        st = stream if not isinstance(stream, int) else torch.cuda.ExternalStream(stream, device=dev)
+        st.wait_stream(cur)  # inputs, zeroed buffers and scratch were staged on the current stream
+    st_handle = C.c_void_p(st.cuda_stream)
     max_grid = max(l.grid for l in prog.launches) if prog.launches else 1
     scratch_elems = max([l.scratch_elems_per_block * l.grid for l in prog.launches] + [1])
     if prog.carried:
@@ -879,6 +884,8 @@ def execute(module, inputs: dict, precision: Optional[str] = None, stream=None, 
         arr = (C.c_void_p * len(args))(*[C.cast(C.pointer(a), C.c_void_p) for a in args])
         _lib.check(L.nt_launch(fn, ln.grid, THREADS, ln.smem_bytes, arr, st_handle), "nt_launch")
     ev1.record(st)
+    if st is not cur:
+        cur.wait_stream(st)  # outputs and the error flag are read on the current stream
     ev1.synchronize()
     if int(err.item()) & 1:
         raise DivisionByZero("tile divide")

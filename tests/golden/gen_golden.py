@@ -96,7 +96,30 @@ CASES = [
          assign=dict(t0_i=32, t0_j=64)),
     dict(name="causal512_t128x64", prog="llama_causal", bind=dict(N=512, M=512, D=128), seeds=[0],
          io=True, mask="causal", assign=dict(t0_i=128, t0_j=64)),
+    # the same programs scheduled for the B200 profile (paper_2604_14825_b200/b200.device,
+    # SchedulerOptions(backends=("sm100a",))): config 2 at E=4096 schedules without overrides
+    dict(name="b200_attn256", prog="attention", bind=dict(N=256, M=256, D=64), seeds="all", io=True,
+         profile="b200"),
+    dict(name="b200_bert512", prog="scaled_0p125", bind=dict(N=512, M=512, D=64), seeds=[0], io=True,
+         profile="b200"),
+    dict(name="b200_causal512", prog="llama_causal", bind=dict(N=512, M=512, D=128), seeds=[0], io=True,
+         mask="causal", profile="b200"),
+    dict(name="b200_decode4", prog="llama", bind=dict(N=4, M=2048, D=128), seeds=[0], io=True, profile="b200"),
+    dict(name="b200_gemm_v6", prog="gemm2", bind=dict(N=256, K=256, F=512, E=128), seeds=[0], io=True,
+         scales={"W1": 1 / 16.0, "W2": 1 / math.sqrt(512)}, profile="b200"),
+    dict(name="b200_gemm_e512", prog="gemm2", bind=dict(N=256, K=256, F=256, E=512), seeds=[0], io=True,
+         scales={"W1": 1 / 16.0, "W2": 1 / 16.0}, profile="b200"),
+    dict(name="b200_gemm4k_e4096", prog="gemm2", bind=dict(N=4096, K=4096, F=4096, E=4096), seeds=[0],
+         io=False, profile="b200"),
+    dict(name="b200_causal8k", prog="llama_causal", bind=dict(N=8192, M=8192, D=128), seeds=[0], io=False,
+         profile="b200"),
 ]
+
+
+def b200_context():
+    from tilecc.ma.device import load_device
+    return (load_device(os.path.join(REPO, "paper_2604_14825_b200", "b200.device")),
+            SchedulerOptions(backends=("sm100a",)))
 
 
 def main():
@@ -104,15 +127,19 @@ def main():
     for case in CASES:
         name = case["name"]
         src = PROGRAMS[case["prog"]]
-        device = DEFAULT_DEVICE
+        device, opts = DEFAULT_DEVICE, SchedulerOptions()
+        if case.get("profile") == "b200":
+            device, opts = b200_context()
         if case.get("device"):
-            device = replace(DEFAULT_DEVICE, **case["device"])
+            device = replace(device, **case["device"])
         bound, base = frontend(src, case["bind"])
-        seeds = run_autoscheduler(base, device, SchedulerOptions())
+        seeds = run_autoscheduler(base, device, opts)
         which = range(len(seeds)) if case["seeds"] == "all" else case["seeds"]
         entry = {"program": case["prog"], "binding": case["bind"], "n_seeds": len(seeds),
                  "seeds": list(which), "assignment": case.get("assign"),
                  "device": case.get("device"), "io": case["io"], "mask": case.get("mask")}
+        if case.get("profile"):
+            entry["profile"] = case["profile"]
         for k in which:
             sd = seeds[k]
             assignment = None

@@ -20,7 +20,7 @@ def _check(got, ref, max_abs=2e-2, rel=1e-2):
     assert mx <= max_abs and rl <= rel, (mx, rl)
 
 
-@pytest.mark.parametrize("case", ["decode4", "decode1"])
+@pytest.mark.parametrize("case", ["decode4", "decode1", "b200_decode4"])
 def test_execute_ma_decode_matches_reference(case):
     from paper_2604_14825_b200 import execute_ma
 

@@ -22,7 +22,7 @@ def test_every_golden_kernel_is_recognised(fname):
     specs = recognize(mod)
     assert len(specs) == 1
     spec = specs[0]
-    if fname.startswith("gemm"):
+    if fname.startswith(("gemm", "b200_gemm")):
         assert isinstance(spec, GemmChainSpec)
         assert spec.n_blocks * spec.block_m == spec.n
         assert spec.n_iters * spec.block_f == spec.f
@@ -43,7 +43,8 @@ def test_every_golden_kernel_is_recognised(fname):
 @pytest.mark.parametrize("fname", all_ma_files())
 def test_static_cost_matches_reference_cost_model(fname):
     mod = _load(fname)
-    mine = cost.cost_model(mod)
+    # b200_* goldens were scheduled under paper_2604_14825_b200/b200.device
+    mine = cost.cost_model(mod, cost.b200_profile() if fname.startswith("b200_") else cost.DEFAULT)
     with open(os.path.join(GOLDEN, fname.replace(".ma.json", ".cost.json"))) as f:
         ref = json.load(f)
     assert mine.bytes_global == ref["bytes"]["Global"]
@@ -74,7 +75,7 @@ def _ma_slices(mod):
     return out
 
 
-@pytest.mark.parametrize("fname", [f for f in all_ma_files() if not f.startswith("gemm")
+@pytest.mark.parametrize("fname", [f for f in all_ma_files() if "gemm" not in f
                                    and ("256" in f or "512" in f or "decode" in f)])
 def test_attention_index_math_matches_gpu_tiling(fname):
     """Each GPU (CTA, kv-tile) is exactly the union of the MA (block, j0) tiles
@@ -138,3 +139,32 @@ def test_access_audit_equals_reference_cost_report(case):
     unique, audit = cost.access_audit(mod)
     assert unique == ref["unique_global_bytes"]
     assert audit == ref["read_audit"]
+
+
+def test_b200_profile_parses_like_the_reference():
+    """cost.parse_profile and the reference's parse_device read b200.device identically."""
+    import dataclasses
+
+    from paper_2604_14825_b200.frontdoor import B200_PROFILE, b200_device, import_tilecc
+    try:
+        import_tilecc()
+    except ImportError:
+        pytest.skip("reference front end not importable")
+    ref = b200_device()
+    mine = cost.b200_profile()
+    for f in dataclasses.fields(mine):
+        assert getattr(mine, f.name) == getattr(ref, f.name), f.name
+    assert ref.inner_cap == 256 and ref.max_tile_elems >= 262144 and ref.warp_choices == (4, 8)
+    assert "sm100a" in ref.backends()
+
+
+def test_b200_profile_schedules_config2_e4096_without_overrides():
+    """the default profile rejects the E=4096 chain; the B200 profile schedules it."""
+    import json as _json
+    with open(os.path.join(GOLDEN, "manifest.json")) as f:
+        man = _json.load(f)
+    e = man["b200_gemm4k_e4096"]
+    assert e["profile"] == "b200" and e["device"] is None and e["n_seeds"] >= 1
+    spec = recognize(_load("b200_gemm4k_e4096.seed0.ma.json"))[0]
+    assert isinstance(spec, GemmChainSpec) and spec.e == 4096
+    assert _load("b200_gemm4k_e4096.seed0.ma.json").kernels[0].backend == "sm100a"
