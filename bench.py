@@ -430,7 +430,7 @@ def build_workload(cfg, spec, rank, world, dev):
                  host_inputs={"q": q, "k": k, "v": v}, outer=None, mask_kind=mask_kind, e4m3=True,
                  in_bytes=q.numel() + k.numel() + v.numel())
         return w
-    plan = AttentionPlan(q, k, v, o, spec.scale, mask_kind)
+    plan = AttentionPlan(q, k, v, o, spec.scale, mask_kind, item_rows=cfg.get("item_rows", 0))
     w.update(plan=plan, out=o, local_flops=plan.flops(), total_flops=attention_flops(cfg), bound="tensor",
              host_inputs={spec.q: q, spec.k: k, spec.v: v}, outer=(Bl, Hql, Hkvl), mask_kind=mask_kind,
              in_bytes=(q.numel() + k.numel() + v.numel()) * 2)
@@ -579,6 +579,7 @@ def run_ours(args, cfg, rank, world, dist):
         "dtype": "e4m3" if w.get("e4m3") else "bf16", "data": "synthetic (torch.randn, seeded)",
         "config": config_block(cfg, args, world),
         "ma_source": ma_src, "kernel_ms": ms_kernel,
+        "k1_item_rows": getattr(plan, "item_rows", None), "k1_ctas_per_sm": getattr(plan, "ctas_per_sm", None),
         "ms_per_step_compute_only": ms_compute, "ms_per_step_with_gather": ms_step,
         "pct_of_peak": {"measured_burst": value / peak_t,
                         "measured_sustained": value / peaks.get("bf16_tflops_sustained", peak_t),
@@ -622,8 +623,12 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--item-rows", type=int, default=0, choices=[0, 128, 256],
+                    help="K1 query rows per work item (0 = library choice)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
+    if args.item_rows:
+        cfg = dict(cfg, item_rows=args.item_rows)
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(spawn_ranks(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))

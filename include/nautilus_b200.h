@@ -30,7 +30,7 @@ extern "C" {
 
 /* 2: workspace_bytes in the decode / gemm / chain argument structs (the library
  *    rejects a workspace smaller than the launch needs instead of writing past it) */
-#define NT_ABI_VERSION 2
+#define NT_ABI_VERSION 3
 
 /* status codes (mapped by the host onto tilecc.errors CompilerError subclasses) */
 #define NT_OK 0
@@ -89,6 +89,10 @@ typedef struct nt_attn_args {
    * run unsplit).  The kernel then writes fp32 partials and a merge kernel follows. */
   void* workspace;
   int64_t workspace_bytes;
+  /* query rows per work item (ABI 3): 0 = library choice, 256 = two 128-row
+   * tiles per CTA (one CTA per SM), 128 = one tile per CTA, two CTAs per SM
+   * (bf16 only).  The MA's t0_i tunable realised on the GPU (tuner.py). */
+  int32_t item_rows;
 } nt_attn_args;
 int nt_attn_fwd(const nt_attn_args* args, void* stream);
 int64_t nt_attn_workspace_bytes(const nt_attn_args* args);
@@ -97,6 +101,9 @@ int64_t nt_attn_workspace_bytes(const nt_attn_args* args);
  * loads the lazily loaded kernel image).  Call once per plan so the first
  * launch costs what every later one does.  No device work is enqueued. */
 int nt_attn_prepare(const nt_attn_args* args);
+/* CTAs of the kernel `args` selects that are resident per SM (the persistent
+ * grid is this x #SMs); a negative NT_ERR_* on invalid arguments. */
+int nt_attn_resident_ctas(const nt_attn_args* args);
 
 /*
  * K2 split-KV decode attention + combine (flash-decoding) for short query

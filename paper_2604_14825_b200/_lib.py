@@ -20,7 +20,7 @@ NT_DTYPE_BF16, NT_DTYPE_F32, NT_DTYPE_E4M3 = 0, 1, 2
 
 # Every symbol include/nautilus_b200.h declares (checked by tests/test_capi.py).
 EXPORTED = (
-    "nt_attn_fwd", "nt_attn_workspace_bytes", "nt_attn_prepare", "nt_attn_decode", "nt_decode_workspace_bytes", "nt_decode_num_splits", "nt_gemm",
+    "nt_attn_fwd", "nt_attn_workspace_bytes", "nt_attn_prepare", "nt_attn_resident_ctas", "nt_attn_decode", "nt_decode_workspace_bytes", "nt_decode_num_splits", "nt_gemm",
     "nt_gemm_chain", "nt_gemm_chain_workspace_bytes", "nt_gemm_k_splits", "nt_gemm_workspace_bytes",
     "nt_cast_f32_to_bf16", "nt_cast_bf16_to_f32", "nt_abi_version", "nt_last_error", "nt_launch_count",
     "nt_module_load", "nt_module_function", "nt_launch", "nt_module_unload", "nt_attn_decode_paged",
@@ -42,7 +42,7 @@ class AttnArgs(C.Structure):
                 ("out_dtype", C.c_int32), ("err_flag", C.c_void_p), ("work_counter", C.c_void_p),
                 ("kv_stages", C.c_int32), ("in_dtype", C.c_int32), ("q_descale", C.c_float),
                 ("k_descale", C.c_float), ("v_descale", C.c_float), ("workspace", C.c_void_p),
-                ("workspace_bytes", C.c_int64)]
+                ("workspace_bytes", C.c_int64), ("item_rows", C.c_int32)]
 
 
 class DecodeArgs(C.Structure):
@@ -96,6 +96,7 @@ def lib():
             L = C.CDLL(LIB_PATH)
             L.nt_attn_fwd.argtypes = [C.POINTER(AttnArgs), C.c_void_p]
             L.nt_attn_prepare.argtypes = [C.POINTER(AttnArgs)]
+            L.nt_attn_resident_ctas.argtypes = [C.POINTER(AttnArgs)]
             L.nt_attn_decode.argtypes = [C.POINTER(DecodeArgs), C.c_void_p]
             L.nt_attn_decode_paged.argtypes = [C.POINTER(DecodePagedArgs), C.c_void_p]
             L.nt_decode_workspace_bytes.argtypes = [C.c_int32] * 5
@@ -124,7 +125,7 @@ def lib():
             L.nt_memcpy2d_async.restype = C.c_int
             L.nt_last_error.restype = C.c_char_p
             L.nt_launch_count.restype = C.c_int64
-            for name in ("nt_attn_fwd", "nt_attn_prepare", "nt_attn_decode", "nt_attn_decode_paged", "nt_gemm", "nt_gemm_chain",
+            for name in ("nt_attn_fwd", "nt_attn_prepare", "nt_attn_resident_ctas", "nt_attn_decode", "nt_attn_decode_paged", "nt_gemm", "nt_gemm_chain",
                          "nt_cast_f32_to_bf16", "nt_cast_bf16_to_f32", "nt_abi_version",
                          "nt_module_load", "nt_module_function", "nt_launch", "nt_module_unload"):
                 getattr(L, name).restype = C.c_int

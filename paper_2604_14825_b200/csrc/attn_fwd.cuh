@@ -31,6 +31,14 @@
 // TMEM (512 cols): S0 [0,128) S1 [128,256) O0 [256,256+D) O1 [384,384+D);
 // P_t (bf16, 64 cols) aliases the first half of S_t.
 //
+// NQ = 1 ("128-row items"): the same pipeline with ONE query tile per item and
+// one softmax warpgroup (256 threads, 256 TMEM columns: S [0,128), O [128,..)),
+// sized so that TWO CTAs share an SM.  The two co-resident CTAs are independent
+// streams of work items -- each with its own Q, K/V ring and barriers -- so one
+// CTA's item boundary (Q landing, first S, epilogue) overlaps the other CTA's
+// KV loop, and items are half as long (finer LPT balance).  This is the MA's
+// t0_i choice made real on the GPU: 128 vs 256 query rows per work item.
+//
 // Numerics: bf16 operands, fp32 accumulation, P rounded to bf16 before P.V.
 // The scale c is folded into the exp2 constant (c*log2e), which differs from
 // the MA's K_s*c only in rounding.  The running max is updated lazily: a warp
@@ -49,7 +57,7 @@ enum { MASK_NONE = 0, MASK_CAUSAL = 1, MASK_TENSOR = 2 };
 struct AttnFwdParams {
   int B, Hq, Hkv, N, M;
   int q_per_kv;
-  int n_mblocks;      // ceil(N / 256)
+  int n_mblocks;      // ceil(N / rows per item)
   int n_kv_total;     // ceil(M / 128)
   int n_items;        // n_mblocks * B * Hq
   int causal_offset;  // key j visible to query i iff j <= i + causal_offset
@@ -71,9 +79,14 @@ struct AttnFwdParams {
 };
 constexpr int kMaxSplitMblocks = 384;  // prefix table size in shared memory
 
-constexpr int kAttnThreads = 384;
+template <int NQ>
+constexpr int attn_threads() { return 128 + 128 * NQ; }
+constexpr int kAttnThreads = attn_threads<2>();
 #ifndef NT_REG_LO64
 #define NT_REG_LO64 104  // D=64 register split (88 / 96 / 104 -> softmax 208 / 204 / 200)
+#endif
+#ifndef NT_REG_LO_NQ1
+#define NT_REG_LO_NQ1 64  // NQ = 1 register split (56 / 64 / 72 -> softmax 200 / 192 / 184; 56 spills the issuer)
 #endif
 constexpr int kItemRing = 4;  // work-item slots handed from the producer to the MMA / softmax warps
 constexpr float kRescaleLog2 = 8.0f;
@@ -94,14 +107,20 @@ constexpr int kPolyEvery = NT_POLY_EVERY > 0 ? NT_POLY_EVERY : 1;
 // (SetParam stages, tilecc/autosched/scheduler.py:116-124) picks it: stages = 1
 // keeps one K/V tile pair (D=128) / two pairs (D=64) in flight, stages >= 2 the
 // most shared memory allows (64 KB of K/V per stage).
-template <int D>
+template <int D, int NQ = 2>
 constexpr int attn_kv_slots(int ma_stages) {
+  if (NQ == 1) return (D == 128) ? 2 : (ma_stages <= 1 ? 2 : 4);  // half an SM's shared memory
   return (D == 128) ? (ma_stages <= 1 ? 2 : 4) : (ma_stages <= 1 ? 4 : 8);
 }
 
-template <int D, int KVS = attn_kv_slots<D>(2), bool OUT_F32 = false, bool FP8 = false>
+template <int D, int KVS = attn_kv_slots<D>(2), bool OUT_F32 = false, bool FP8 = false, int NQ = 2,
+          bool SPLIT = false>
 struct AttnCfg {
   static constexpr int BM = 128, BN = 128;
+  static constexpr int ROWS = 128 * NQ;          // query rows per work item
+  static constexpr int THREADS = attn_threads<NQ>();
+  static constexpr int TMEM_COLS = NQ == 2 ? 512 : 256;
+  static constexpr int O_COL0 = 128 * NQ;        // TMEM column of O_0 (O_t at O_COL0 + 128 t)
   static constexpr int ESZ = FP8 ? 1 : 2;     // operand bytes (bf16 | e4m3)
   static constexpr int HALF = 128 * 128;      // one 128-row x 128-byte swizzle-128B panel
   static constexpr int PANELS = D * ESZ / 128;
@@ -118,16 +137,22 @@ struct AttnCfg {
   // while the current one runs); D = 128 has no shared memory left for it
   static constexpr int QB = (D == 64 || FP8) ? 2 : 1;
   static constexpr int SMEM_Q = 0;
-  static constexpr int SMEM_KV = 2 * QB * TQ;
+  static constexpr int SMEM_KV = NQ * QB * TQ;
   // epilogue staging: per softmax warp one 32-row x 32-column O box (TMA store),
   // 64B-swizzled (bf16) / 128B-swizzled (fp32) so the row-per-thread writes are
   // bank-conflict free
-  static constexpr int OBOX = 32 * 32 * 4;  // fp32-sized: split-KV partials are fp32
+  // fp32 O / split-KV partial boxes: 32 columns (128-byte rows, SWIZZLE_128B) or,
+  // NQ = 1 (two CTAs per SM, tight shared memory), 16 columns (64-byte rows,
+  // SWIZZLE_64B); bf16 boxes are 32 columns of 64-byte rows
+  static constexpr int F32_BOX_COLS = NQ == 1 ? 16 : 32;
+  static constexpr int OBOX = ((OUT_F32 || SPLIT) && NQ == 2) ? 32 * 32 * 4 : 32 * 32 * 2;
   static constexpr int SMEM_O = SMEM_KV + STAGES * TKV;
-  static constexpr int SMEM_BAR = SMEM_O + 8 * OBOX;
+  static constexpr int SMEM_BAR = SMEM_O + 4 * NQ * OBOX;
   static constexpr int NBAR = 4 * QB + 2 * STAGES + 2 + 2 + 2 + 2 + 2 + 2 * kItemRing;
   static constexpr int SMEM_PREFIX = SMEM_BAR + NBAR * 8 + 16 + 4 * kItemRing;
-  static constexpr int SMEM_BYTES = SMEM_PREFIX + 4 * (kMaxSplitMblocks + 1) + 1024;  // + alignment slack
+  static constexpr int SMEM_BYTES = SMEM_PREFIX + (SPLIT ? 4 * (kMaxSplitMblocks + 1) : 0) + 1024;  // + alignment slack
+  // two CTAs per SM (NQ = 1): 2 x (SMEM_BYTES + 1 KB reserved) <= 228 KB
+  static constexpr bool FITS = NQ == 2 ? SMEM_BYTES <= 227 * 1024 : SMEM_BYTES <= (233472 - 2 * 1024) / 2;
 };
 
 __device__ __forceinline__ float f_ninf() { return __int_as_float(0xff800000); }
@@ -218,17 +243,17 @@ struct AttnItem {
 };
 
 // KV tiles of m-block mb (causal: up to the diagonal of its last row)
-template <int MASK>
+template <int MASK, int ROWS = 256>
 __device__ __forceinline__ int attn_mb_nkv(const AttnFwdParams& p, int mb) {
   int n_kv = p.n_kv_total;
   if (MASK == MASK_CAUSAL) {
-    const int last_q = min(mb * 256 + 255, p.N - 1) + p.causal_offset;
+    const int last_q = min(mb * ROWS + ROWS - 1, p.N - 1) + p.causal_offset;
     n_kv = max(min(n_kv, last_q / 128 + 1), 1);
   }
   return n_kv;
 }
 
-template <int MASK>
+template <int MASK, int ROWS>
 __device__ __forceinline__ AttnItem attn_item(const AttnFwdParams& p, int w) {
   const int BH = p.B * p.Hq;
   const int bh = w % BH;
@@ -238,8 +263,8 @@ __device__ __forceinline__ AttnItem attn_item(const AttnFwdParams& p, int w) {
   it.hq = bh % p.Hq;
   it.b = bh / p.Hq;
   it.hkv = it.hq / p.q_per_kv;
-  it.q_row0 = mb * 256;
-  it.n_kv = attn_mb_nkv<MASK>(p, mb);
+  it.q_row0 = mb * ROWS;
+  it.n_kv = attn_mb_nkv<MASK, ROWS>(p, mb);
   it.kv_lo = 0;
   it.unit = w;
   it.split = false;
@@ -249,9 +274,9 @@ __device__ __forceinline__ AttnItem attn_item(const AttnFwdParams& p, int w) {
 // Work unit w: items in the same LPT order (heaviest m-blocks first); with
 // kv_split, m-block position i holds ceil(n_kv / kv_split) x B x Hq units
 // (chunk-major), located by a binary search of the prefix table.
-template <int MASK, bool SPLIT>
+template <int MASK, bool SPLIT, int ROWS = 256>
 __device__ __forceinline__ AttnItem attn_unit(const AttnFwdParams& p, const int* prefix, int w) {
-  if (!SPLIT) return attn_item<MASK>(p, w);
+  if (!SPLIT) return attn_item<MASK, ROWS>(p, w);
   int lo = 0, hi = p.n_mblocks;
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
@@ -262,12 +287,12 @@ __device__ __forceinline__ AttnItem attn_unit(const AttnFwdParams& p, const int*
   const int r = w - prefix[lo];
   const int c = r / BH, bh = r - c * BH;
   const int mb = (MASK == MASK_CAUSAL) ? (p.n_mblocks - 1 - lo) : lo;
-  const int n_full = attn_mb_nkv<MASK>(p, mb);
+  const int n_full = attn_mb_nkv<MASK, ROWS>(p, mb);
   AttnItem it;
   it.hq = bh % p.Hq;
   it.b = bh / p.Hq;
   it.hkv = it.hq / p.q_per_kv;
-  it.q_row0 = mb * 256;
+  it.q_row0 = mb * ROWS;
   it.kv_lo = c * p.kv_split;
   it.n_kv = min(p.kv_split, n_full - it.kv_lo);
   it.unit = w;
@@ -275,16 +300,18 @@ __device__ __forceinline__ AttnItem attn_unit(const AttnFwdParams& p, const int*
   return it;
 }
 
-template <int D, int MASK, bool OUT_F32, int KVS, bool FP8 = false, bool SPLIT = false>
-__global__ void __launch_bounds__(kAttnThreads, 1)
+template <int D, int MASK, bool OUT_F32, int KVS, bool FP8 = false, bool SPLIT = false, int NQ = 2>
+__global__ void __launch_bounds__(attn_threads<NQ>(), NQ == 2 ? 1 : 2)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
                     const __grid_constant__ CUtensorMap tmP, const AttnFwdParams p) {
-  using C = AttnCfg<D, KVS, OUT_F32, FP8>;
+  using C = AttnCfg<D, KVS, OUT_F32, FP8, NQ, SPLIT>;
+  constexpr int ROWS = C::ROWS;
   // register split between warpgroup 0 (producer / MMA issuer) and the softmax
-  // warpgroups: 128 x lo + 256 x hi = 384 x 168
-  constexpr int kRegSplitLo = (D == 64) ? NT_REG_LO64 : 104;
-  static_assert(C::SMEM_BYTES <= 227 * 1024, "K1 shared memory exceeds the 227 KB opt-in limit");
+  // warpgroups: NQ = 2: 128 x lo + 256 x hi = 384 x 168; NQ = 1 (two CTAs per
+  // SM): 128 x lo + 128 x hi = 256 x 128
+  constexpr int kRegSplitLo = NQ == 1 ? NT_REG_LO_NQ1 : (D == 64) ? NT_REG_LO64 : 104;
+  static_assert(C::FITS, "K1 shared memory exceeds the per-CTA budget");
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_u32 = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_u32 + 1023u) & ~1023u) - raw_u32);
@@ -338,11 +365,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     }
     for (int s = 0; s < kItemRing; ++s) {
       mbar_init(&bar_item_full[s], 1);
-      mbar_init(&bar_item_empty[s], 9);
+      mbar_init(&bar_item_empty[s], 1 + 4 * NQ);
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
   if (SPLIT && warp == 2) {
     // split-KV unit prefix over m-block positions (warp scan, 32 positions per step)
     const int BH = p.B * p.Hq;
@@ -352,7 +379,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       int cnt = 0;
       if (i < p.n_mblocks) {
         const int mb = (MASK == MASK_CAUSAL) ? (p.n_mblocks - 1 - i) : i;
-        cnt = (attn_mb_nkv<MASK>(p, mb) + p.kv_split - 1) / p.kv_split * BH;
+        cnt = (attn_mb_nkv<MASK, ROWS>(p, mb) + p.kv_split - 1) / p.kv_split * BH;
       }
 #pragma unroll
       for (int off = 1; off < 32; off <<= 1) {
@@ -377,7 +404,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     // registers): 128 x 104 + 256 x 200 = 64512
     if constexpr (kRegSplitLo == 104) asm volatile("setmaxnreg.dec.sync.aligned.u32 104;");
     else if constexpr (kRegSplitLo == 96) asm volatile("setmaxnreg.dec.sync.aligned.u32 96;");
-    else asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
+    else if constexpr (kRegSplitLo == 88) asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
+    else if constexpr (kRegSplitLo == 72) asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
+    else if constexpr (kRegSplitLo == 64) asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
+    else asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
     if (warp == 0) {
       // ================= TMA producer
       if (lane == 0) {
@@ -395,12 +425,12 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           mbar_arrive(&bar_item_full[slot_i]);
           if (li < 15) NT_STAMP(3, 48 + li, 1);  // trace: item li published
           if (w >= p.n_items) break;
-          const AttnItem itm = attn_unit<MASK, SPLIT>(p, unit_prefix, w);
+          const AttnItem itm = attn_unit<MASK, SPLIT, ROWS>(p, unit_prefix, w);
           // Q_t of this item may only land once the previous item's last S_t is
           // done; K(0) goes first, into the ring, so it is resident when Q is
           auto load_q = [&]() {
-            const int qb = (li % C::QB) * 2;
-            for (int t = 0; t < 2; ++t) {
+            const int qb = (li % C::QB) * NQ;
+            for (int t = 0; t < NQ; ++t) {
               if (li >= C::QB) mbar_wait(&bar_q_empty[qb + t], ((li / C::QB) - 1) & 1, p.err, 11);
               mbar_arrive_expect_tx(&bar_q[qb + t], C::TQ);
 #pragma unroll
@@ -451,9 +481,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           for (int k = 0; k < 128 / C::KSTEP; ++k) {
             // KSTEP keys of V (MN-major, 128-byte rows) x P's 8 TMEM columns
             const uint64_t bd = sdesc_sw128(sKVa + slot * C::TKV + k * C::KSTEP * 128, C::HALF, 1024);
-            const uint32_t pcol = C::SEP_P ? (256 + t * 128 + 64) : (t * 128);
-            if (FP8) umma_ts_f8(tmem + 256 + t * 128, tmem + pcol + k * 8, bd, idO, (acc || k > 0) ? 1u : 0u);
-            else umma_ts(tmem + 256 + t * 128, tmem + pcol + k * 8, bd, idO, (acc || k > 0) ? 1u : 0u);
+            const uint32_t pcol = C::SEP_P ? (C::O_COL0 + t * 128 + 64) : (t * 128);
+            if (FP8) umma_ts_f8(tmem + C::O_COL0 + t * 128, tmem + pcol + k * 8, bd, idO, (acc || k > 0) ? 1u : 0u);
+            else umma_ts(tmem + C::O_COL0 + t * 128, tmem + pcol + k * 8, bd, idO, (acc || k > 0) ? 1u : 0u);
           }
         };
         // The issue stream runs across work items: the next item's first score
@@ -467,9 +497,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           return w < p.n_items ? w : -1;
         };
         auto wait_q = [&](int li) {
-          qb = (li % C::QB) * 2;
-          mbar_wait(&bar_q[qb], (li / C::QB) & 1, p.err, 2);
-          mbar_wait(&bar_q[qb + 1], (li / C::QB) & 1, p.err, 2);
+          qb = (li % C::QB) * NQ;
+          for (int t = 0; t < NQ; ++t) mbar_wait(&bar_q[qb + t], (li / C::QB) & 1, p.err, 2);
           if (li < 15) NT_STAMP(3, 48 + li, 3);  // trace: MMA has Q of item li
         };
         // S_t(0) of an item from its K(0) at ring index g (both tiles)
@@ -477,7 +506,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           const int slotK = g % C::STAGES;
           mbar_wait(&bar_kv_full[slotK], (g / C::STAGES) & 1, p.err, 3);
           tc_fence_after();
-          for (int t = 0; t < 2; ++t) {
+          for (int t = 0; t < NQ; ++t) {
             issue_s(t, slotK);
             umma_commit(&bar_s_full[t]);
             if (n_kv == 1) umma_commit(&bar_q_empty[qb + t]);
@@ -488,7 +517,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         uint32_t p_phase[2] = {0u, 0u};
         uint32_t sf_phase[2] = {0u, 0u};
         int w = fetch(0);
-        int n_kv = w >= 0 ? attn_unit<MASK, SPLIT>(p, unit_prefix, w).n_kv : 0;
+        int n_kv = w >= 0 ? attn_unit<MASK, SPLIT, ROWS>(p, unit_prefix, w).n_kv : 0;
         if (w >= 0) {
           wait_q(0);
           first_s(0, n_kv);
@@ -506,7 +535,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             tc_fence_after();
             if constexpr (C::SEP_P) {
               // S_t(j) waits only until the softmax warps have read S_t(j-1) out of TMEM
-              for (int t = 0; t < 2; ++t) {
+              for (int t = 0; t < NQ; ++t) {
                 mbar_wait(&bar_s_free[t], sf_phase[t], p.err, 15);
                 sf_phase[t] ^= 1u;
                 tc_fence_after();
@@ -516,7 +545,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                 if (j == n_kv - 1) umma_commit(&bar_q_empty[qb + t]);
               }
               umma_commit(&bar_kv_empty[slotK]);
-              for (int t = 0; t < 2; ++t) {
+              for (int t = 0; t < NQ; ++t) {
                 mbar_wait(&bar_p_full[t], p_phase[t], p.err, 4);
                 p_phase[t] ^= 1u;
                 if (t == 0) mbar_wait(&bar_kv_full[slotV], (gV / C::STAGES) & 1, p.err, 5);
@@ -528,14 +557,14 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
               umma_commit(&bar_kv_empty[slotV]);
             } else {
               // P_t(j-1) aliases S_t: PV_t(j-1) then S_t(j), tile 0 then tile 1
-              for (int t = 0; t < 2; ++t) {
+              for (int t = 0; t < NQ; ++t) {
                 mbar_wait(&bar_p_full[t], p_phase[t], p.err, 4);
                 p_phase[t] ^= 1u;
                 if (li == NT_TRACE_LI) NT_STAMP(0, j, 2 + 2 * t);
                 if (t == 0) mbar_wait(&bar_kv_full[slotV], (gV / C::STAGES) & 1, p.err, 5);
                 tc_fence_after();
                 issue_pv(t, slotV, j - 1 > 0);
-                if (t == 1) umma_commit(&bar_kv_empty[slotV]);
+                if (t == NQ - 1) umma_commit(&bar_kv_empty[slotV]);
                 issue_s(t, slotK);
                 umma_commit(&bar_s_full[t]);
                 if (j == n_kv - 1) umma_commit(&bar_q_empty[qb + t]);
@@ -546,12 +575,12 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           }
           // ---- tail: PV_t(n_kv-1) -> O complete, interleaved with the next item's S_t(0)
           const int wn = fetch(li + 1);
-          const int n_next = wn >= 0 ? attn_unit<MASK, SPLIT>(p, unit_prefix, wn).n_kv : 0;
+          const int n_next = wn >= 0 ? attn_unit<MASK, SPLIT, ROWS>(p, unit_prefix, wn).n_kv : 0;
           const int gV = kv_base + 2 * n_kv - 1;
           const int slotV = gV % C::STAGES;
           const int gKn = kv_base + 2 * n_kv;  // ring index of the next item's K(0)
           if constexpr (C::SEP_P) {
-            for (int t = 0; t < 2; ++t) {
+            for (int t = 0; t < NQ; ++t) {
               mbar_wait(&bar_s_free[t], sf_phase[t], p.err, 16);
               sf_phase[t] ^= 1u;
             }
@@ -559,7 +588,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
               wait_q(li + 1);
               first_s(gKn, n_next);
             }
-            for (int t = 0; t < 2; ++t) {
+            for (int t = 0; t < NQ; ++t) {
               mbar_wait(&bar_p_full[t], p_phase[t], p.err, 6);
               p_phase[t] ^= 1u;
               if (t == 0) mbar_wait(&bar_kv_full[slotV], (gV / C::STAGES) & 1, p.err, 7);
@@ -571,7 +600,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             umma_commit(&bar_kv_empty[slotV]);
           } else {
             const int slotKn = gKn % C::STAGES;
-            for (int t = 0; t < 2; ++t) {
+            for (int t = 0; t < NQ; ++t) {
               mbar_wait(&bar_p_full[t], p_phase[t], p.err, 6);
               p_phase[t] ^= 1u;
               if (t == 0) mbar_wait(&bar_kv_full[slotV], (gV / C::STAGES) & 1, p.err, 7);
@@ -599,7 +628,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       }
     }
   } else {
-    if constexpr (kRegSplitLo == 104) asm volatile("setmaxnreg.inc.sync.aligned.u32 200;");
+    if constexpr (NQ == 1) {
+      if constexpr (kRegSplitLo == 72) asm volatile("setmaxnreg.inc.sync.aligned.u32 184;");
+      else if constexpr (kRegSplitLo == 64) asm volatile("setmaxnreg.inc.sync.aligned.u32 192;");
+      else asm volatile("setmaxnreg.inc.sync.aligned.u32 200;");
+    } else if constexpr (kRegSplitLo == 104) asm volatile("setmaxnreg.inc.sync.aligned.u32 200;");
     else if constexpr (kRegSplitLo == 96) asm volatile("setmaxnreg.inc.sync.aligned.u32 204;");
     else asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
     // ================= softmax (+ lazy O correction + epilogue), one thread per query row
@@ -608,7 +641,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     const int r = wq * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
     const uint32_t tS = tmem + t * 128 + lane_off;
-    const uint32_t tO = tmem + 256 + t * 128 + lane_off;
+    const uint32_t tO = tmem + C::O_COL0 + t * 128 + lane_off;
     const uint32_t tP = C::SEP_P ? (tO + 64) : tS;  // where P_t (bf16 pairs) is stored
     const float NINF = f_ninf();
     const float sc = (MASK == MASK_TENSOR) ? 1.0f : p.scale_log2;
@@ -632,9 +665,35 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         uint32_t o[32];
         tmem_ld32(tO + c * 32, o);
         tmem_wait_ld();
+        const bool f32box = OUT_F32 || (SPLIT && pend_part);
+        if (C::F32_BOX_COLS == 16 && f32box) {
+          // two 16-column fp32 boxes: 64-byte rows, chunk q at q ^ ((row >> 1) & 3) (SWIZZLE_64B)
+#pragma unroll
+          for (int hbox = 0; hbox < 2; ++hbox) {
+            if (lane == 0) bulk_wait_read0();
+            __syncwarp();
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int e = hbox * 16 + 4 * q;
+              const uint4 v = make_uint4(__float_as_uint(__uint_as_float(o[e]) * inv),
+                                         __float_as_uint(__uint_as_float(o[e + 1]) * inv),
+                                         __float_as_uint(__uint_as_float(o[e + 2]) * inv),
+                                         __float_as_uint(__uint_as_float(o[e + 3]) * inv));
+              *reinterpret_cast<uint4*>(stg + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)) = v;
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              if (SPLIT && pend_part) tma_store_2d(&tmP, stg, c * 32 + hbox * 16, pend_row0);
+              else tma_store_4d(&tmO, stg, c * 32 + hbox * 16, pend_row0, pend_hq, pend_b);
+              bulk_commit();
+            }
+          }
+          continue;
+        }
         if (lane == 0) bulk_wait_read0();  // this warp's previous box has left shared memory
         __syncwarp();
-        if (OUT_F32 || (SPLIT && pend_part)) {
+        if (f32box) {
           // 128-byte rows, 16-byte chunk q at q ^ (row & 7) (SWIZZLE_128B)
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
@@ -676,7 +735,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_item_empty[slot_i]);
       if (w >= p.n_items) break;
-      const AttnItem itm = attn_unit<MASK, SPLIT>(p, unit_prefix, w);
+      const AttnItem itm = attn_unit<MASK, SPLIT, ROWS>(p, unit_prefix, w);
       const int qi = itm.q_row0 + t * 128 + r;
       float m_run = NINF, l_run = 0.f;
       if (t == 0 && wq == 0 && lane == 0 && li < 16) NT_STAMP(3, 32 + li, 6);  // item start (trace)
@@ -787,9 +846,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       if (SPLIT && itm.split) {
         // partial of a split item: (m, l) per row now, O unnormalised (store_o);
         // a KV range can legitimately miss a causal row (l = 0): the combine checks
-        p.part_ml[(long long)itm.unit * 256 + t * 128 + r] = make_float2(m_run, l_run);
+        p.part_ml[(long long)itm.unit * ROWS + t * 128 + r] = make_float2(m_run, l_run);
         pend_inv = 1.0f;
-        pend_row0 = itm.unit * 256 + t * 128 + wq * 32;
+        pend_row0 = itm.unit * ROWS + t * 128 + wq * 32;
       } else {
         if (valid && !(l_run > 0.f) && p.err) atomicOr(p.err, 1);
         pend_inv = (l_run > 0.f) ? p.o_scale / l_run : 0.f;
@@ -811,7 +870,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, 512);
+    tmem_dealloc(tmem, C::TMEM_COLS);
   }
 #ifdef NT_TRACE
   if (threadIdx.x == 0 && g_nt_cta_times) g_nt_cta_times[blockIdx.x * 3 + 1] = globaltimer();
@@ -831,23 +890,23 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 // w_c = exp2(m_c - max m) (the repair law, tilecc/schedule/repair.py:80-88).
 // Block = 8 rows (one warp per row, D/32 columns per lane) of one (m-block
 // position, batch x head); m-blocks with a single unit exit at once.
-template <int D, int MASK, bool OUT_F32>
+template <int D, int MASK, bool OUT_F32, int ROWS = 256>
 __global__ void __launch_bounds__(256) attn_combine_kernel(const float* __restrict__ part_o, const AttnFwdParams p) {
   const int mbi = blockIdx.z, bh = blockIdx.y;
   const int mb = (MASK == MASK_CAUSAL) ? (p.n_mblocks - 1 - mbi) : mbi;
-  const int n_full = attn_mb_nkv<MASK>(p, mb);
+  const int n_full = attn_mb_nkv<MASK, ROWS>(p, mb);
   const int nc = (n_full + p.kv_split - 1) / p.kv_split;
   if (nc <= 1) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int row = blockIdx.x * 8 + warp;  // 0..255 within the m-block
-  const int qr = mb * 256 + row;
+  const int row = blockIdx.x * 8 + warp;  // 0..ROWS-1 within the m-block
+  const int qr = mb * ROWS + row;
   if (qr >= p.N) return;
   const int BH = p.B * p.Hq;
   const int u0 = p.unit_prefix[mbi] + bh;
   // (m, l) of every chunk in one round trip: lane c holds chunk c (nc <= 32 by construction)
   float mc = f_ninf(), lc = 0.f;
   if (lane < nc) {
-    const float2 ml = p.part_ml[(long long)(u0 + lane * BH) * 256 + row];
+    const float2 ml = p.part_ml[(long long)(u0 + lane * BH) * ROWS + row];
     mc = ml.x;
     lc = ml.y;
   }
@@ -862,8 +921,8 @@ __global__ void __launch_bounds__(256) attn_combine_kernel(const float* __restri
   float acc[CPL];
 #pragma unroll
   for (int i = 0; i < CPL; ++i) acc[i] = 0.f;
-  const float* base = part_o + ((long long)u0 * 256 + row) * D + lane * CPL;
-  const long long cstride = (long long)BH * 256 * D;
+  const float* base = part_o + ((long long)u0 * ROWS + row) * D + lane * CPL;
+  const long long cstride = (long long)BH * ROWS * D;
   for (int c0 = 0; c0 < nc; c0 += 4) {
     float v[4][CPL];
 #pragma unroll

@@ -10,7 +10,7 @@
 #include <string>
 
 #include "../../include/nautilus_b200.h"
-#include "attn_fwd.cuh"
+#include "attn_launch.cuh"
 #include "common_host.h"
 
 namespace nt {
@@ -21,6 +21,7 @@ std::atomic<int64_t> g_launches{0};
 // kernel selection, per-device smem attribute -- which also loads the lazily
 // loaded kernel image) but stop before the launch
 thread_local bool g_prepare_only = false;
+thread_local int g_prepared_ctas_per_sm = 0;
 
 int set_error(int code, const std::string& msg) {
   g_last_error = msg;
@@ -121,12 +122,6 @@ int make_map_pages_5d(CUtensorMap* m, const void* ptr, int64_t page_size, int64_
 }
 
 // ----------------------------------------------------------------- attention
-struct AttnMaps {
-  CUtensorMap q, k, v, o;
-  CUtensorMap p;   // split KV: fp32 partial O [units * 256, D]
-  float* part_o;   // its base
-};
-
 // Split-KV plan (host restatement of attn_unit's prefix): kv_split = 0 unless the
 // heaviest item exceeds 2x the per-SM average of KV-tile steps (few, long items:
 // one kv-group per GPU at 8 GPUs); then items are cut into ~avg/3-tile units.
@@ -137,15 +132,25 @@ struct AttnSplit {
   int kv_split = 0, n_units = 0;
   int64_t bytes = 0, off_ml = 0, off_o = 0;
 };
+// Query rows per work item: 256 (two 128-row tiles, one CTA per SM) or 128 (one
+// tile, two CTAs per SM -- the NQ = 1 instantiations; bf16 Q/K/V only).
+// args->item_rows 0 = library choice.
+static int attn_item_rows(const nt_attn_args* a) {
+  if (a->in_dtype == NT_DTYPE_E4M3) return 256;
+  if (a->item_rows == 128 || a->item_rows == 256) return a->item_rows;
+  return 256;
+}
+
 static AttnSplit attn_split_plan(const nt_attn_args* a) {
   AttnSplit sp;
-  const int nmb = (a->seq_q + 255) / 256, nkv_total = (a->seq_kv + 127) / 128;
+  const int rows = attn_item_rows(a);
+  const int nmb = (a->seq_q + rows - 1) / rows, nkv_total = (a->seq_kv + 127) / 128;
   const long long BH = (long long)a->batch * a->heads_q;
   sp.n_units = (int)(nmb * BH);
   if (nmb > kMaxSplitMblocks || a->mask_kind == NT_MASK_TENSOR) return sp;
   auto nkv = [&](int mb) {
     if (a->mask_kind != NT_MASK_CAUSAL) return nkv_total;
-    const int last_q = std::min(mb * 256 + 255, a->seq_q - 1) + a->causal_offset;
+    const int last_q = std::min(mb * rows + rows - 1, a->seq_q - 1) + a->causal_offset;
     return std::max(std::min(nkv_total, last_q / 128 + 1), 1);
   };
   long long total = 0;
@@ -154,7 +159,8 @@ static AttnSplit attn_split_plan(const nt_attn_args* a) {
     total += nkv(mb) * BH;
     mx = std::max(mx, nkv(mb));
   }
-  const double avg = (double)total / num_sms();
+  // per resident CTA: one per SM with 256-row items, two with 128-row items
+  const double avg = (double)total / (num_sms() * (rows == 128 ? 2 : 1));
   // experiment overrides: NT_ATTN_SPLIT_THRESH (x avg), NT_ATTN_SPLIT_DIV (avg / div tiles per unit)
   static const double thresh = getenv("NT_ATTN_SPLIT_THRESH") ? atof(getenv("NT_ATTN_SPLIT_THRESH")) : 2.0;
   static const double div = getenv("NT_ATTN_SPLIT_DIV") ? atof(getenv("NT_ATTN_SPLIT_DIV")) : 3.0;
@@ -168,87 +174,9 @@ static AttnSplit attn_split_plan(const nt_attn_args* a) {
   sp.n_units = (int)units;
   const int64_t prefix_bytes = ((int64_t)(nmb + 1) * 4 + 255) / 256 * 256;
   sp.off_ml = prefix_bytes;
-  sp.off_o = sp.off_ml + ((int64_t)units * 256 * 8 + 255) / 256 * 256;
-  sp.bytes = sp.off_o + (int64_t)units * 256 * a->head_dim * 4;
+  sp.off_o = sp.off_ml + ((int64_t)units * rows * 8 + 255) / 256 * 256;
+  sp.bytes = sp.off_o + (int64_t)units * rows * a->head_dim * 4;
   return sp;
-}
-
-template <int D, int MASK, bool F32, int KVS, bool FP8, bool SPLIT>
-static int launch_attn_kernel(const AttnMaps& m, const AttnFwdParams& p, cudaStream_t st) {
-  constexpr auto kern = attn_fwd_kernel<D, MASK, F32, KVS, FP8, SPLIT>;
-  const int smem = AttnCfg<D, KVS, F32, FP8>::SMEM_BYTES;
-  if (const int rc0 = configure_smem<kern>(smem, "cudaFuncSetAttribute(attn_fwd)")) return rc0;
-  if (g_prepare_only) {
-    cudaFuncAttributes fa;
-    if constexpr (SPLIT) return check_cuda(cudaFuncGetAttributes(&fa, attn_combine_kernel<D, MASK, F32>),
-                                           "cudaFuncGetAttributes(attn_combine)");
-    return NT_OK;
-  }
-  // persistent: at most one CTA per SM, each walking items blockIdx.x + k * gridDim.x
-  const int grid = std::min(p.n_items, num_sms());
-  kern<<<grid, kAttnThreads, smem, st>>>(m.q, m.k, m.v, m.o, m.p, p);
-  g_launches++;
-  return check_cuda(cudaGetLastError(), "attn_fwd launch");
-}
-
-template <int D, int MASK, bool F32, int KVS, bool FP8 = false>
-static int launch_attn(const AttnMaps& m, const AttnFwdParams& p, cudaStream_t st) {
-  // the split-KV path is its own instantiation: its extra state costs the
-  // unsplit kernel registers (BERT 58 -> 63 us when shared)
-  if constexpr (MASK != MASK_TENSOR) {
-    if (p.kv_split > 0) {
-      int rc = launch_attn_kernel<D, MASK, F32, KVS, FP8, true>(m, p, st);
-      if (rc || g_prepare_only) return rc;
-      // split-KV items: merge the fp32 partials
-      attn_combine_kernel<D, MASK, F32><<<dim3(32, p.B * p.Hq, p.n_mblocks), 256, 0, st>>>(m.part_o, p);
-      g_launches++;
-      return check_cuda(cudaGetLastError(), "attn_combine launch");
-    }
-  }
-  return launch_attn_kernel<D, MASK, F32, KVS, FP8, false>(m, p, st);
-}
-
-template <int D, int MASK, bool F32>
-static int launch_attn_stages(int ma_stages, const AttnMaps& m, const AttnFwdParams& p, cudaStream_t st) {
-  constexpr int kShallow = attn_kv_slots<D>(1), kDeep = attn_kv_slots<D>(2);
-  return attn_kv_slots<D>(ma_stages) == kShallow ? launch_attn<D, MASK, F32, kShallow>(m, p, st)
-                                                 : launch_attn<D, MASK, F32, kDeep>(m, p, st);
-}
-
-// e4m3 Q/K/V (head_dim 128, no / causal mask): 16 KB K/V tiles, ring depth as at D=64
-template <int MASK, bool F32>
-static int launch_attn_e4m3(int ma_stages, const AttnMaps& m, const AttnFwdParams& p, cudaStream_t st) {
-  constexpr int kShallow = attn_kv_slots<64>(1), kDeep = attn_kv_slots<64>(2);
-  return attn_kv_slots<64>(ma_stages) == kShallow ? launch_attn<128, MASK, F32, kShallow, true>(m, p, st)
-                                                  : launch_attn<128, MASK, F32, kDeep, true>(m, p, st);
-}
-
-static int dispatch_attn_e4m3(const nt_attn_args* a, const AttnMaps& m, const AttnFwdParams& p, cudaStream_t st) {
-  const bool f32 = a->out_dtype == NT_DTYPE_F32;
-  const int sg = a->kv_stages > 0 ? a->kv_stages : 2;
-  if (a->mask_kind == NT_MASK_NONE)
-    return f32 ? launch_attn_e4m3<MASK_NONE, true>(sg, m, p, st)
-               : launch_attn_e4m3<MASK_NONE, false>(sg, m, p, st);
-  return f32 ? launch_attn_e4m3<MASK_CAUSAL, true>(sg, m, p, st)
-             : launch_attn_e4m3<MASK_CAUSAL, false>(sg, m, p, st);
-}
-
-template <int D>
-static int dispatch_attn(const nt_attn_args* a, const AttnMaps& m, const AttnFwdParams& p, cudaStream_t st) {
-  const bool f32 = a->out_dtype == NT_DTYPE_F32;
-  const int sg = a->kv_stages > 0 ? a->kv_stages : 2;  // the MA default (VirtualDevice.stage_default)
-  switch (a->mask_kind) {
-    case NT_MASK_NONE:
-      return f32 ? launch_attn_stages<D, MASK_NONE, true>(sg, m, p, st)
-                 : launch_attn_stages<D, MASK_NONE, false>(sg, m, p, st);
-    case NT_MASK_CAUSAL:
-      return f32 ? launch_attn_stages<D, MASK_CAUSAL, true>(sg, m, p, st)
-                 : launch_attn_stages<D, MASK_CAUSAL, false>(sg, m, p, st);
-    case NT_MASK_TENSOR:
-      return f32 ? launch_attn_stages<D, MASK_TENSOR, true>(sg, m, p, st)
-                 : launch_attn_stages<D, MASK_TENSOR, false>(sg, m, p, st);
-  }
-  return set_error(NT_ERR_INVALID, "unknown mask_kind");
 }
 
 }  // namespace nt
@@ -264,9 +192,15 @@ extern "C" int nt_attn_fwd(const nt_attn_args* a, void* stream);
 
 extern "C" int nt_attn_prepare(const nt_attn_args* a) {
   g_prepare_only = true;
+  g_prepared_ctas_per_sm = 0;
   const int rc = nt_attn_fwd(a, nullptr);
   g_prepare_only = false;
   return rc;
+}
+
+extern "C" int nt_attn_resident_ctas(const nt_attn_args* a) {
+  const int rc = nt_attn_prepare(a);
+  return rc ? -rc : g_prepared_ctas_per_sm;
 }
 
 extern "C" int nt_attn_fwd(const nt_attn_args* a, void* stream) {
@@ -280,6 +214,11 @@ extern "C" int nt_attn_fwd(const nt_attn_args* a, void* stream) {
   if (a->mask_kind == NT_MASK_TENSOR && !a->mask) return set_error(NT_ERR_INVALID, "tensor mask missing");
   const bool e4m3 = a->in_dtype == NT_DTYPE_E4M3;
   if (a->in_dtype != NT_DTYPE_BF16 && !e4m3) return set_error(NT_ERR_UNSUPPORTED, "q/k/v must be bf16 or e4m3");
+  if (a->item_rows != 0 && a->item_rows != 128 && a->item_rows != 256)
+    return set_error(NT_ERR_INVALID, "item_rows must be 0, 128 or 256");
+  if (e4m3 && a->item_rows == 128) return set_error(NT_ERR_UNSUPPORTED, "e4m3 attention: 256-row items only");
+  const int rows = attn_item_rows(a);
+  const int nq = rows / 128;
   if (e4m3 && (a->head_dim != 128 || a->mask_kind == NT_MASK_TENSOR))
     return set_error(NT_ERR_UNSUPPORTED, "e4m3 attention: head_dim 128, no or causal mask");
   const int D = a->head_dim;
@@ -302,9 +241,11 @@ extern "C" int nt_attn_fwd(const nt_attn_args* a, void* stream) {
   if (reinterpret_cast<uintptr_t>(a->o.ptr) % 16 || (a->o.stride_s * (f32 ? 4 : 2)) % 16 ||
       (a->o.stride_h * (f32 ? 4 : 2)) % 16 || (a->o.stride_b * (f32 ? 4 : 2)) % 16)
     return set_error(NT_ERR_INVALID, "output must be 16B aligned with 16B-multiple strides");
+  // fp32 boxes: 32 columns (SWIZZLE_128B), or 16 (SWIZZLE_64B) for 128-row items (AttnCfg::F32_BOX_COLS)
+  const int f32_cols = nq == 1 ? 16 : 32;
   if ((rc = make_map_4d(&mo, a->o.ptr, D, a->seq_q, a->heads_q, a->batch, a->o.stride_s, a->o.stride_h,
-                        a->o.stride_b, 32, f32 ? 4 : 2, 32,
-                        f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B)))
+                        a->o.stride_b, 32, f32 ? 4 : 2, f32 ? f32_cols : 32,
+                        (f32 && f32_cols == 32) ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B)))
     return rc;
   AttnFwdParams p{};
   p.B = a->batch;
@@ -313,7 +254,7 @@ extern "C" int nt_attn_fwd(const nt_attn_args* a, void* stream) {
   p.N = a->seq_q;
   p.M = a->seq_kv;
   p.q_per_kv = a->heads_q / a->heads_kv;
-  p.n_mblocks = (a->seq_q + 255) / 256;
+  p.n_mblocks = (a->seq_q + rows - 1) / rows;
   p.n_kv_total = (a->seq_kv + 127) / 128;
   p.n_items = p.n_mblocks * a->batch * a->heads_q;
   p.causal_offset = a->causal_offset;
@@ -339,14 +280,15 @@ extern "C" int nt_attn_fwd(const nt_attn_args* a, void* stream) {
     p.unit_prefix = reinterpret_cast<int*>(ws);
     p.part_ml = reinterpret_cast<float2*>(ws + sp.off_ml);
     m.part_o = reinterpret_cast<float*>(ws + sp.off_o);
-    if ((rc = make_map_2d(&m.p, m.part_o, D, (int64_t)sp.n_units * 256, D, 32, 32, 4, CU_TENSOR_MAP_SWIZZLE_128B)))
+    if ((rc = make_map_2d(&m.p, m.part_o, D, (int64_t)sp.n_units * rows, D, f32_cols, 32, 4,
+                          f32_cols == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B)))
       return rc;
   } else {
     m.p = m.o;  // unused (no split)
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (e4m3) return dispatch_attn_e4m3(a, m, p, st);
-  return D == 64 ? dispatch_attn<64>(a, m, p, st) : dispatch_attn<128>(a, m, p, st);
+  return D == 64 ? dispatch_attn_d64(a, m, p, nq, st) : dispatch_attn_d128(a, m, p, nq, st);
 }
 
 // ----------------------------------------------------------------- casts

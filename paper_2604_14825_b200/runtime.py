@@ -54,7 +54,7 @@ class AttentionPlan:
                  scale: Optional[float], mask_kind: str = "none", mask: Optional[torch.Tensor] = None,
                  causal_offset: int = 0, err_flag: Optional[torch.Tensor] = None, kv_stages: int = 0,
                  q_descale: float = 1.0, k_descale: float = 1.0, v_descale: float = 1.0,
-                 work_counter: Optional[torch.Tensor] = None):
+                 work_counter: Optional[torch.Tensor] = None, item_rows: int = 0):
         q, k, v, o = _as4(q), _as4(k), _as4(v), _as4(o)
         e4m3 = q.dtype == torch.float8_e4m3fn
         want = torch.float8_e4m3fn if e4m3 else torch.bfloat16
@@ -92,18 +92,21 @@ class AttentionPlan:
         a.kv_stages = int(kv_stages)  # the MA `stages` tunable (0 = scheduler default)
         a.in_dtype = _lib.NT_DTYPE_E4M3 if e4m3 else _lib.NT_DTYPE_BF16
         a.q_descale, a.k_descale, a.v_descale = float(q_descale), float(k_descale), float(v_descale)
+        a.item_rows = int(item_rows)  # 0 = library choice, 128 or 256 query rows per work item
         # split-KV workspace (non-zero only for few, long work items)
         ws = int(_lib.lib().nt_attn_workspace_bytes(C.byref(a)))
         self.ws = torch.empty(ws, dtype=torch.uint8, device=q.device) if ws else None
         a.workspace = self.ws.data_ptr() if ws else None
         a.workspace_bytes = ws
-        self.kv_slots = attn_kv_slots(64 if e4m3 else D, kv_stages)  # e4m3 K/V tiles are D=64-sized
+        self.item_rows = int(item_rows) if item_rows else 256
+        self.kv_slots = attn_kv_slots(64 if e4m3 else D, kv_stages, self.item_rows // 128)  # e4m3: D=64-sized tiles
         self.args = a
         self.shape = (B, Hq, Hkv, N, M, D)
         self._fn = _lib.lib().nt_attn_fwd
         self._ref = C.byref(a)
         # validate + load the kernel now, so the first launch is a plain launch
         _lib.check(_lib.lib().nt_attn_prepare(self._ref), "nt_attn_prepare")
+        self.ctas_per_sm = int(_lib.lib().nt_attn_resident_ctas(self._ref))
 
     def launch(self, stream=None) -> None:
         st = self._fn(self._ref, _stream_handle(stream))
@@ -127,9 +130,11 @@ class AttentionPlan:
             raise RuntimeError(f"device pipeline timeout (wait codes {[c for c in range(16) if flag >> (8 + c) & 1]})")
 
 
-def attn_kv_slots(d: int, ma_stages: int) -> int:
+def attn_kv_slots(d: int, ma_stages: int, nq: int = 2) -> int:
     """K/V ring slots K1 uses for an MA `stages` value (csrc/attn_fwd.cuh attn_kv_slots)."""
     st = ma_stages if ma_stages > 0 else 2
+    if nq == 1:
+        return 2 if d == 128 else (2 if st <= 1 else 4)
     if d == 128:
         return 2 if st <= 1 else 4
     return 4 if st <= 1 else 8

@@ -496,3 +496,90 @@ def test_split_kv_not_used_for_full_grids():
     kv = torch.zeros((1, 8, 8192, 128), device=dev, dtype=torch.bfloat16)
     plan = AttentionPlan(q, kv, kv, torch.empty_like(q), 0.088, "causal")
     assert plan.ws is None and int(_lib.lib().nt_attn_workspace_bytes(plan._ref)) == 0
+
+
+# ------------------------------------------------------------ 128-row work items (NQ = 1)
+@pytest.mark.parametrize("B,Hq,Hkv,N,M,D,kind,out_f32,stages", [
+    (2, 8, 2, 1024, 1024, 128, "causal", False, 2),
+    (1, 2, 2, 1000, 1000, 128, "causal", True, 2),    # ragged, fp32 16-column boxes
+    (4, 12, 12, 512, 512, 64, "none", False, 2),      # BERT-like
+    (2, 3, 3, 512, 512, 64, "none", True, 1),
+    (1, 2, 1, 384, 700, 64, "none", True, 2),         # N != M, ragged KV
+    (1, 1, 1, 200, 256, 64, "tensor", True, 2),
+    (1, 1, 1, 129, 129, 128, "tensor", False, 2),
+    (16, 12, 12, 512, 64 * 8, 64, "none", True, 4),   # more items than 2 x SMs
+])
+def test_item_rows_128_is_bitwise_the_256_row_result(B, Hq, Hkv, N, M, D, kind, out_f32, stages):
+    """One query tile per CTA (two CTAs per SM) computes each row exactly as the two-tile
+    CTA does: same MMA tiles, same KV order, same per-warp rescale decisions -> same bits."""
+    from paper_2604_14825_b200.runtime import AttentionPlan
+
+    dev = torch.device("cuda")
+    q = torch.from_numpy(_rand((B, Hq, N, D), 71)).to(dev).bfloat16()
+    k = torch.from_numpy(_rand((B, Hkv, M, D), 72)).to(dev).bfloat16()
+    v = torch.from_numpy(_rand((B, Hkv, M, D), 73)).to(dev).bfloat16()
+    mask = None
+    if kind == "tensor":
+        g = np.random.default_rng(74)
+        mk = np.where(g.random((N, M)) < 0.3, -np.inf, g.standard_normal((N, M)) * 0.5).astype(np.float32)
+        mk[:, 0] = 0.0
+        mask = torch.from_numpy(mk).to(dev)
+    outs, split = [], False
+    for rows in (256, 128):
+        o = torch.full((B, Hq, N, D), float("nan"), dtype=torch.float32 if out_f32 else torch.bfloat16, device=dev)
+        plan = AttentionPlan(q, k, v, o, D ** -0.5, kind, mask, kv_stages=stages, item_rows=rows)
+        split = split or plan.ws is not None  # small grids may split KV (other fp order)
+        assert plan.ctas_per_sm == (2 if rows == 128 else 1)
+        for _ in range(3):  # repeated launches: the self-resetting counter with 2 CTAs per SM
+            plan.launch()
+        torch.cuda.synchronize()
+        plan.check_errors()
+        assert plan.work.tolist() == [0, 0]
+        outs.append(o)
+    if not split:
+        assert torch.equal(outs[0], outs[1])
+    qn, kn, vn = (t.float().cpu().numpy() for t in (q, k, v))
+    if kind == "tensor":
+        ref = reference_math.attention_fp64(qn[0, 0], kn[0, 0], vn[0, 0], D ** -0.5, mk)[None, None]
+    else:
+        ref = reference_math.attention_batched_fp64(qn, kn, vn, D ** -0.5, kind == "causal")
+    _check(outs[1].float().cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,N,M,D,causal,out_f32", [
+    (1, 4, 1, 8192, 8192, 128, True, False),
+    (1, 2, 1, 3000, 3000, 64, True, True),
+    (2, 1, 1, 2048, 5000, 64, False, False),
+])
+def test_item_rows_128_split_kv_vs_fp64(B, Hq, Hkv, N, M, D, causal, out_f32):
+    from paper_2604_14825_b200.runtime import AttentionPlan
+
+    scale = 1.0 / np.sqrt(D)
+    q, k, v = _rand((B, Hq, N, D), 81), _rand((B, Hkv, M, D), 82), _rand((B, Hkv, M, D), 83)
+    dev = torch.device("cuda")
+    o = torch.full((B, Hq, N, D), float("nan"), dtype=torch.float32 if out_f32 else torch.bfloat16, device=dev)
+    plan = AttentionPlan(*(torch.from_numpy(x).to(dev).to(torch.bfloat16) for x in (q, k, v)), o, scale,
+                         "causal" if causal else "none", item_rows=128)
+    assert plan.ws is not None, "expected the split-KV path for this shape"
+    plan.launch()
+    torch.cuda.synchronize()
+    plan.check_errors()
+    first = o.clone()
+    plan.launch()
+    torch.cuda.synchronize()
+    assert torch.equal(o, first)
+    _check(o.float().cpu().numpy(), reference_math.attention_batched_fp64(q, k, v, scale, causal))
+
+
+def test_item_rows_rejects_bad_values():
+    from paper_2604_14825_b200.errors import InvalidArguments, UnsupportedMA
+    from paper_2604_14825_b200.runtime import AttentionPlan
+
+    dev = torch.device("cuda")
+    q = torch.zeros((1, 1, 128, 128), device=dev).bfloat16()
+    o = torch.empty((1, 1, 128, 128), device=dev)
+    with pytest.raises(InvalidArguments):
+        AttentionPlan(q, q, q, o, 0.1, "none", item_rows=64)
+    q8 = q.to(torch.float8_e4m3fn)
+    with pytest.raises(UnsupportedMA):
+        AttentionPlan(q8, q8, q8, o, 0.1, "none", item_rows=128)

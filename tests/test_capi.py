@@ -24,14 +24,15 @@ def test_library_loads_and_exports_all_symbols():
     L = _lib.lib()
     for name in declared_symbols():
         assert hasattr(L, name), name
-    assert L.nt_abi_version() == 2
+    assert L.nt_abi_version() == 3
     assert L.nt_launch_count() >= 0
 
 
 def test_struct_layouts_match_header():
     # sizes computed from the header's field order (x86-64 SysV)
     assert ctypes.sizeof(_lib.Tensor4) == 32
-    assert ctypes.sizeof(_lib.AttnArgs) == 4 * 32 + 6 * 4 + 4 + 4 + 4 + 4 + 8 + 8 + 4 + 4 + 8 + 8 + 4 + 4 + 3 * 4 + 4 + 8 + 8
+    # ... + item_rows (int32, ABI 3) + tail padding to 8
+    assert ctypes.sizeof(_lib.AttnArgs) == 4 * 32 + 6 * 4 + 4 + 4 + 4 + 4 + 8 + 8 + 4 + 4 + 8 + 8 + 4 + 4 + 3 * 4 + 4 + 8 + 8 + 4 + 4
     assert ctypes.sizeof(_lib.GemmArgs) == 6 * 8 + 4 * 4 + 4 + 4 + 8 + 8
 
 

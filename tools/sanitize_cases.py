@@ -25,6 +25,14 @@ from oracle.ma_interp import round_bf16  # noqa: E402
 DEV = torch.device("cuda")
 
 
+def nan_filled(shape, dtype, device):
+    """Outputs start as NaN (written by a plain fill kernel): initcheck then sees
+    initialised memory -- it does not track TMA (cp.async.bulk.tensor) stores, so a
+    torch.empty output written only by TMA stores reads as uninitialised -- and the
+    NaN-free check in close() proves every element was overwritten by the kernel."""
+    return torch.full(shape, float("nan"), dtype=dtype, device=device)
+
+
 def rnd(shape, seed, scale=1.0):
     return round_bf16(np.random.default_rng(seed).standard_normal(shape) * scale)
 
@@ -55,7 +63,7 @@ def k1():
             mask = np.where(g.random((N, M)) < 0.3, -np.inf, 0.0).astype(np.float32)
             mask[:, 0] = 0.0
         tq, tk, tv = (torch.from_numpy(x).to(DEV).bfloat16() for x in (q, k, v))
-        o = torch.empty((B, Hq, N, D), dtype=torch.float32 if f32 else torch.bfloat16, device=DEV)
+        o = nan_filled((B, Hq, N, D), dtype=torch.float32 if f32 else torch.bfloat16, device=DEV)
         plan = AttentionPlan(tq, tk, tv, o, 1 / np.sqrt(D), kind,
                              torch.from_numpy(mask).to(DEV) if mask is not None else None)
         plan.launch()
@@ -71,7 +79,7 @@ def k1():
     q, k, v = rnd((B, Hq, N, D), 5), rnd((B, Hkv, N, D), 6), rnd((B, Hkv, N, D), 7)
     tq, tk, tv = (torch.from_numpy(x).to(DEV).to(torch.float8_e4m3fn) for x in (q, k, v))
     deq = [t.float().cpu().numpy() for t in (tq, tk, tv)]
-    o = torch.empty((B, Hq, N, D), dtype=torch.float32, device=DEV)
+    o = nan_filled((B, Hq, N, D), dtype=torch.float32, device=DEV)
     plan = AttentionPlan(tq, tk, tv, o, 1 / np.sqrt(D), "causal")
     plan.launch()
     torch.cuda.synchronize()
@@ -85,7 +93,7 @@ def k2():
     B, Hq, Hkv, D, M = 2, 8, 2, 128, 1500
     q, k, v = rnd((B, Hq, 1, D), 8), rnd((B, Hkv, M, D), 9), rnd((B, Hkv, M, D), 10)
     tq, tk, tv = (torch.from_numpy(x).to(DEV).bfloat16() for x in (q, k, v))
-    o = torch.empty((B, Hq, 1, D), dtype=torch.float32, device=DEV)
+    o = nan_filled((B, Hq, 1, D), dtype=torch.float32, device=DEV)
     plan = DecodePlan(tq, tk, tv, o, 1 / np.sqrt(D), num_splits=3)
     plan.launch()
     torch.cuda.synchronize()
@@ -123,7 +131,7 @@ def k3():
 
     for M, N, K, f32 in ((2048, 2048, 512, False), (256, 128, 2048, True)):
         a, b = rnd((M, K), 11), rnd((K, N), 12, 1 / np.sqrt(K))
-        c = torch.empty((M, N), dtype=torch.float32 if f32 else torch.bfloat16, device=DEV)
+        c = nan_filled((M, N), dtype=torch.float32 if f32 else torch.bfloat16, device=DEV)
         plan = GemmPlan(torch.from_numpy(a).to(DEV).bfloat16(), torch.from_numpy(b).to(DEV).bfloat16(), c)
         plan.launch()
         torch.cuda.synchronize()
@@ -135,7 +143,7 @@ def chain():
 
     N, K, F, E = 256, 256, 512, 128
     x, w1, w2 = rnd((N, K), 13), rnd((K, F), 14, 1 / 16), rnd((F, E), 15, 1 / np.sqrt(F))
-    y = torch.empty((N, E), dtype=torch.float32, device=DEV)
+    y = nan_filled((N, E), dtype=torch.float32, device=DEV)
     plan = ChainPlan(*(torch.from_numpy(t).to(DEV).bfloat16() for t in (x, w1, w2)), y)
     assert plan.fused
     plan.launch()
