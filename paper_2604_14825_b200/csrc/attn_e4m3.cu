@@ -2,6 +2,7 @@
 #include "attn_launch.cuh"
 
 namespace nt {
+NT_DEFINE_TRACE_SETTER(trace_set_e4m3)
 int dispatch_attn_e4m3(const nt_attn_args* a, const AttnMaps& m, const AttnFwdParams& p, cudaStream_t st) {
   return dispatch_attn_nq<128, true, 2>(a, m, p, st);
 }

@@ -90,18 +90,34 @@ constexpr int kAttnThreads = attn_threads<2>();
 #endif
 constexpr int kItemRing = 4;  // work-item slots handed from the producer to the MMA / softmax warps
 constexpr float kRescaleLog2 = 8.0f;
-// Fraction of exp2 evaluated by the FMA-pipe polynomial instead of MUFU.EX2
-// (1 in NT_POLY_EVERY pairs; 0 = MUFU only).
-#ifndef NT_POLY_EVERY
-#define NT_POLY_EVERY 0
+// exp2 on the FMA pipe: 1 in POLY_EVERY pairs of P go through the degree-3
+// polynomial (ex2_poly2) instead of MUFU.EX2 (0 = MUFU only), per head dim.
+#ifndef NT_POLY_EVERY_D64
+#define NT_POLY_EVERY_D64 8  // BERT 58.8 -> 57.5 us with the late PV wait (A/B, r02); D=128: 1/8 slower (446 -> 456 us)
 #endif
-constexpr bool kPolyExp = NT_POLY_EVERY > 0;
-// P -> bf16 pack: 0 = cvt.rn.bf16x2.f32 (F2FP, on the XU pipe beside MUFU.EX2),
-// 1 = integer add + byte permute (ALU pipe).
-#ifndef NT_PACK_ALU
-#define NT_PACK_ALU 0
+#ifndef NT_POLY_EVERY_D128
+#define NT_POLY_EVERY_D128 0
 #endif
-constexpr int kPolyEvery = NT_POLY_EVERY > 0 ? NT_POLY_EVERY : 1;
+// P -> bf16 pack: 0 = cvt.rn.bf16x2.f32 (F2FP), 1 = integer add + byte permute
+// (round half up, ALU pipe), 2 = byte permute only (truncation, ALU pipe) with
+// the exponent pre-biased by log2(1 + E[rel. truncation error]) so P is
+// unbiased on average and l divided by the same factor (kTruncScale).
+#ifndef NT_PACK_D64
+#define NT_PACK_D64 0
+#endif
+#ifndef NT_PACK_D128
+#define NT_PACK_D128 0
+#endif
+// D=64 (SEP_P): wait for PV_t(j-1) after the exp pass instead of before it
+#ifndef NT_SEP_P_LATE
+#define NT_SEP_P_LATE 1
+#endif
+template <int D> constexpr int attn_poly_every() { return D == 64 ? NT_POLY_EVERY_D64 : NT_POLY_EVERY_D128; }
+template <int D> constexpr int attn_pack_mode() { return D == 64 ? NT_PACK_D64 : NT_PACK_D128; }
+// mean relative truncation error of a bf16 (7 stored mantissa bits) under
+// Benford-distributed mantissas: 2^-8 * (1/ln 2) * (1 - 1/2) = 2.818e-3
+constexpr float kTruncScale = 1.0028177f;
+constexpr float kTruncLog2 = 0.0040601f;  // log2(kTruncScale)
 
 // KV ring depth in 128-key K or V tiles.  The MA kernel's `stages` tunable
 // (SetParam stages, tilecc/autosched/scheduler.py:116-124) picks it: stages = 1
@@ -174,11 +190,12 @@ __device__ __forceinline__ void attn_rescale_o(uint32_t tO, float alpha) {
 // P = exp2(S*sc - m) for one 128-key row, packed into pk (bf16 pairs, or e4m3
 // quads when FP8: 64 / 32 words) and, when STORE, written to TMEM at tP chunk by
 // chunk; returns the row sum of P (fp32, before rounding).
-template <bool FP8, bool STORE>
+template <bool FP8, bool STORE, int POLY = 0, int PACK = 0, bool EXACT_ZERO = true>
 __device__ __forceinline__ float attn_exp_pass(const uint32_t (&s)[128], float sc, float m, uint32_t tP,
                                                uint32_t (&pk)[64]) {
   const float2 sc2 = make_float2(sc, sc);
-  const float2 nm2 = make_float2(-m, -m);
+  const float mb = (PACK == 2 && !FP8) ? -m + kTruncLog2 : -m;
+  const float2 nm2 = make_float2(mb, mb);
   float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
   for (int ch = 0; ch < 4; ++ch) {
@@ -188,8 +205,8 @@ __device__ __forceinline__ float attn_exp_pass(const uint32_t (&s)[128], float s
       const float s0 = __uint_as_float(s[ch * 32 + 2 * i]), s1 = __uint_as_float(s[ch * 32 + 2 * i + 1]);
       const float2 x = ffma2(make_float2(s0, s1), sc2, nm2);
       float2 e;
-      if (kPolyExp && (i % kPolyEvery) == kPolyEvery - 1) {
-        e = ex2_poly2(x);  // FMA-pipe exp2 for 1/kPolyEvery of the pairs
+      if (POLY > 0 && (i % POLY) == POLY - 1) {
+        e = ex2_poly2<EXACT_ZERO>(x);  // FMA-pipe exp2 for 1/POLY of the pairs
       } else {
         e = make_float2(ex2(x.x), ex2(x.y));
       }
@@ -198,7 +215,8 @@ __device__ __forceinline__ float attn_exp_pass(const uint32_t (&s)[128], float s
         if (i & 1) pk[ch * 8 + (i >> 1)] = pack_e4m3x4(prev.x, prev.y, e.x, e.y);
         prev = e;
       } else {
-        pk[ch * 16 + i] = NT_PACK_ALU ? pack_bf16_alu(e.x, e.y) : pack_bf16(e.x, e.y);
+        pk[ch * 16 + i] = PACK == 2 ? pack_bf16_trunc(e.x, e.y)
+                          : PACK == 1 ? pack_bf16_alu(e.x, e.y) : pack_bf16(e.x, e.y);
       }
     }
     if (STORE) {
@@ -307,6 +325,8 @@ __global__ void __launch_bounds__(attn_threads<NQ>(), NQ == 2 ? 1 : 2)
                     const __grid_constant__ CUtensorMap tmP, const AttnFwdParams p) {
   using C = AttnCfg<D, KVS, OUT_F32, FP8, NQ, SPLIT>;
   constexpr int ROWS = C::ROWS;
+  constexpr int kPoly = FP8 ? 0 : attn_poly_every<D>();
+  constexpr int kPack = FP8 ? 0 : attn_pack_mode<D>();
   // register split between warpgroup 0 (producer / MMA issuer) and the softmax
   // warpgroups: NQ = 2: 128 x lo + 256 x hi = 384 x 168; NQ = 1 (two CTAs per
   // SM): 128 x lo + 128 x hi = 256 x 128
@@ -790,7 +810,8 @@ __global__ void __launch_bounds__(attn_threads<NQ>(), NQ == 2 ? 1 : 2)
           mx = fmaxf(fmax3(a0, a1, a2), a3);
         }
         if (li == NT_TRACE_LI && lane == 0 && wq == 0) NT_STAMP(1 + t, j, 3);
-        if (C::SEP_P && j > 0) {
+        constexpr bool kLate = C::SEP_P && NT_SEP_P_LATE;
+        if (C::SEP_P && !kLate && j > 0) {
           // PV_t(j-1) must be complete before O_t is rescaled or P_t overwritten;
           // completions up to j-2 were waited for at j-1, so the parity is exact
           mbar_wait(&bar_pv_done[t], (pv_base + j - 1) & 1, p.err, 10);
@@ -798,20 +819,37 @@ __global__ void __launch_bounds__(attn_threads<NQ>(), NQ == 2 ? 1 : 2)
         }
         const float m_new = fmaxf(m_run, mx * sc);
         const bool need = m_new > m_run + kRescaleLog2;
-        if (__any_sync(0xffffffffu, need)) {
-          const float alpha = (m_new == NINF) ? 1.0f : ex2(m_run - m_new);
-          if (j > 0) attn_rescale_o<D>(tO, alpha);
+        float alpha = 1.0f;
+        const bool rescale = __any_sync(0xffffffffu, need);
+        if (rescale) {
+          alpha = (m_new == NINF) ? 1.0f : ex2(m_run - m_new);
+          if (!kLate && j > 0) attn_rescale_o<D>(tO, alpha);
           l_run *= alpha;
           m_run = m_new;
         }
         const float m_use = (m_run == NINF) ? 0.f : m_run;
         uint32_t pk[64];
         float sum;
-        if (j == 0 && pend) {
+        if (kLate) {
+          // SEP_P (D=64): P_t(j) overwrites P_t(j-1) and O_t is rescaled only after
+          // PV_t(j-1) completed -- wait for that AFTER the exps (into registers), so
+          // the PV latency hides behind them instead of stalling the exp phase
+          sum = attn_exp_pass<FP8, false, kPoly, kPack, MASK != MASK_NONE>(s, sc, m_use, tP, pk);
+          if (j == 0 && pend) {
+            store_o();  // the previous item's O (its last PV waited inside)
+            pend = false;
+          } else if (j > 0) {
+            mbar_wait(&bar_pv_done[t], (pv_base + j - 1) & 1, p.err, 10);
+            tc_fence_after();
+            if (rescale) attn_rescale_o<D>(tO, alpha);
+          }
+#pragma unroll
+          for (int c = 0; c < 4; ++c) tmem_st16(tP + c * 16, pk + c * 16);
+        } else if (j == 0 && pend) {
           // first tile of an item while the previous item's O is still in TMEM:
           // exps into registers, then that epilogue (its last PV has had the S load,
           // max and exps to finish), then P -- PV(0) may overwrite O only after it
-          sum = attn_exp_pass<FP8, false>(s, sc, m_use, tP, pk);
+          sum = attn_exp_pass<FP8, false, kPoly, kPack, MASK != MASK_NONE>(s, sc, m_use, tP, pk);
           store_o();
           pend = false;
           if (!FP8) {
@@ -822,7 +860,7 @@ __global__ void __launch_bounds__(attn_threads<NQ>(), NQ == 2 ? 1 : 2)
             tmem_st16(tP + 16, pk + 16);
           }
         } else {
-          sum = attn_exp_pass<FP8, true>(s, sc, m_use, tP, pk);
+          sum = attn_exp_pass<FP8, true, kPoly, kPack, MASK != MASK_NONE>(s, sc, m_use, tP, pk);
         }
         if (li == NT_TRACE_LI && lane == 0 && wq == 0) NT_STAMP(1 + t, j, 4);
         l_run += sum;
@@ -834,6 +872,7 @@ __global__ void __launch_bounds__(attn_threads<NQ>(), NQ == 2 ? 1 : 2)
       }
 
       pv_base += itm.n_kv;
+      if (kPack == 2) l_run *= 1.0f / kTruncScale;  // P was pre-biased by kTruncScale before truncation
 
       // ---- epilogue.  D=64 (short items): deferred into the next item's first
       // tile, where it overlaps the last PV's latency with that tile's S load, max

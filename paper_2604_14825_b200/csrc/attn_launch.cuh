@@ -132,6 +132,26 @@ int dispatch_attn_nq(const nt_attn_args* a, const AttnMaps& m, const AttnFwdPara
   return set_error(NT_ERR_INVALID, "unknown mask_kind");
 }
 
+#ifdef NT_TRACE
+// The trace symbols (attn_fwd.cuh) exist once per translation unit: every TU that
+// instantiates K1 defines a setter, capi.cu's nt_debug_set_trace calls them all.
+#define NT_DEFINE_TRACE_SETTER(NAME)                                                       \
+  void NAME(unsigned long long* buf, int cta, int item, unsigned long long* cta_times, int what) { \
+    if (what == 0) {                                                                       \
+      cudaMemcpyToSymbol(g_nt_trace, &buf, sizeof(buf));                                   \
+      cudaMemcpyToSymbol(g_nt_trace_cta, &cta, sizeof(cta));                               \
+      cudaMemcpyToSymbol(g_nt_trace_li, &item, sizeof(item));                              \
+    } else {                                                                               \
+      cudaMemcpyToSymbol(g_nt_cta_times, &cta_times, sizeof(cta_times));                   \
+    }                                                                                      \
+  }
+void trace_set_d64(unsigned long long*, int, int, unsigned long long*, int);
+void trace_set_d128(unsigned long long*, int, int, unsigned long long*, int);
+void trace_set_e4m3(unsigned long long*, int, int, unsigned long long*, int);
+#else
+#define NT_DEFINE_TRACE_SETTER(NAME)
+#endif
+
 // defined in attn_d64.cu / attn_d128.cu / attn_e4m3.cu
 int dispatch_attn_d64(const nt_attn_args* a, const AttnMaps& m, const AttnFwdParams& p, int nq, cudaStream_t st);
 int dispatch_attn_d128(const nt_attn_args* a, const AttnMaps& m, const AttnFwdParams& p, int nq, cudaStream_t st);

@@ -338,13 +338,11 @@ extern "C" int nt_cast_bf16_to_f32(const void* src, float* dst, int64_t n, void*
 #ifdef NT_TRACE
 // debug builds only: route the K1 pipeline timeline stamps of one CTA into `buf`
 extern "C" int nt_debug_set_trace(unsigned long long* buf, int cta, int item) {
-  cudaMemcpyToSymbol(nt::g_nt_trace, &buf, sizeof(buf));
-  cudaMemcpyToSymbol(nt::g_nt_trace_cta, &cta, sizeof(cta));
-  cudaMemcpyToSymbol(nt::g_nt_trace_li, &item, sizeof(item));
+  for (auto f : {trace_set_d64, trace_set_d128, trace_set_e4m3}) f(buf, cta, item, nullptr, 0);
   return check_cuda(cudaGetLastError(), "nt_debug_set_trace");
 }
 extern "C" int nt_debug_set_cta_times(unsigned long long* buf) {
-  cudaMemcpyToSymbol(nt::g_nt_cta_times, &buf, sizeof(buf));
+  for (auto f : {trace_set_d64, trace_set_d128, trace_set_e4m3}) f(nullptr, 0, 0, buf, 1);
   return check_cuda(cudaGetLastError(), "nt_debug_set_cta_times");
 }
 #endif

@@ -355,6 +355,13 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return r;
 }
 
+// fp32 pair -> bf16x2 by truncation (one PRMT on the ALU pipe): the caller
+// pre-biases the values so the truncation is unbiased on average (K1 kTruncScale)
+__device__ __forceinline__ uint32_t pack_bf16_trunc(float lo, float hi) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, 0x7632;" : "=r"(r) : "r"(__float_as_uint(lo)), "r"(__float_as_uint(hi)));
+  return r;
+}
 // fp32 pair -> bf16x2 on the integer pipe (round half away from zero on the
 // dropped 16 bits; ties are measure-zero for softmax probabilities).  The
 // cvt.rn.bf16x2.f32 (F2FP) alternative issues on the same XU pipe as
@@ -405,9 +412,12 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
 // far below the bf16 rounding P gets next), 2^j added to the exponent bits.
 // x is clamped at -126 so the exponent add cannot wrap below the denormal
 // range; inputs below -126 (masked -inf entries) return exactly 0.
+// EXACT_ZERO = false (no masked -inf inputs possible): inputs below -126 give
+// 2^-126-ish instead of 0, saving the compare / select.
+template <bool EXACT_ZERO = true>
 __device__ __forceinline__ float2 ex2_poly2(float2 x) {
   const float2 magic = make_float2(12582912.0f, 12582912.0f);  // 1.5 * 2^23
-  const bool z0 = x.x < -126.0f, z1 = x.y < -126.0f;  // exp2 underflows: exact 0 (masked -inf)
+  const bool z0 = EXACT_ZERO && x.x < -126.0f, z1 = EXACT_ZERO && x.y < -126.0f;  // masked -inf -> exact 0
   x.x = fmaxf(x.x, -126.0f);
   x.y = fmaxf(x.y, -126.0f);
   const float2 t = fadd2(x, magic);

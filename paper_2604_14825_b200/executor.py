@@ -40,7 +40,7 @@ from . import _lib, cost
 from . import ma_ir as ir
 from .errors import DivisionByZero, OutOfBounds, UnsupportedMA
 from .recognize import AttentionSpec, GemmChainSpec, recognize
-from .runtime import AttentionPlan, DecodePlan, decode_eligible
+from .runtime import AttentionPlan, DecodePlan, attn_item_rows, decode_eligible
 
 
 @dataclass
@@ -178,7 +178,8 @@ def _prepare_attention(spec: AttentionSpec, module: ir.Module, inputs: dict, out
         # short query block over a long KV range: K2 split-KV decode
         plan = DecodePlan(q, k, v, o, spec.scale)
     else:
-        plan = AttentionPlan(q, k, v, o, spec.scale, kind, mask_t, kv_stages=spec.stages)
+        plan = AttentionPlan(q, k, v, o, spec.scale, kind, mask_t, kv_stages=spec.stages,
+                             item_rows=attn_item_rows(spec.block_m))
     return plan, o, outer
 
 
@@ -266,7 +267,7 @@ def _attention_streamed(spec: AttentionSpec, inputs: dict, outer, mask_kind, out
                 plan = DecodePlan(qv, kv, vv, ov, spec.scale, err_flag=err)
             else:
                 plan = AttentionPlan(qv, kv, vv, ov, spec.scale, kind, err_flag=err, kv_stages=spec.stages,
-                                     work_counter=work)
+                                     work_counter=work, item_rows=attn_item_rows(spec.block_m))
             plan.launch(comp)
             plans.append(plan)  # keep argument structs / workspaces alive until the sync
             flops += plan.flops()
@@ -326,7 +327,8 @@ def _causal_rows_streamed(spec, q_h, k_h, v_h, o_h, q_d, k_d, v_d, o_d, out, com
         kv_done = r1
         comp.wait_stream(s_in)
         plan = AttentionPlan(q_d[:, :, r0:r1], k_d[:, :, :r1], v_d[:, :, :r1], o_d[:, :, r0:r1], spec.scale,
-                             "causal", causal_offset=r0, err_flag=err, kv_stages=spec.stages)
+                             "causal", causal_offset=r0, err_flag=err, kv_stages=spec.stages,
+                             item_rows=attn_item_rows(spec.block_m))
         plan.launch(comp)
         plans.append(plan)
         flops += plan.flops()
@@ -488,8 +490,9 @@ def execute_ma(module, inputs: dict, device=None, precision=None, *, outer=None,
                                            "splits": plan.splits, "ma_tile": (spec.block_m, spec.block_n)})
             else:
                 report.realisation.append({"kernel": "attn_fwd", "mask": plan.mask_kind,
-                                           "grid_ctas": -(-spec.n // 256) * o.shape[0] * o.shape[1],
-                                           "gpu_tile": (256, 128), "ma_tile": (spec.block_m, spec.block_n)})
+                                           "items": -(-spec.n // plan.item_rows) * o.shape[0] * o.shape[1],
+                                           "ctas_per_sm": plan.ctas_per_sm, "kv_slots": plan.kv_slots,
+                                           "gpu_tile": (plan.item_rows, 128), "ma_tile": (spec.block_m, spec.block_n)})
             cur = torch.cuda.current_stream(dev)
             st = _launch_stream(stream, cur)
             ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

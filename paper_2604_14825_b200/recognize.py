@@ -196,9 +196,13 @@ class AttentionSpec:
     backend: str
     kind: str = "attention"
 
-    # GPU realisation: 256-row CTA (two 128-row tiles) x 128-row KV tiles
-    GPU_BM = 256
+    # GPU realisation: 256-row work items (two 128-row tiles) -- or 128-row items
+    # for small MA query tiles (attn_item_rows) -- x 128-row KV tiles
     GPU_BN = 128
+
+    @property
+    def gpu_bm(self) -> int:
+        return attn_item_rows(self.block_m)
 
     def flops(self, causal: bool = False) -> float:
         """Megatron/FA convention: the two GEMMs only."""
@@ -213,17 +217,27 @@ class AttentionSpec:
         check that the union of the MA slices equals each GPU tile and that
         iteration order is ascending as in the MA's sequential loop.
         """
-        q_per = self.GPU_BM // self.block_m if self.block_m <= self.GPU_BM else None
-        n_cta = math.ceil(self.n / self.GPU_BM)
+        bm = self.gpu_bm
+        n_cta = math.ceil(self.n / bm)
         n_kv = math.ceil(self.m / self.GPU_BN)
         for c in range(n_cta):
-            rows = (c * self.GPU_BM, min(self.n, (c + 1) * self.GPU_BM))
+            rows = (c * bm, min(self.n, (c + 1) * bm))
             blocks = [i for i in range(self.n_blocks)
                       if rows[0] <= i * self.block_m < rows[1]]
             for j in range(n_kv):
                 cols = (j * self.GPU_BN, min(self.m, (j + 1) * self.GPU_BN))
                 iters = [t for t in range(self.n_iters) if cols[0] <= t * self.block_n < cols[1]]
                 yield c, blocks, j, iters
+
+
+def attn_item_rows(ma_block_rows: int) -> int:
+    """GPU query rows per K1 work item for the MA's query tile t0_i (the scheduler's
+    `t0_i` tunable, tilecc/autosched/scheduler.py:116-124): small MA tiles (t0_i <= 32)
+    -> 128-row items (one query tile per CTA, two CTAs per SM); otherwise 256-row
+    items (two query tiles sharing each K/V tile, one CTA per SM).  Both realise the
+    same MA blocks exactly (unions of consecutive MA row tiles)."""
+    return 128 if 0 < ma_block_rows <= 32 else 256
+
 
 
 @dataclass(frozen=True)

@@ -14,6 +14,7 @@ import torch
 
 from . import _lib
 from .errors import DivisionByZero, InvalidArguments
+from .recognize import attn_item_rows  # noqa: F401  (the MA t0_i -> K1 item-rows rule)
 
 
 def _stream_handle(stream) -> int:
@@ -95,7 +96,9 @@ class AttentionPlan:
         a.item_rows = int(item_rows)  # 0 = library choice, 128 or 256 query rows per work item
         # split-KV workspace (non-zero only for few, long work items)
         ws = int(_lib.lib().nt_attn_workspace_bytes(C.byref(a)))
-        self.ws = torch.empty(ws, dtype=torch.uint8, device=q.device) if ws else None
+        # zeroed once per plan: every byte the merge reads is written by K1's TMA stores,
+        # which compute-sanitizer's initcheck does not track
+        self.ws = torch.zeros(ws, dtype=torch.uint8, device=q.device) if ws else None
         a.workspace = self.ws.data_ptr() if ws else None
         a.workspace_bytes = ws
         self.item_rows = int(item_rows) if item_rows else 256

@@ -51,12 +51,14 @@ def _lower(base, schedule, assignment, device):
 
 
 def realisation_key(spec, outer, mask_kind) -> tuple:
-    """Fields that determine the sm_100a launch (MA tile sizes do not: the GPU tile is fixed)."""
+    """Fields that determine the sm_100a launch: for attention the MA query tile t0_i
+    picks the K1 work-item rows (128 / 256, runtime.attn_item_rows) and `stages` the
+    K/V ring depth; the KV tile t0_j does not change the GPU tile (128 keys)."""
     if isinstance(spec, AttentionSpec):
-        from .runtime import attn_kv_slots
-        # the MA tile sizes do not change the GPU tiles; `stages` picks the K/V ring depth
+        from .runtime import attn_item_rows, attn_kv_slots
+        rows = attn_item_rows(spec.block_m)
         return ("attn", spec.n, spec.m, spec.d, spec.scale, spec.mask is not None, mask_kind, outer,
-                attn_kv_slots(spec.d, spec.stages))
+                rows, attn_kv_slots(spec.d, spec.stages, rows // 128))
     if isinstance(spec, GemmChainSpec):
         return ("chain", spec.n, spec.k, spec.f, spec.e)
     return (type(spec).__name__,)

@@ -430,9 +430,9 @@ def test_e4m3_rejects_unsupported_shapes():
     dev = torch.device("cuda")
     q = torch.zeros((1, 1, 128, 64), device=dev).to(torch.float8_e4m3fn)
     o = torch.empty((1, 1, 128, 64), device=dev)
-    plan = AttentionPlan(q, q, q, o, 0.125, "none")
+    # rejected when the plan is prepared (nt_attn_prepare validates like nt_attn_fwd)
     with pytest.raises(Exception, match="e4m3"):
-        plan.launch()
+        AttentionPlan(q, q, q, o, 0.125, "none")
 
 
 # ------------------------------------------------------------ split-KV work units

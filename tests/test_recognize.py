@@ -95,8 +95,8 @@ def test_attention_index_math_matches_gpu_tiling(fname):
     seen_q, seen_k = set(), set()
     for cta, blocks, kv, iters in spec.gpu_tiles():
         rows = sorted(q_rows[b] for b in blocks)
-        lo = cta * 256
-        hi = min(spec.n, lo + 256)
+        lo = cta * spec.gpu_bm
+        hi = min(spec.n, lo + spec.gpu_bm)
         covered = sorted(r for o, l in rows for r in range(o, o + l))
         assert covered == list(range(lo, hi))
         assert iters == sorted(iters)
@@ -168,3 +168,20 @@ def test_b200_profile_schedules_config2_e4096_without_overrides():
     spec = recognize(_load("b200_gemm4k_e4096.seed0.ma.json"))[0]
     assert isinstance(spec, GemmChainSpec) and spec.e == 4096
     assert _load("b200_gemm4k_e4096.seed0.ma.json").kernels[0].backend == "sm100a"
+
+
+def test_tile_tunables_select_distinct_realisations():
+    """The MA's t0_i picks K1's work-item rows and `stages` its K/V ring: the device
+    tuner sees distinct kernels for distinct tile choices (tuner.realisation_key)."""
+    from dataclasses import replace as dc_replace
+
+    from paper_2604_14825_b200.tuner import realisation_key
+
+    spec = recognize(_load("attn256.seed0.ma.json"))[0]
+    keys = set()
+    for bm in (16, 32, 64, 128):
+        for st in (1, 2, 3):
+            keys.add(realisation_key(dc_replace(spec, block_m=bm, stages=st), None, "none"))
+    assert len(keys) == 4  # {128, 256} rows x {shallow, deep} ring at D=64
+    assert recognize(_load("attn256_t32x64.seed0.ma.json"))[0].gpu_bm == 128
+    assert recognize(_load("attn256_t128x128.seed0.ma.json"))[0].gpu_bm == 256

@@ -88,8 +88,33 @@ def test_device_tuner_search_runs_on_gpu():
 
     seeds, base, probe, dev = _setup(n=2048, d=64)
     scorer = tuner.DeviceScorer(outer=(1, 8, 8), reps=3)
-    res = tuner.search(seeds, base, probe, dev, ref.TunerConfig(budget=12, population=6, seed=0), scorer=scorer)
-    assert res.measurements == 12
+    res = tuner.search(seeds, base, probe, dev, ref.TunerConfig(budget=24, population=8, seed=0), scorer=scorer)
+    assert res.measurements == 24
     best = res.best()
     assert 0 < best.cost < 1e5  # microseconds
-    assert scorer.timed >= 1
+    # tile tunables reach distinct kernels: t0_i -> item rows, stages -> K/V ring
+    assert scorer.timed >= 2
+    rows = {k[0][8] for k in scorer.cache if k[0][0] == "attn"}
+    assert rows <= {128, 256}
+
+
+@pytest.mark.gpu
+def test_pool_scorer_on_device():
+    """PoolScorer(kind="device") scores a generation in worker processes (one per GPU;
+    one here) and returns candidate-ordered device timings."""
+    _tilecc()
+    from tilecc.tuner import tuner as ref
+
+    from paper_2604_14825_b200 import tuner
+
+    seeds, base, probe, dev = _setup(n=1024, d=64)
+    pool = tuner.PoolScorer(1, kind="device", scorer_kwargs=dict(outer=(4, 8, 8), reps=3))
+    try:
+        res = tuner.search(seeds, base, probe, dev, ref.TunerConfig(budget=8, population=4, seed=1),
+                           batch_scorer=pool)
+    finally:
+        pool.close()
+    assert res.measurements == 8
+    costs = [c.cost for c in res.candidates]
+    assert all(0 < c < 1e5 for c in costs if c != float("inf"))
+    assert any(c != float("inf") for c in costs)

@@ -10,7 +10,7 @@ ap.add_argument("--d", type=int, default=128); ap.add_argument("--b", type=int, 
 ap.add_argument("--hq", type=int, default=32); ap.add_argument("--hkv", type=int, default=8)
 a = ap.parse_args()
 L = _lib.lib(); L.nt_debug_set_cta_times.argtypes = [ctypes.c_void_p]
-buf = torch.zeros(148 * 3, dtype=torch.int64, device="cuda")
+buf = torch.zeros(2 * 148 * 3, dtype=torch.int64, device="cuda")
 q = torch.randn(a.b, a.hq, a.n, a.d, device="cuda").bfloat16(); k = torch.randn(a.b, a.hkv, a.n, a.d, device="cuda").bfloat16()
 v = torch.randn(a.b, a.hkv, a.n, a.d, device="cuda").bfloat16(); o = torch.empty(a.b, a.hq, a.n, a.d, device="cuda").bfloat16()
 plan = AttentionPlan(q, k, v, o, a.d ** -0.5, "causal" if a.causal else "none")
@@ -20,7 +20,7 @@ L.nt_debug_set_cta_times(buf.data_ptr())
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record(); plan.launch(); e1.record(); e1.synchronize()
 L.nt_debug_set_cta_times(None)
-t = buf.view(148, 3).cpu().numpy()
+t = buf.view(2 * 148, 3).cpu().numpy()
 t = t[t[:, 0] > 0]
 t0 = t[:, 0].min()
 start = (t[:, 0] - t0) / 1e3; end = (t[:, 1] - t0) / 1e3
