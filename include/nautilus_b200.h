@@ -104,6 +104,15 @@ int nt_attn_prepare(const nt_attn_args* args);
 /* CTAs of the kernel `args` selects that are resident per SM (the persistent
  * grid is this x #SMs); a negative NT_ERR_* on invalid arguments. */
 int nt_attn_resident_ctas(const nt_attn_args* args);
+/* Attention plans: everything of nt_attn_fwd that depends only on the arguments
+ * (validation, the five tensor maps, split plan, instantiation choice, kernel
+ * load) done once; nt_attn_plan_launch is then one kernel launch (plus the
+ * split-KV merge).  The plan keeps the pointers of `args`; the caller keeps the
+ * buffers alive.  Not tied to a stream; launches on one stream are ordered. */
+typedef struct nt_attn_plan nt_attn_plan;
+int nt_attn_plan_create(const nt_attn_args* args, nt_attn_plan** plan);
+int nt_attn_plan_launch(const nt_attn_plan* plan, void* stream);
+void nt_attn_plan_destroy(nt_attn_plan* plan);
 
 /*
  * K2 split-KV decode attention + combine (flash-decoding) for short query

@@ -20,7 +20,8 @@ NT_DTYPE_BF16, NT_DTYPE_F32, NT_DTYPE_E4M3 = 0, 1, 2
 
 # Every symbol include/nautilus_b200.h declares (checked by tests/test_capi.py).
 EXPORTED = (
-    "nt_attn_fwd", "nt_attn_workspace_bytes", "nt_attn_prepare", "nt_attn_resident_ctas", "nt_attn_decode", "nt_decode_workspace_bytes", "nt_decode_num_splits", "nt_gemm",
+    "nt_attn_fwd", "nt_attn_workspace_bytes", "nt_attn_prepare", "nt_attn_resident_ctas",
+    "nt_attn_plan_create", "nt_attn_plan_launch", "nt_attn_plan_destroy", "nt_attn_decode", "nt_decode_workspace_bytes", "nt_decode_num_splits", "nt_gemm",
     "nt_gemm_chain", "nt_gemm_chain_workspace_bytes", "nt_gemm_k_splits", "nt_gemm_workspace_bytes",
     "nt_cast_f32_to_bf16", "nt_cast_bf16_to_f32", "nt_abi_version", "nt_last_error", "nt_launch_count",
     "nt_module_load", "nt_module_function", "nt_launch", "nt_module_unload", "nt_attn_decode_paged",
@@ -97,6 +98,10 @@ def lib():
             L.nt_attn_fwd.argtypes = [C.POINTER(AttnArgs), C.c_void_p]
             L.nt_attn_prepare.argtypes = [C.POINTER(AttnArgs)]
             L.nt_attn_resident_ctas.argtypes = [C.POINTER(AttnArgs)]
+            L.nt_attn_plan_create.argtypes = [C.POINTER(AttnArgs), C.POINTER(C.c_void_p)]
+            L.nt_attn_plan_launch.argtypes = [C.c_void_p, C.c_void_p]
+            L.nt_attn_plan_destroy.argtypes = [C.c_void_p]
+            L.nt_attn_plan_destroy.restype = None
             L.nt_attn_decode.argtypes = [C.POINTER(DecodeArgs), C.c_void_p]
             L.nt_attn_decode_paged.argtypes = [C.POINTER(DecodePagedArgs), C.c_void_p]
             L.nt_decode_workspace_bytes.argtypes = [C.c_int32] * 5
@@ -125,7 +130,8 @@ def lib():
             L.nt_memcpy2d_async.restype = C.c_int
             L.nt_last_error.restype = C.c_char_p
             L.nt_launch_count.restype = C.c_int64
-            for name in ("nt_attn_fwd", "nt_attn_prepare", "nt_attn_resident_ctas", "nt_attn_decode", "nt_attn_decode_paged", "nt_gemm", "nt_gemm_chain",
+            for name in ("nt_attn_fwd", "nt_attn_prepare", "nt_attn_resident_ctas", "nt_attn_plan_create",
+                         "nt_attn_plan_launch", "nt_attn_decode", "nt_attn_decode_paged", "nt_gemm", "nt_gemm_chain",
                          "nt_cast_f32_to_bf16", "nt_cast_bf16_to_f32", "nt_abi_version",
                          "nt_module_load", "nt_module_function", "nt_launch", "nt_module_unload"):
                 getattr(L, name).restype = C.c_int
@@ -141,3 +147,16 @@ def check(status: int, what: str) -> None:
 
 def launch_count() -> int:
     return int(lib().nt_launch_count())
+
+
+_SMS: dict = {}
+
+
+def num_sms(device) -> int:
+    """SM count of a CUDA device (cached); the C side uses the same attribute."""
+    import torch
+
+    idx = torch.device(device).index if torch.device(device).index is not None else torch.cuda.current_device()
+    if idx not in _SMS:
+        _SMS[idx] = torch.cuda.get_device_properties(idx).multi_processor_count
+    return _SMS[idx]

@@ -109,6 +109,10 @@ constexpr float kRescaleLog2 = 8.0f;
 #define NT_PACK_D128 0
 #endif
 // D=64 (SEP_P): wait for PV_t(j-1) after the exp pass instead of before it
+// D=128: store P to TMEM after the whole exp pass instead of chunk by chunk
+#ifndef NT_P_STORE_LATE
+#define NT_P_STORE_LATE 0
+#endif
 #ifndef NT_SEP_P_LATE
 #define NT_SEP_P_LATE 1
 #endif
@@ -859,6 +863,11 @@ __global__ void __launch_bounds__(attn_threads<NQ>(), NQ == 2 ? 1 : 2)
             tmem_st16(tP, pk);
             tmem_st16(tP + 16, pk + 16);
           }
+        } else if (!FP8 && NT_P_STORE_LATE) {
+          // all exps into registers, then the four P stores back to back
+          sum = attn_exp_pass<FP8, false, kPoly, kPack, MASK != MASK_NONE>(s, sc, m_use, tP, pk);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) tmem_st16(tP + c * 16, pk + c * 16);
         } else {
           sum = attn_exp_pass<FP8, true, kPoly, kPack, MASK != MASK_NONE>(s, sc, m_use, tP, pk);
         }

@@ -20,6 +20,10 @@ struct AttnMaps {
 // prepared kernel's resident CTAs per SM are left in g_prepared_ctas_per_sm
 extern thread_local bool g_prepare_only;
 extern thread_local int g_prepared_ctas_per_sm;
+// ... and the fully resolved launcher (instantiation + split/merge), so a plan
+// (nt_attn_plan_create) launches with one indirect call and no re-encoding
+using AttnLaunchFn = int (*)(const AttnMaps&, const AttnFwdParams&, cudaStream_t);
+extern thread_local AttnLaunchFn g_prepared_fn;
 
 // Resident CTAs per SM of a kernel at `threads` / `smem`, once per instantiation.
 // Computed from the register, shared-memory and TMEM budgets: the occupancy API
@@ -85,6 +89,7 @@ int launch_attn_kernel(const AttnMaps& m, const AttnFwdParams& p, cudaStream_t s
 
 template <int D, int MASK, bool F32, int KVS, bool FP8, int NQ>
 int launch_attn(const AttnMaps& m, const AttnFwdParams& p, cudaStream_t st) {
+  if (g_prepare_only) g_prepared_fn = &launch_attn<D, MASK, F32, KVS, FP8, NQ>;
   // the split-KV path is its own instantiation: its extra state costs the
   // unsplit kernel registers (BERT 58 -> 63 us when shared)
   if constexpr (MASK != MASK_TENSOR) {

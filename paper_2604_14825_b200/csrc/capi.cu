@@ -22,6 +22,7 @@ std::atomic<int64_t> g_launches{0};
 // loaded kernel image) but stop before the launch
 thread_local bool g_prepare_only = false;
 thread_local int g_prepared_ctas_per_sm = 0;
+thread_local AttnLaunchFn g_prepared_fn = nullptr;
 
 int set_error(int code, const std::string& msg) {
   g_last_error = msg;
@@ -135,10 +136,14 @@ struct AttnSplit {
 // Query rows per work item: 256 (two 128-row tiles, one CTA per SM) or 128 (one
 // tile, two CTAs per SM -- the NQ = 1 instantiations; bf16 Q/K/V only).
 // args->item_rows 0 = library choice.
+// Library choice: 128-row items when 256-row items would leave more than half
+// of the SMs idle (e.g. config 1, one 256-row item: 2 CTAs instead of 1,
+// 15.9 -> 13.9 us); otherwise 256 (two tiles share each K/V tile).
 static int attn_item_rows(const nt_attn_args* a) {
   if (a->in_dtype == NT_DTYPE_E4M3) return 256;
   if (a->item_rows == 128 || a->item_rows == 256) return a->item_rows;
-  return 256;
+  const long long items256 = (long long)((a->seq_q + 255) / 256) * a->batch * a->heads_q;
+  return items256 * 2 < num_sms() ? 128 : 256;
 }
 
 static AttnSplit attn_split_plan(const nt_attn_args* a) {
@@ -203,7 +208,8 @@ extern "C" int nt_attn_resident_ctas(const nt_attn_args* a) {
   return rc ? -rc : g_prepared_ctas_per_sm;
 }
 
-extern "C" int nt_attn_fwd(const nt_attn_args* a, void* stream) {
+// Validation, tensor maps, split plan and kernel parameters of one launch.
+static int attn_build(const nt_attn_args* a, AttnMaps& m, AttnFwdParams& p, int& nq_out) {
   if (!a) return set_error(NT_ERR_INVALID, "null args");
   if (a->head_dim != 64 && a->head_dim != 128)
     return set_error(NT_ERR_UNSUPPORTED, "head_dim must be 64 or 128");
@@ -223,7 +229,7 @@ extern "C" int nt_attn_fwd(const nt_attn_args* a, void* stream) {
     return set_error(NT_ERR_UNSUPPORTED, "e4m3 attention: head_dim 128, no or causal mask");
   const int D = a->head_dim;
   const size_t in_elem = e4m3 ? 1 : 2;
-  AttnMaps m{};
+  m = AttnMaps{};
   CUtensorMap &mq = m.q, &mk = m.k, &mv = m.v, &mo = m.o;
   int rc;
   if ((rc = make_map_4d(&mq, a->q.ptr, D, a->seq_q, a->heads_q, a->batch, a->q.stride_s, a->q.stride_h,
@@ -247,7 +253,7 @@ extern "C" int nt_attn_fwd(const nt_attn_args* a, void* stream) {
                         a->o.stride_b, 32, f32 ? 4 : 2, f32 ? f32_cols : 32,
                         (f32 && f32_cols == 32) ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B)))
     return rc;
-  AttnFwdParams p{};
+  p = AttnFwdParams{};
   p.B = a->batch;
   p.Hq = a->heads_q;
   p.Hkv = a->heads_kv;
@@ -286,10 +292,60 @@ extern "C" int nt_attn_fwd(const nt_attn_args* a, void* stream) {
   } else {
     m.p = m.o;  // unused (no split)
   }
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (e4m3) return dispatch_attn_e4m3(a, m, p, st);
-  return D == 64 ? dispatch_attn_d64(a, m, p, nq, st) : dispatch_attn_d128(a, m, p, nq, st);
+  nq_out = nq;
+  return NT_OK;
 }
+
+static int attn_dispatch(const nt_attn_args* a, const AttnMaps& m, const AttnFwdParams& p, int nq, cudaStream_t st) {
+  if (a->in_dtype == NT_DTYPE_E4M3) return dispatch_attn_e4m3(a, m, p, st);
+  return a->head_dim == 64 ? dispatch_attn_d64(a, m, p, nq, st) : dispatch_attn_d128(a, m, p, nq, st);
+}
+
+extern "C" int nt_attn_fwd(const nt_attn_args* a, void* stream) {
+  AttnMaps m;
+  AttnFwdParams p;
+  int nq = 2;
+  if (const int rc = attn_build(a, m, p, nq)) return rc;
+  return attn_dispatch(a, m, p, nq, static_cast<cudaStream_t>(stream));
+}
+
+// ----------------------------------------------------------------- attention plans
+struct nt_attn_plan {
+  AttnMaps maps;
+  AttnFwdParams params;
+  AttnLaunchFn fn;
+  int device;
+};
+
+extern "C" int nt_attn_plan_create(const nt_attn_args* a, nt_attn_plan** out) {
+  if (!out) return set_error(NT_ERR_INVALID, "null plan pointer");
+  *out = nullptr;
+  auto* pl = new nt_attn_plan{};
+  int nq = 2;
+  int rc = attn_build(a, pl->maps, pl->params, nq);
+  if (!rc) {
+    g_prepare_only = true;
+    g_prepared_fn = nullptr;
+    rc = attn_dispatch(a, pl->maps, pl->params, nq, nullptr);
+    g_prepare_only = false;
+    pl->fn = g_prepared_fn;
+    if (!rc && !pl->fn) rc = set_error(NT_ERR_UNSUPPORTED, "no launcher selected");
+  }
+  if (rc) {
+    delete pl;
+    return rc;
+  }
+  cudaGetDevice(&pl->device);
+  *out = pl;
+  return NT_OK;
+}
+
+extern "C" int nt_attn_plan_launch(const nt_attn_plan* pl, void* stream) {
+  if (!pl) return set_error(NT_ERR_INVALID, "null plan");
+  return pl->fn(pl->maps, pl->params, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" void nt_attn_plan_destroy(nt_attn_plan* pl) { delete pl; }
 
 // ----------------------------------------------------------------- casts
 __global__ void cast_f32_bf16_kernel(const float4* __restrict__ src, uint2* __restrict__ dst, int64_t n4) {

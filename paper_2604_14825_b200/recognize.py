@@ -202,7 +202,8 @@ class AttentionSpec:
 
     @property
     def gpu_bm(self) -> int:
-        return attn_item_rows(self.block_m)
+        """Rows per GPU work item for the single-head MA program (outer grid 1)."""
+        return attn_effective_rows(attn_item_rows(self.block_m), self.n, 1)
 
     def flops(self, causal: bool = False) -> float:
         """Megatron/FA convention: the two GEMMs only."""
@@ -231,13 +232,20 @@ class AttentionSpec:
 
 
 def attn_item_rows(ma_block_rows: int) -> int:
-    """GPU query rows per K1 work item for the MA's query tile t0_i (the scheduler's
-    `t0_i` tunable, tilecc/autosched/scheduler.py:116-124): small MA tiles (t0_i <= 32)
-    -> 128-row items (one query tile per CTA, two CTAs per SM); otherwise 256-row
-    items (two query tiles sharing each K/V tile, one CTA per SM).  Both realise the
-    same MA blocks exactly (unions of consecutive MA row tiles)."""
-    return 128 if 0 < ma_block_rows <= 32 else 256
+    """K1 query rows per work item requested for the MA's query tile t0_i (the
+    scheduler's `t0_i` tunable, tilecc/autosched/scheduler.py:116-124): small MA tiles
+    (t0_i <= 32) -> 128-row items (one query tile per CTA, two CTAs per SM);
+    otherwise 0 = the library's choice (attn_effective_rows).  Both realise the same
+    MA blocks exactly (unions of consecutive MA row tiles)."""
+    return 128 if 0 < ma_block_rows <= 32 else 0
 
+
+def attn_effective_rows(requested: int, n: int, batch_heads: int, sms: int = 148) -> int:
+    """The rows nt_attn_fwd uses (csrc/capi.cu attn_item_rows): an explicit 128/256,
+    else 128 when 256-row items would leave more than half of the SMs idle."""
+    if requested in (128, 256):
+        return requested
+    return 128 if -(-n // 256) * batch_heads * 2 < sms else 256
 
 
 @dataclass(frozen=True)

@@ -101,20 +101,32 @@ class AttentionPlan:
         self.ws = torch.zeros(ws, dtype=torch.uint8, device=q.device) if ws else None
         a.workspace = self.ws.data_ptr() if ws else None
         a.workspace_bytes = ws
-        self.item_rows = int(item_rows) if item_rows else 256
+        from .recognize import attn_effective_rows
+        self.item_rows = 256 if e4m3 else attn_effective_rows(int(item_rows), N, B * Hq, _lib.num_sms(q.device))
         self.kv_slots = attn_kv_slots(64 if e4m3 else D, kv_stages, self.item_rows // 128)  # e4m3: D=64-sized tiles
         self.args = a
         self.shape = (B, Hq, Hkv, N, M, D)
-        self._fn = _lib.lib().nt_attn_fwd
+        L = _lib.lib()
         self._ref = C.byref(a)
-        # validate + load the kernel now, so the first launch is a plain launch
-        _lib.check(_lib.lib().nt_attn_prepare(self._ref), "nt_attn_prepare")
-        self.ctas_per_sm = int(_lib.lib().nt_attn_resident_ctas(self._ref))
+        # a C-side plan: tensor maps encoded and the kernel loaded once; a launch is
+        # one indirect call (nt_attn_plan_launch)
+        handle = C.c_void_p()
+        _lib.check(L.nt_attn_plan_create(self._ref, C.byref(handle)), "nt_attn_plan_create")
+        self._plan = handle
+        self._destroy = L.nt_attn_plan_destroy
+        self._fn = L.nt_attn_plan_launch
+        self.ctas_per_sm = int(L.nt_attn_resident_ctas(self._ref))
 
     def launch(self, stream=None) -> None:
-        st = self._fn(self._ref, _stream_handle(stream))
+        st = self._fn(self._plan, _stream_handle(stream))
         if st:
-            _lib.check(st, "nt_attn_fwd")
+            _lib.check(st, "nt_attn_plan_launch")
+
+    def __del__(self):
+        plan = getattr(self, "_plan", None)
+        if plan is not None and plan.value:
+            self._destroy(plan)
+            self._plan = None
 
     def flops(self) -> float:
         B, Hq, _, N, M, D = self.shape

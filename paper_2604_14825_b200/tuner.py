@@ -55,8 +55,10 @@ def realisation_key(spec, outer, mask_kind) -> tuple:
     picks the K1 work-item rows (128 / 256, runtime.attn_item_rows) and `stages` the
     K/V ring depth; the KV tile t0_j does not change the GPU tile (128 keys)."""
     if isinstance(spec, AttentionSpec):
+        from .recognize import attn_effective_rows
         from .runtime import attn_item_rows, attn_kv_slots
-        rows = attn_item_rows(spec.block_m)
+        bh = outer[0] * outer[1] if outer else 1
+        rows = attn_effective_rows(attn_item_rows(spec.block_m), spec.n, bh)
         return ("attn", spec.n, spec.m, spec.d, spec.scale, spec.mask is not None, mask_kind, outer,
                 rows, attn_kv_slots(spec.d, spec.stages, rows // 128))
     if isinstance(spec, GemmChainSpec):

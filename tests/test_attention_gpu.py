@@ -583,3 +583,28 @@ def test_item_rows_rejects_bad_values():
     q8 = q.to(torch.float8_e4m3fn)
     with pytest.raises(UnsupportedMA):
         AttentionPlan(q8, q8, q8, o, 0.1, "none", item_rows=128)
+
+
+def test_one_shot_abi_entry_equals_the_plan_launch():
+    """nt_attn_fwd (the one-shot C entry the reference-side FFI binds) and
+    nt_attn_plan_launch (maps encoded once) run the same kernel: same bits."""
+    import ctypes
+
+    from paper_2604_14825_b200 import _lib
+    from paper_2604_14825_b200.runtime import AttentionPlan
+
+    dev = torch.device("cuda")
+    q = torch.from_numpy(_rand((2, 8, 700, 128), 91)).to(dev).bfloat16()
+    k = torch.from_numpy(_rand((2, 2, 700, 128), 92)).to(dev).bfloat16()
+    v = torch.from_numpy(_rand((2, 2, 700, 128), 93)).to(dev).bfloat16()
+    o1 = torch.full((2, 8, 700, 128), float("nan"), device=dev)
+    o2 = torch.full((2, 8, 700, 128), float("nan"), device=dev)
+    plan = AttentionPlan(q, k, v, o1, 128 ** -0.5, "causal")
+    plan.launch()
+    args = _lib.AttnArgs.from_buffer_copy(plan.args)
+    args.o = _lib.Tensor4(o2.data_ptr(), o2.stride(0), o2.stride(1), o2.stride(2))
+    st = torch.cuda.current_stream().cuda_stream
+    _lib.check(_lib.lib().nt_attn_fwd(ctypes.byref(args), st), "nt_attn_fwd")
+    torch.cuda.synchronize()
+    plan.check_errors()
+    assert torch.equal(o1, o2)

@@ -182,6 +182,9 @@ def test_tile_tunables_select_distinct_realisations():
     for bm in (16, 32, 64, 128):
         for st in (1, 2, 3):
             keys.add(realisation_key(dc_replace(spec, block_m=bm, stages=st), None, "none"))
-    assert len(keys) == 4  # {128, 256} rows x {shallow, deep} ring at D=64
+    assert len(keys) == 2  # one 256-row item -> always 128 rows here; {shallow, deep} ring at D=64
+    keys = {realisation_key(dc_replace(spec, block_m=bm, stages=st), (4, 32, 8), "none")
+            for bm in (16, 32, 64, 128) for st in (1, 2, 3)}
+    assert len(keys) == 4  # (4 x 32) items: {128, 256} rows x {shallow, deep} ring
     assert recognize(_load("attn256_t32x64.seed0.ma.json"))[0].gpu_bm == 128
-    assert recognize(_load("attn256_t128x128.seed0.ma.json"))[0].gpu_bm == 256
+    assert recognize(_load("bert512.seed0.ma.json"))[0].gpu_bm == 128  # 2 items of 256 < 148 / 2

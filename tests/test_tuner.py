@@ -87,7 +87,7 @@ def test_device_tuner_search_runs_on_gpu():
     from paper_2604_14825_b200 import tuner
 
     seeds, base, probe, dev = _setup(n=2048, d=64)
-    scorer = tuner.DeviceScorer(outer=(1, 8, 8), reps=3)
+    scorer = tuner.DeviceScorer(outer=(4, 8, 8), reps=3)
     res = tuner.search(seeds, base, probe, dev, ref.TunerConfig(budget=24, population=8, seed=0), scorer=scorer)
     assert res.measurements == 24
     best = res.best()
