@@ -53,6 +53,13 @@ CONFIGS = {
     # the paper's FP8 regime: e4m3 Q/K/V with per-tensor descales, kind::f8f6f4
     "llama8k_causal_e4m3": dict(prog="llama_causal", B=1, Hq=32, Hkv=8, N=8192, D=128, causal=True,
                                 golden="causal8k", scale=LLAMA_SCALE, in_dtype="e4m3"),
+    # a general (non-causal) 0 / -inf Mask input to the masked MA program: random 50 %
+    # key visibility per row, realised as visibility bits (NT_MASK_BITS) or, for
+    # comparison, as the fp32 tensor the MA reads (NT_MASK_TENSOR)
+    "llama4k_mask_bits": dict(prog="llama_causal", B=1, Hq=32, Hkv=8, N=4096, D=128, causal=False,
+                              golden="causal4k", scale=LLAMA_SCALE, mask="bits"),
+    "llama4k_mask_f32": dict(prog="llama_causal", B=1, Hq=32, Hkv=8, N=4096, D=128, causal=False,
+                             golden="causal4k", scale=LLAMA_SCALE, mask="tensor"),
     "bert512": dict(prog="scaled_0p125", B=32, Hq=12, Hkv=12, N=512, D=64, causal=False,
                     golden="bert512", scale=0.125),
     "attn256": dict(prog="attention", B=1, Hq=1, Hkv=1, N=256, D=64, causal=False,
@@ -310,7 +317,7 @@ def attention_flops(cfg):
         return 2.0 * cfg["N"] * cfg["F"] * (cfg["K"] + cfg["E"])
     if cfg["causal"]:
         return 2.0 * B * Hq * D * N * (N + 1)
-    return 4.0 * B * Hq * N * M * D
+    return 4.0 * B * Hq * N * M * D  # (masked configs: dense-equivalent, every pair is computed)
 
 
 def config_block(cfg, args, world):
@@ -430,10 +437,25 @@ def build_workload(cfg, spec, rank, world, dev):
                  host_inputs={"q": q, "k": k, "v": v}, outer=None, mask_kind=mask_kind, e4m3=True,
                  in_bytes=q.numel() + k.numel() + v.numel())
         return w
-    plan = AttentionPlan(q, k, v, o, spec.scale, mask_kind, item_rows=cfg.get("item_rows", 0))
+    mask_t = None
+    if cfg.get("mask"):
+        # dense-equivalent FLOPs (every (query, key) pair is computed; masked ones exp to 0)
+        from paper_2604_14825_b200.runtime import pack_mask_bits
+        gm = torch.Generator(device=dev)
+        gm.manual_seed(99)
+        mf = torch.where(torch.rand((N, M), generator=gm, device=dev) < 0.5, float("-inf"), 0.0)
+        mf[:, 0] = 0.0
+        mask_kind = cfg["mask"]
+        mask_t = pack_mask_bits(mf)[0] if mask_kind == "bits" else mf
+        w["mask_f32"] = mf
+    plan = AttentionPlan(q, k, v, o, spec.scale, mask_kind, mask_t, item_rows=cfg.get("item_rows", 0))
+    host_inputs = {spec.q: q, spec.k: k, spec.v: v}
+    in_bytes = (q.numel() + k.numel() + v.numel()) * 2
+    if cfg.get("mask"):
+        host_inputs[spec.mask] = w["mask_f32"]  # the MA's fp32 Mask input, packed on the device per call
+        in_bytes += w["mask_f32"].numel() * 4
     w.update(plan=plan, out=o, local_flops=plan.flops(), total_flops=attention_flops(cfg), bound="tensor",
-             host_inputs={spec.q: q, spec.k: k, spec.v: v}, outer=(Bl, Hql, Hkvl), mask_kind=mask_kind,
-             in_bytes=(q.numel() + k.numel() + v.numel()) * 2)
+             host_inputs=host_inputs, outer=(Bl, Hql, Hkvl), mask_kind=mask_kind, in_bytes=in_bytes)
     return w
 
 

@@ -41,6 +41,10 @@ extern "C" {
 #define NT_MASK_NONE 0
 #define NT_MASK_CAUSAL 1 /* Mask[i, j] = 0 if j <= i + causal_offset else -inf */
 #define NT_MASK_TENSOR 2 /* explicit fp32 Mask[seq_q, seq_kv] added to S*c    */
+#define NT_MASK_BITS 3   /* a 0 / -inf Mask as visibility bits (nt_mask_to_bits):
+                          * `mask` = uint32 rows, bit j % 32 of word j / 32 set = key j
+                          * visible; mask_stride_row in words (multiple of 4, >=
+                          * ceil(seq_kv / 128) * 4); rows 16-byte aligned */
 
 #define NT_DTYPE_BF16 0
 #define NT_DTYPE_F32 1
@@ -226,6 +230,12 @@ int nt_launch(void* fn, uint32_t grid_x, uint32_t block_x, uint32_t smem_bytes, 
 int nt_module_unload(nt_module* module);
 
 /* dtype conversion helpers (device buffers) */
+/* Pack a 0 / -inf fp32 Mask[seq_q, seq_kv] (row stride in elements) into
+ * NT_MASK_BITS rows of words_per_row uint32 (>= ceil(seq_kv / 128) * 4; words past
+ * seq_kv are written 0).  Sets *flag bit 0 (device int32, may be NULL) if any value
+ * is neither 0 nor -inf.  Stream-ordered; seq_q <= 65535. */
+int nt_mask_to_bits(const float* mask, int64_t seq_q, int64_t seq_kv, int64_t row_stride, uint32_t* bits,
+                    int64_t words_per_row, int32_t* flag, void* stream);
 int nt_cast_f32_to_bf16(const float* src, void* dst, int64_t n, void* stream);
 int nt_cast_bf16_to_f32(const void* src, float* dst, int64_t n, void* stream);
 

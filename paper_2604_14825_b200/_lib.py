@@ -15,7 +15,7 @@ from .errors import NativeLibraryMissing, raise_for_status
 LIB_PATH = os.environ.get("NT_LIB_PATH") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "_native", "libnautilus_b200.so")
 
-NT_MASK_NONE, NT_MASK_CAUSAL, NT_MASK_TENSOR = 0, 1, 2
+NT_MASK_NONE, NT_MASK_CAUSAL, NT_MASK_TENSOR, NT_MASK_BITS = 0, 1, 2, 3
 NT_DTYPE_BF16, NT_DTYPE_F32, NT_DTYPE_E4M3 = 0, 1, 2
 
 # Every symbol include/nautilus_b200.h declares (checked by tests/test_capi.py).
@@ -25,7 +25,7 @@ EXPORTED = (
     "nt_gemm_chain", "nt_gemm_chain_workspace_bytes", "nt_gemm_k_splits", "nt_gemm_workspace_bytes",
     "nt_cast_f32_to_bf16", "nt_cast_bf16_to_f32", "nt_abi_version", "nt_last_error", "nt_launch_count",
     "nt_module_load", "nt_module_function", "nt_launch", "nt_module_unload", "nt_attn_decode_paged",
-    "nt_memcpy2d_async",
+    "nt_memcpy2d_async", "nt_mask_to_bits",
 )
 
 
@@ -128,6 +128,9 @@ def lib():
             L.nt_memcpy2d_async.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
                                             C.c_void_p]
             L.nt_memcpy2d_async.restype = C.c_int
+            L.nt_mask_to_bits.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_int64,
+                                          C.c_void_p, C.c_void_p]
+            L.nt_mask_to_bits.restype = C.c_int
             L.nt_last_error.restype = C.c_char_p
             L.nt_launch_count.restype = C.c_int64
             for name in ("nt_attn_fwd", "nt_attn_prepare", "nt_attn_resident_ctas", "nt_attn_plan_create",

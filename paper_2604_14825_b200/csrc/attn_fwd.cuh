@@ -52,7 +52,9 @@
 
 namespace nt {
 
-enum { MASK_NONE = 0, MASK_CAUSAL = 1, MASK_TENSOR = 2 };
+// MASK_BITS: a 0 / -inf Mask packed to one bit per key (nt_mask_to_bits): the
+// softmax reads 16 bytes per row per 128-key tile instead of 512 bytes of fp32
+enum { MASK_NONE = 0, MASK_CAUSAL = 1, MASK_TENSOR = 2, MASK_BITS = 3 };
 
 struct AttnFwdParams {
   int B, Hq, Hkv, N, M;
@@ -62,7 +64,7 @@ struct AttnFwdParams {
   int n_items;        // n_mblocks * B * Hq
   int causal_offset;  // key j visible to query i iff j <= i + causal_offset
   float scale_log2;   // c * log2(e)
-  const float* mask;  // MASK_TENSOR: fp32 [N, M]
+  const float* mask;  // MASK_TENSOR: fp32 [N, M]; MASK_BITS: uint32 bit rows (bit j: key j visible)
   long long mask_row_stride;
   void* o;            // output (bf16, or fp32 if OUT_F32), element strides below; D contiguous
   long long o_sb, o_sh, o_sn;
@@ -788,6 +790,17 @@ __global__ void __launch_bounds__(attn_threads<NQ>(), NQ == 2 ? 1 : 2)
             const int kv = kv0 + c;
             const float mk = (kv < p.M) ? __ldg(mrow + kv) : NINF;
             s[c] = __float_as_uint(fmaf(__uint_as_float(s[c]), p.scale_log2, mk * 1.4426950408889634f));
+          }
+        } else if (MASK == MASK_BITS) {
+          // 128 visibility bits of this row's KV tile in one 16-byte load (bits past M are 0)
+          const uint4 w = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint32_t*>(p.mask) +
+                                                             (long long)min(qi, p.N - 1) * p.mask_row_stride +
+                                                             (kv0 >> 5)));
+          if ((w.x & w.y & w.z & w.w) != 0xffffffffu) {
+            const uint32_t wd[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int c = 0; c < 128; ++c)
+              if (!((wd[c >> 5] >> (c & 31)) & 1u)) s[c] = __float_as_uint(NINF);
           }
         } else {
           const int lim = (MASK == MASK_CAUSAL) ? min(qi + p.causal_offset, p.M - 1) : (p.M - 1);

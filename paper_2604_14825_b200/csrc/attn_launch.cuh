@@ -92,7 +92,7 @@ int launch_attn(const AttnMaps& m, const AttnFwdParams& p, cudaStream_t st) {
   if (g_prepare_only) g_prepared_fn = &launch_attn<D, MASK, F32, KVS, FP8, NQ>;
   // the split-KV path is its own instantiation: its extra state costs the
   // unsplit kernel registers (BERT 58 -> 63 us when shared)
-  if constexpr (MASK != MASK_TENSOR) {
+  if constexpr (MASK != MASK_TENSOR && MASK != MASK_BITS) {
     if (p.kv_split > 0) {
       int rc = launch_attn_kernel<D, MASK, F32, KVS, FP8, true, NQ>(m, p, st);
       if (rc || g_prepare_only) return rc;
@@ -132,6 +132,11 @@ int dispatch_attn_nq(const nt_attn_args* a, const AttnMaps& m, const AttnFwdPara
       if constexpr (!FP8)
         return f32 ? launch_attn_stages<D, MASK_TENSOR, true, FP8, NQ>(sg, m, p, st)
                    : launch_attn_stages<D, MASK_TENSOR, false, FP8, NQ>(sg, m, p, st);
+      break;
+    case NT_MASK_BITS:
+      if constexpr (!FP8)
+        return f32 ? launch_attn_stages<D, MASK_BITS, true, FP8, NQ>(sg, m, p, st)
+                   : launch_attn_stages<D, MASK_BITS, false, FP8, NQ>(sg, m, p, st);
       break;
   }
   return set_error(NT_ERR_INVALID, "unknown mask_kind");

@@ -152,7 +152,7 @@ static AttnSplit attn_split_plan(const nt_attn_args* a) {
   const int nmb = (a->seq_q + rows - 1) / rows, nkv_total = (a->seq_kv + 127) / 128;
   const long long BH = (long long)a->batch * a->heads_q;
   sp.n_units = (int)(nmb * BH);
-  if (nmb > kMaxSplitMblocks || a->mask_kind == NT_MASK_TENSOR) return sp;
+  if (nmb > kMaxSplitMblocks || a->mask_kind == NT_MASK_TENSOR || a->mask_kind == NT_MASK_BITS) return sp;
   auto nkv = [&](int mb) {
     if (a->mask_kind != NT_MASK_CAUSAL) return nkv_total;
     const int last_q = std::min(mb * rows + rows - 1, a->seq_q - 1) + a->causal_offset;
@@ -217,7 +217,13 @@ static int attn_build(const nt_attn_args* a, AttnMaps& m, AttnFwdParams& p, int&
     return set_error(NT_ERR_INVALID, "non-positive extent");
   if (a->heads_q % a->heads_kv) return set_error(NT_ERR_INVALID, "heads_q must be a multiple of heads_kv");
   if (!(a->scale > 0.f)) return set_error(NT_ERR_UNSUPPORTED, "scale must be positive");
+  if (a->mask_kind < NT_MASK_NONE || a->mask_kind > NT_MASK_BITS) return set_error(NT_ERR_INVALID, "unknown mask_kind");
   if (a->mask_kind == NT_MASK_TENSOR && !a->mask) return set_error(NT_ERR_INVALID, "tensor mask missing");
+  if (a->mask_kind == NT_MASK_BITS) {
+    if (!a->mask || reinterpret_cast<uintptr_t>(a->mask) % 16 || a->mask_stride_row % 4 ||
+        a->mask_stride_row < (int64_t)((a->seq_kv + 127) / 128) * 4)
+      return set_error(NT_ERR_INVALID, "bit mask: 16-byte aligned rows of >= ceil(seq_kv / 128) * 4 words");
+  }
   const bool e4m3 = a->in_dtype == NT_DTYPE_E4M3;
   if (a->in_dtype != NT_DTYPE_BF16 && !e4m3) return set_error(NT_ERR_UNSUPPORTED, "q/k/v must be bf16 or e4m3");
   if (a->item_rows != 0 && a->item_rows != 128 && a->item_rows != 256)
@@ -225,7 +231,7 @@ static int attn_build(const nt_attn_args* a, AttnMaps& m, AttnFwdParams& p, int&
   if (e4m3 && a->item_rows == 128) return set_error(NT_ERR_UNSUPPORTED, "e4m3 attention: 256-row items only");
   const int rows = attn_item_rows(a);
   const int nq = rows / 128;
-  if (e4m3 && (a->head_dim != 128 || a->mask_kind == NT_MASK_TENSOR))
+  if (e4m3 && (a->head_dim != 128 || a->mask_kind == NT_MASK_TENSOR || a->mask_kind == NT_MASK_BITS))
     return set_error(NT_ERR_UNSUPPORTED, "e4m3 attention: head_dim 128, no or causal mask");
   const int D = a->head_dim;
   const size_t in_elem = e4m3 ? 1 : 2;
@@ -402,6 +408,47 @@ extern "C" int nt_debug_set_cta_times(unsigned long long* buf) {
   return check_cuda(cudaGetLastError(), "nt_debug_set_cta_times");
 }
 #endif
+
+// 0 / -inf fp32 Mask -> visibility bits (bit j % 32 of word j / 32 of a row: key j
+// visible); words past seq_kv are zero.  Any other value sets *flag bit 0 (the
+// mask is not a pure 0 / -inf pattern: use NT_MASK_TENSOR).
+__global__ void mask_to_bits_kernel(const float* __restrict__ mask, int64_t n, int64_t m, int64_t stride,
+                                    uint32_t* __restrict__ bits, int64_t words, int* flag) {
+  const int64_t row = blockIdx.y;
+  const float* src = mask + row * stride;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < words; w += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t b = 0;
+    bool bad = false;
+    const int64_t j0 = w * 32;
+    if (j0 < m) {
+#pragma unroll 8
+      for (int i = 0; i < 32; ++i) {
+        const int64_t j = j0 + i;
+        if (j < m) {
+          const float x = __ldg(src + j);
+          if (x == 0.f) b |= 1u << i;
+          else if (!(isinf(x) && x < 0.f)) bad = true;
+        }
+      }
+    }
+    bits[row * words + w] = b;
+    if (bad && flag) atomicOr(flag, 1);
+  }
+}
+
+extern "C" int nt_mask_to_bits(const float* mask, int64_t seq_q, int64_t seq_kv, int64_t row_stride, uint32_t* bits,
+                               int64_t words_per_row, int32_t* flag, void* stream) {
+  if (seq_q <= 0 || seq_kv <= 0) return NT_OK;
+  if (!mask || !bits || words_per_row < (seq_kv + 127) / 128 * 4 || row_stride < seq_kv || seq_q > 65535)
+    return set_error(NT_ERR_INVALID, "nt_mask_to_bits: bad arguments");
+  const int64_t words = words_per_row;
+  const int tpb = 128;
+  const int bx = (int)std::min<int64_t>((words + tpb - 1) / tpb, 64);
+  mask_to_bits_kernel<<<dim3(bx, (unsigned)seq_q), tpb, 0, static_cast<cudaStream_t>(stream)>>>(
+      mask, seq_q, seq_kv, row_stride, bits, words, flag);
+  g_launches++;
+  return check_cuda(cudaGetLastError(), "mask_to_bits");
+}
 
 extern "C" int nt_memcpy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width,
                                  int64_t height, void* stream) {

@@ -40,7 +40,7 @@ from . import _lib, cost
 from . import ma_ir as ir
 from .errors import DivisionByZero, OutOfBounds, UnsupportedMA
 from .recognize import AttentionSpec, GemmChainSpec, recognize
-from .runtime import AttentionPlan, DecodePlan, attn_item_rows, decode_eligible
+from .runtime import AttentionPlan, DecodePlan, attn_item_rows, decode_eligible, pack_mask_bits
 
 
 @dataclass
@@ -168,6 +168,16 @@ def _prepare_attention(spec: AttentionSpec, module: ir.Module, inputs: dict, out
             kind = mask_kind
         if kind == "tensor":
             mask_t = _to_device(mk, dev, spec.mask).float().contiguous()
+            if mask_kind in (None, "auto"):
+                # a pure 0 / -inf mask goes to K1 as one visibility bit per key
+                bits, pure = pack_mask_bits(mask_t)
+                if pure:
+                    kind, mask_t = "bits", bits
+        elif kind == "bits":
+            bits, pure = pack_mask_bits(_to_device(mk, dev, spec.mask).float().contiguous())
+            if not pure:
+                raise UnsupportedMA("mask_kind='bits' needs a Mask of only 0 and -inf")
+            mask_t = bits
     elif mask_kind not in (None, "auto", "none"):
         kind = mask_kind  # caller asserts a structured mask on an unmasked program
     odt = torch.float32 if out_dtype in (None, "fp32", torch.float32) else torch.bfloat16

@@ -70,7 +70,8 @@ class AttentionPlan:
             raise InvalidArguments("q/k/v/o shapes inconsistent")
         self.q, self.k, self.v, self.o, self.mask = q, k, v, o, mask
         self.err = err_flag if err_flag is not None else torch.zeros(1, dtype=torch.int32, device=q.device)
-        kind = {"none": _lib.NT_MASK_NONE, "causal": _lib.NT_MASK_CAUSAL, "tensor": _lib.NT_MASK_TENSOR}[mask_kind]
+        kind = {"none": _lib.NT_MASK_NONE, "causal": _lib.NT_MASK_CAUSAL, "tensor": _lib.NT_MASK_TENSOR,
+                "bits": _lib.NT_MASK_BITS}[mask_kind]
         self.mask_kind = mask_kind
         a = _lib.AttnArgs()
         a.q, a.k, a.v, a.o = _t4(q), _t4(k), _t4(v), _t4(o)
@@ -81,6 +82,11 @@ class AttentionPlan:
         if kind == _lib.NT_MASK_TENSOR:
             if mask is None or mask.dtype != torch.float32 or not mask.is_cuda or mask.stride(-1) != 1:
                 raise InvalidArguments("tensor mask must be a CUDA fp32 [N, M] tensor")
+            a.mask = mask.data_ptr()
+            a.mask_stride_row = mask.stride(0)
+        elif kind == _lib.NT_MASK_BITS:
+            if mask is None or mask.dtype != torch.int32 or not mask.is_cuda or mask.stride(-1) != 1:
+                raise InvalidArguments("bit mask must be a CUDA int32 [N, words] tensor (pack_mask_bits)")
             a.mask = mask.data_ptr()
             a.mask_stride_row = mask.stride(0)
         a.out_dtype = _lib.NT_DTYPE_F32 if o.dtype == torch.float32 else _lib.NT_DTYPE_BF16
@@ -143,6 +149,20 @@ class AttentionPlan:
             raise DivisionByZero("tile divide: softmax denominator is zero (row fully masked)")
         if flag >> 8:
             raise RuntimeError(f"device pipeline timeout (wait codes {[c for c in range(16) if flag >> (8 + c) & 1]})")
+
+
+def pack_mask_bits(mask: torch.Tensor, stream=None):
+    """fp32 CUDA Mask [N, M] -> (int32 [N, ceil(M/128)*4] visibility bits, pure) where
+    ``pure`` says every value was 0 or -inf (only then may K1 use NT_MASK_BITS)."""
+    if mask.dtype != torch.float32 or not mask.is_cuda or mask.dim() != 2 or mask.stride(-1) != 1:
+        raise InvalidArguments("mask must be a CUDA fp32 [N, M] tensor with unit column stride")
+    n, m = mask.shape
+    words = -(-m // 128) * 4
+    bits = torch.empty((n, words), dtype=torch.int32, device=mask.device)
+    flag = torch.zeros(1, dtype=torch.int32, device=mask.device)
+    _lib.check(_lib.lib().nt_mask_to_bits(mask.data_ptr(), n, m, mask.stride(0), bits.data_ptr(), words,
+                                          flag.data_ptr(), _stream_handle(stream)), "nt_mask_to_bits")
+    return bits, int(flag.item()) == 0
 
 
 def attn_kv_slots(d: int, ma_stages: int, nq: int = 2) -> int:

@@ -77,6 +77,7 @@ CASES = [
          mask="causal"),
     dict(name="llama2k", prog="llama", bind=dict(N=2048, M=2048, D=128), seeds=[0], io=False),
     dict(name="causal2k", prog="llama_causal", bind=dict(N=2048, M=2048, D=128), seeds=[0], io=False),
+    dict(name="causal4k", prog="llama_causal", bind=dict(N=4096, M=4096, D=128), seeds=[0], io=False),
     dict(name="causal8k", prog="llama_causal", bind=dict(N=8192, M=8192, D=128), seeds=[0], io=False),
     dict(name="causal16k", prog="llama_causal", bind=dict(N=16384, M=16384, D=128), seeds=[0], io=False),
     dict(name="decode4", prog="llama", bind=dict(N=4, M=2048, D=128), seeds=[0], io=True),

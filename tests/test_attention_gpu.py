@@ -608,3 +608,63 @@ def test_one_shot_abi_entry_equals_the_plan_launch():
     torch.cuda.synchronize()
     plan.check_errors()
     assert torch.equal(o1, o2)
+
+
+# ------------------------------------------------------------ 0 / -inf masks as bits
+@pytest.mark.parametrize("N,M,D,density,rows", [(256, 384, 64, 0.3, 256), (1000, 700, 128, 0.6, 256),
+                                               (512, 512, 64, 0.05, 128), (300, 1100, 128, 0.95, 128)])
+def test_bit_mask_vs_fp64_and_tensor_path(N, M, D, density, rows):
+    """A 0 / -inf Mask packed to bits (nt_mask_to_bits) gives the fp32-mask result
+    (within rounding) and the fp64 oracle's; ragged M, both item sizes."""
+    from paper_2604_14825_b200.runtime import AttentionPlan, pack_mask_bits
+
+    g = np.random.default_rng(N + M)
+    mk = np.where(g.random((N, M)) < density, -np.inf, 0.0).astype(np.float32)
+    mk[:, g.integers(0, M, N)] = 0.0  # keep a visible key in most rows
+    mk[np.arange(N), g.integers(0, M, N)] = 0.0
+    q, k, v = _rand((1, 1, N, D), 101), _rand((1, 1, M, D), 102), _rand((1, 1, M, D), 103)
+    dev = torch.device("cuda")
+    tq, tk, tv = (torch.from_numpy(x).to(dev).bfloat16() for x in (q, k, v))
+    tm = torch.from_numpy(mk).to(dev)
+    bits, pure = pack_mask_bits(tm)
+    assert pure and bits.shape == (N, -(-M // 128) * 4)
+    # the bits themselves
+    hb = bits.cpu().numpy().view(np.uint32)
+    for i in (0, N // 2, N - 1):
+        vis = [(hb[i, j // 32] >> (j % 32)) & 1 for j in range(hb.shape[1] * 32)]
+        assert vis[:M] == list((mk[i] == 0).astype(int)) and not any(vis[M:])
+    outs = []
+    for kind, m_ in (("bits", bits), ("tensor", tm)):
+        o = torch.full((1, 1, N, D), float("nan"), device=dev)
+        plan = AttentionPlan(tq, tk, tv, o, D ** -0.5, kind, m_, item_rows=rows)
+        plan.launch()
+        torch.cuda.synchronize()
+        plan.check_errors()
+        outs.append(o)
+    ref = reference_math.attention_fp64(q[0, 0], k[0, 0], v[0, 0], D ** -0.5, mk)
+    for o in outs:
+        _check(o[0, 0].cpu().numpy(), ref)
+    assert float((outs[0] - outs[1]).abs().max()) < 2e-3
+
+
+def test_bit_mask_detection_in_execute_ma():
+    from paper_2604_14825_b200 import execute_ma
+    from paper_2604_14825_b200.runtime import pack_mask_bits
+
+    mod, inputs, interp32, ref64 = load_golden("causal512")
+    g = np.random.default_rng(5)
+    mk = np.where(g.random((512, 512)) < 0.5, -np.inf, 0.0).astype(np.float32)
+    mk[:, 0] = 0.0
+    ins = dict(inputs, Mask=mk)
+    bufs, rep = execute_ma(mod, ins)
+    assert rep.realisation[0]["mask"] == "bits"
+    got = np.asarray(bufs[mod.output])
+    scale = 0.08838834764831845
+    ref = reference_math.attention_fp64(ins["Q"], ins["K"], ins["V"], scale, mk)
+    _check(got, ref)
+    mk2 = mk.copy()
+    mk2[3, 5] = -1.5  # not 0 / -inf: the fp32 tensor path
+    _, pure = pack_mask_bits(torch.from_numpy(mk2).cuda())
+    assert not pure
+    bufs, rep = execute_ma(mod, dict(inputs, Mask=mk2))
+    assert rep.realisation[0]["mask"] == "tensor"
