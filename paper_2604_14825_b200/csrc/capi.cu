@@ -125,7 +125,7 @@ int make_map_pages_5d(CUtensorMap* m, const void* ptr, int64_t page_size, int64_
 // ----------------------------------------------------------------- attention
 // Split-KV plan (host restatement of attn_unit's prefix): kv_split = 0 unless the
 // heaviest item exceeds 2x the per-SM average of KV-tile steps (few, long items:
-// one kv-group per GPU at 8 GPUs); then items are cut into ~avg/3-tile units.
+// one kv-group per GPU at 8 GPUs); then items are cut into ~1.1 x avg-tile units.
 // Measured (tools/split_probe.py, Llama 8K causal): Hq=4 131 -> 101 us; Hq=8
 // (1.1x) 135 -> 153-185 us -- each unit reloads Q, stores an fp32 partial and
 // refills the pipeline, so splitting only pays when the heaviest item dominates.
@@ -168,7 +168,11 @@ static AttnSplit attn_split_plan(const nt_attn_args* a) {
   const double avg = (double)total / (num_sms() * (rows == 128 ? 2 : 1));
   // experiment overrides: NT_ATTN_SPLIT_THRESH (x avg), NT_ATTN_SPLIT_DIV (avg / div tiles per unit)
   static const double thresh = getenv("NT_ATTN_SPLIT_THRESH") ? atof(getenv("NT_ATTN_SPLIT_THRESH")) : 2.0;
-  static const double div = getenv("NT_ATTN_SPLIT_DIV") ? atof(getenv("NT_ATTN_SPLIT_DIV")) : 3.0;
+  // div 0.9 (units of ~1.1x the per-CTA average) measured best for one kv-group of
+  // Llama 8K causal (r02 sweep, main kernel + merge): div 3 102.8 us, 1.5 106.8,
+  // 1.2 108.0, 1.0 93.4, 0.9 88.3, 0.75 100.6, 0.6 116.1 -- fewer, longer units
+  // write fewer fp32 partials and the merge reads fewer (10 vs 18 us)
+  static const double div = getenv("NT_ATTN_SPLIT_DIV") ? atof(getenv("NT_ATTN_SPLIT_DIV")) : 0.9;
   if (mx <= thresh * avg) return sp;
   // >= 4 tiles per unit; <= 32 units per item (the combine holds one chunk per lane)
   const int S = std::max(std::max(4, (int)std::ceil(avg / div)), (mx + 31) / 32);

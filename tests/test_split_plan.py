@@ -24,48 +24,55 @@ def _args(B, Hq, Hkv, N, M, D, mask):
     return a
 
 
-def _nkv(mb, N, M, causal, off=0):
+def _rows(B, Hq, N):
+    """Library choice of query rows per work item (capi.cu attn_item_rows, item_rows = 0)."""
+    return 128 if (N + 255) // 256 * B * Hq * 2 < SMS else 256
+
+
+def _nkv(mb, N, M, causal, off=0, rows=256):
     total = (M + 127) // 128
     if not causal:
         return total
-    last_q = min(mb * 256 + 255, N - 1) + off
+    last_q = min(mb * rows + rows - 1, N - 1) + off
     return max(min(total, last_q // 128 + 1), 1)
 
 
 def _plan(B, Hq, N, M, D, causal):
     """Restatement of attn_split_plan: (kv_split, n_units, workspace bytes)."""
-    nmb = (N + 255) // 256
+    rows = _rows(B, Hq, N)
+    nmb = (N + rows - 1) // rows
     BH = B * Hq
-    nk = [_nkv(mb, N, M, causal) for mb in range(nmb)]
+    nk = [_nkv(mb, N, M, causal, rows=rows) for mb in range(nmb)]
     total = sum(nk) * BH
-    avg = total / SMS
+    avg = total / (SMS * (2 if rows == 128 else 1))
     mx = max(nk)
     if nmb > 384 or mx <= 2.0 * avg:
         return 0, nmb * BH, 0
-    S = max(max(4, math.ceil(avg / 3.0)), (mx + 31) // 32)
+    S = max(max(4, math.ceil(avg / 0.9)), (mx + 31) // 32)
     if S >= mx:
         return 0, nmb * BH, 0
     units = sum((n + S - 1) // S for n in nk) * BH
     prefix = ((nmb + 1) * 4 + 255) // 256 * 256
-    ml = (units * 256 * 8 + 255) // 256 * 256
-    return S, units, prefix + ml + units * 256 * D * 4
+    ml = (units * rows * 8 + 255) // 256 * 256
+    return S, units, prefix + ml + units * rows * D * 4
 
 
 def _units(B, Hq, N, M, causal, S):
     """Restatement of the kernel's unit map: unit -> (b*Hq + hq, m-block, first tile, tiles)."""
-    nmb = (N + 255) // 256
+    rows = _rows(B, Hq, N)
+    nmb = (N + rows - 1) // rows
     BH = B * Hq
     prefix = [0]
     for i in range(nmb):
         mb = nmb - 1 - i if causal else i
-        prefix.append(prefix[-1] + (_nkv(mb, N, M, causal) + S - 1) // S * BH)
+        prefix.append(prefix[-1] + (_nkv(mb, N, M, causal, rows=rows) + S - 1) // S * BH)
     out = []
     for w in range(prefix[-1]):
         lo = max(i for i in range(nmb) if prefix[i] <= w)
         r = w - prefix[lo]
         c, bh = divmod(r, BH)
         mb = nmb - 1 - lo if causal else lo
-        n_full = _nkv(mb, N, M, causal)
+        n_full = _nkv(mb, N, M, causal, rows=rows)
         out.append((bh, mb, c * S, min(S, n_full - c * S)))
     return out
 
@@ -91,8 +98,10 @@ def test_split_plan_matches_library_and_covers_every_tile(B, Hq, Hkv, N, M, D, c
         assert 1 <= n <= S
         for j in range(lo, lo + n):
             cover[(bh, mb, j)] = cover.get((bh, mb, j), 0) + 1
-    nmb = (N + 255) // 256
-    want = {(bh, mb, j) for bh in range(B * Hq) for mb in range(nmb) for j in range(_nkv(mb, N, M, causal))}
+    rows = _rows(B, Hq, N)
+    nmb = (N + rows - 1) // rows
+    want = {(bh, mb, j) for bh in range(B * Hq) for mb in range(nmb)
+            for j in range(_nkv(mb, N, M, causal, rows=rows))}
     assert set(cover) == want and all(v == 1 for v in cover.values())
     assert len(_units(B, Hq, N, M, causal, S)) == units
 
