@@ -77,6 +77,7 @@ struct AttnFwdParams {
   // merges with the repair law.  kv_split = 0: one unit per item (n_items units).
   int kv_split;
   int* unit_prefix;  // [n_mblocks + 1] units before each m-block position (written by CTA 0)
+  int n_split_mb;    // m-block positions 0 .. n_split_mb-1 (LPT order) hold split items (the merge grid)
   float2* part_ml;   // [unit][256 rows] (m, l)
 };
 constexpr int kMaxSplitMblocks = 384;  // prefix table size in shared memory
@@ -949,8 +950,11 @@ __global__ void __launch_bounds__(attn_threads<NQ>(), NQ == 2 ? 1 : 2)
 
 // Split-KV merge: O[row] = o_scale * sum_c w_c O_c[row] / sum_c w_c l_c with
 // w_c = exp2(m_c - max m) (the repair law, tilecc/schedule/repair.py:80-88).
-// Block = 8 rows (one warp per row, D/32 columns per lane) of one (m-block
-// position, batch x head); m-blocks with a single unit exit at once.
+// Block = 32 rows of one (split m-block position, batch x head): 8 warps x 4 rows,
+// D/32 columns per lane; the grid covers only the split positions (the heaviest
+// m-blocks in LPT order), and each warp issues all its rows' partial loads
+// before the FMAs.
+constexpr int kCombineRowsPerWarp = 4;
 template <int D, int MASK, bool OUT_F32, int ROWS = 256>
 __global__ void __launch_bounds__(256) attn_combine_kernel(const float* __restrict__ part_o, const AttnFwdParams p) {
   const int mbi = blockIdx.z, bh = blockIdx.y;
@@ -959,67 +963,90 @@ __global__ void __launch_bounds__(256) attn_combine_kernel(const float* __restri
   const int nc = (n_full + p.kv_split - 1) / p.kv_split;
   if (nc <= 1) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int row = blockIdx.x * 8 + warp;  // 0..ROWS-1 within the m-block
-  const int qr = mb * ROWS + row;
-  if (qr >= p.N) return;
   const int BH = p.B * p.Hq;
   const int u0 = p.unit_prefix[mbi] + bh;
-  // (m, l) of every chunk in one round trip: lane c holds chunk c (nc <= 32 by construction)
-  float mc = f_ninf(), lc = 0.f;
-  if (lane < nc) {
-    const float2 ml = p.part_ml[(long long)(u0 + lane * BH) * ROWS + row];
-    mc = ml.x;
-    lc = ml.y;
-  }
-  float m = mc;
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-  const float wgt = (lane < nc && mc != f_ninf()) ? ex2(mc - m) : 0.f;
-  float lsum = wgt * lc;
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, off);
   constexpr int CPL = D / 32;  // columns per lane
-  float acc[CPL];
-#pragma unroll
-  for (int i = 0; i < CPL; ++i) acc[i] = 0.f;
-  const float* base = part_o + ((long long)u0 * ROWS + row) * D + lane * CPL;
   const long long cstride = (long long)BH * ROWS * D;
-  for (int c0 = 0; c0 < nc; c0 += 4) {
-    float v[4][CPL];
+  const int b = bh / p.Hq, hq = bh % p.Hq;
+#pragma unroll 1
+  for (int rr = 0; rr < kCombineRowsPerWarp; ++rr) {
+    const int row = blockIdx.x * (8 * kCombineRowsPerWarp) + warp * kCombineRowsPerWarp + rr;  // within the m-block
+    const int qr = mb * ROWS + row;
+    if (qr >= p.N) break;
+    // (m, l) of every chunk in one round trip: lane c holds chunk c (nc <= 32 by construction)
+    float mc = f_ninf(), lc = 0.f;
+    if (lane < nc) {
+      const float2 ml = p.part_ml[(long long)(u0 + lane * BH) * ROWS + row];
+      mc = ml.x;
+      lc = ml.y;
+    }
+    const float* base = part_o + ((long long)u0 * ROWS + row) * D + lane * CPL;
+    // the first chunks' O rows are loaded while the (m, l) reduction runs
+    float v0[4][CPL];
 #pragma unroll
-    for (int k = 0; k < 4; ++k)  // four chunks' loads in flight before the FMAs
-      if (c0 + k < nc) {
+    for (int k = 0; k < 4; ++k)
+      if (k < nc) {
 #pragma unroll
         for (int i = 0; i < CPL; i += 2) {
-          const float2 x = __ldg(reinterpret_cast<const float2*>(base + (c0 + k) * cstride + i));
-          v[k][i] = x.x;
-          v[k][i + 1] = x.y;
+          const float2 x = __ldg(reinterpret_cast<const float2*>(base + k * cstride + i));
+          v0[k][i] = x.x;
+          v0[k][i + 1] = x.y;
         }
       }
+    float m = mc;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+    const float wgt = (lane < nc && mc != f_ninf()) ? ex2(mc - m) : 0.f;
+    float lsum = wgt * lc;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, off);
+    float acc[CPL];
+#pragma unroll
+    for (int i = 0; i < CPL; ++i) acc[i] = 0.f;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const float w = __shfl_sync(0xffffffffu, wgt, (c0 + k) & 31);
-      if (c0 + k < nc) {
+      const float w = __shfl_sync(0xffffffffu, wgt, k);
+      if (k < nc) {
 #pragma unroll
-        for (int i = 0; i < CPL; ++i) acc[i] += w * v[k][i];
+        for (int i = 0; i < CPL; ++i) acc[i] += w * v0[k][i];
       }
     }
-  }
-  if (!(lsum > 0.f)) {
-    if (lane == 0 && p.err) atomicOr(p.err, 1);
-    lsum = 0.f;
-  }
-  const float inv = (lsum > 0.f) ? p.o_scale / lsum : 0.f;
-  const int b = bh / p.Hq, hq = bh % p.Hq;
-  const long long off = (long long)b * p.o_sb + (long long)hq * p.o_sh + (long long)qr * p.o_sn + lane * CPL;
-  if (OUT_F32) {
-    float* dst = static_cast<float*>(p.o) + off;
+    for (int c0 = 4; c0 < nc; c0 += 4) {
+      float v[4][CPL];
 #pragma unroll
-    for (int i = 0; i < CPL; i += 2) *reinterpret_cast<float2*>(dst + i) = make_float2(acc[i] * inv, acc[i + 1] * inv);
-  } else {
-    __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.o) + off;
+      for (int k = 0; k < 4; ++k)
+        if (c0 + k < nc) {
 #pragma unroll
-    for (int i = 0; i < CPL; i += 2) *reinterpret_cast<uint32_t*>(dst + i) = pack_bf16(acc[i] * inv, acc[i + 1] * inv);
+          for (int i = 0; i < CPL; i += 2) {
+            const float2 x = __ldg(reinterpret_cast<const float2*>(base + (c0 + k) * cstride + i));
+            v[k][i] = x.x;
+            v[k][i + 1] = x.y;
+          }
+        }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float w = __shfl_sync(0xffffffffu, wgt, (c0 + k) & 31);
+        if (c0 + k < nc) {
+#pragma unroll
+          for (int i = 0; i < CPL; ++i) acc[i] += w * v[k][i];
+        }
+      }
+    }
+    if (!(lsum > 0.f)) {
+      if (lane == 0 && p.err) atomicOr(p.err, 1);
+      lsum = 0.f;
+    }
+    const float inv = (lsum > 0.f) ? p.o_scale / lsum : 0.f;
+    const long long off = (long long)b * p.o_sb + (long long)hq * p.o_sh + (long long)qr * p.o_sn + lane * CPL;
+    if (OUT_F32) {
+      float* dst = static_cast<float*>(p.o) + off;
+#pragma unroll
+      for (int i = 0; i < CPL; i += 2) *reinterpret_cast<float2*>(dst + i) = make_float2(acc[i] * inv, acc[i + 1] * inv);
+    } else {
+      __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.o) + off;
+#pragma unroll
+      for (int i = 0; i < CPL; i += 2) *reinterpret_cast<uint32_t*>(dst + i) = pack_bf16(acc[i] * inv, acc[i + 1] * inv);
+    }
   }
 }
 

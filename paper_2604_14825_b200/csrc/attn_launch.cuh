@@ -98,7 +98,8 @@ int launch_attn(const AttnMaps& m, const AttnFwdParams& p, cudaStream_t st) {
       if (rc || g_prepare_only) return rc;
       // split-KV items: merge the fp32 partials
       constexpr int ROWS = 128 * NQ;
-      attn_combine_kernel<D, MASK, F32, ROWS><<<dim3(ROWS / 8, p.B * p.Hq, p.n_mblocks), 256, 0, st>>>(m.part_o, p);
+      attn_combine_kernel<D, MASK, F32, ROWS>
+          <<<dim3(ROWS / (8 * kCombineRowsPerWarp), p.B * p.Hq, p.n_split_mb), 256, 0, st>>>(m.part_o, p);
       g_launches++;
       return check_cuda(cudaGetLastError(), "attn_combine launch");
     }

@@ -131,6 +131,7 @@ int make_map_pages_5d(CUtensorMap* m, const void* ptr, int64_t page_size, int64_
 // refills the pipeline, so splitting only pays when the heaviest item dominates.
 struct AttnSplit {
   int kv_split = 0, n_units = 0;
+  int n_split_mb = 0;  // m-block positions (LPT order: heaviest first) whose items are split
   int64_t bytes = 0, off_ml = 0, off_o = 0;
 };
 // Query rows per work item: 256 (two 128-row tiles, one CTA per SM) or 128 (one
@@ -178,7 +179,10 @@ static AttnSplit attn_split_plan(const nt_attn_args* a) {
   const int S = std::max(std::max(4, (int)std::ceil(avg / div)), (mx + 31) / 32);
   if (S >= mx) return sp;
   long long units = 0;
-  for (int mb = 0; mb < nmb; ++mb) units += (nkv(mb) + S - 1) / S * BH;
+  for (int mb = 0; mb < nmb; ++mb) {
+    units += (nkv(mb) + S - 1) / S * BH;
+    sp.n_split_mb += nkv(mb) > S;
+  }
   sp.kv_split = S;
   sp.n_units = (int)units;
   const int64_t prefix_bytes = ((int64_t)(nmb + 1) * 4 + 255) / 256 * 256;
@@ -293,6 +297,7 @@ static int attn_build(const nt_attn_args* a, AttnMaps& m, AttnFwdParams& p, int&
     char* ws = static_cast<char*>(a->workspace);
     p.kv_split = sp.kv_split;
     p.n_items = sp.n_units;
+    p.n_split_mb = sp.n_split_mb;
     p.unit_prefix = reinterpret_cast<int*>(ws);
     p.part_ml = reinterpret_cast<float2*>(ws + sp.off_ml);
     m.part_o = reinterpret_cast<float*>(ws + sp.off_o);
