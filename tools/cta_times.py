@@ -26,3 +26,6 @@ t0 = t[:, 0].min()
 start = (t[:, 0] - t0) / 1e3; end = (t[:, 1] - t0) / 1e3
 print(f"event {e0.elapsed_time(e1)*1e3:.1f} us; CTAs {len(t)}; start spread {start.max():.1f} us; "
       f"end: min {end.min():.1f} median {sorted(end)[len(end)//2]:.1f} max {end.max():.1f} us")
+import numpy as np
+e = np.sort(end)
+print("end-time deciles (us):", " ".join(f"{x:.1f}" for x in np.percentile(e, [0, 10, 25, 50, 75, 90, 100])))

@@ -54,26 +54,34 @@ def k1():
         (1, 1, 1, 129, 129, 128, "none", True),
         (1, 4, 1, 2048, 2048, 128, "causal", True),   # split-KV units + combine
         (1, 2, 2, 2048, 2048, 64, "none", False),       # split-KV D=64
+        (1, 2, 1, 640, 700, 128, "bits", True),         # 0 / -inf mask as bits (128-row items)
+        (4, 8, 8, 512, 512, 64, "bits", False),
     ]
     for B, Hq, Hkv, N, M, D, kind, f32 in cases:
         q, k, v = rnd((B, Hq, N, D), 1), rnd((B, Hkv, M, D), 2), rnd((B, Hkv, M, D), 3)
         mask = None
-        if kind == "tensor":
+        if kind in ("tensor", "bits"):
             g = np.random.default_rng(4)
             mask = np.where(g.random((N, M)) < 0.3, -np.inf, 0.0).astype(np.float32)
             mask[:, 0] = 0.0
         tq, tk, tv = (torch.from_numpy(x).to(DEV).bfloat16() for x in (q, k, v))
         o = nan_filled((B, Hq, N, D), dtype=torch.float32 if f32 else torch.bfloat16, device=DEV)
-        plan = AttentionPlan(tq, tk, tv, o, 1 / np.sqrt(D), kind,
-                             torch.from_numpy(mask).to(DEV) if mask is not None else None)
+        mt = torch.from_numpy(mask).to(DEV) if mask is not None else None
+        if kind == "bits":
+            from paper_2604_14825_b200.runtime import pack_mask_bits
+            mt = pack_mask_bits(mt)[0]
+        plan = AttentionPlan(tq, tk, tv, o, 1 / np.sqrt(D), kind, mt)
         plan.launch()
         torch.cuda.synchronize()
         plan.check_errors()
         if mask is not None:
-            ref = reference_math.attention_fp64(q[0, 0], k[0, 0], v[0, 0], 1 / np.sqrt(D), mask=mask)[None, None]
+            ref = np.stack([np.stack([reference_math.attention_fp64(q[b, h], k[b, h * Hkv // Hq], v[b, h * Hkv // Hq],
+                                                                    1 / np.sqrt(D), mask=mask)
+                                      for h in range(Hq)]) for b in range(B)])
         else:
             ref = reference_math.attention_batched_fp64(q, k, v, 1 / np.sqrt(D), kind == "causal")
-        close(o.float().cpu().numpy(), ref, what=f"k1 {kind} D={D} N={N} split={plan.ws is not None}")
+        close(o.float().cpu().numpy(), ref,
+              what=f"k1 {kind} D={D} N={N} rows={plan.item_rows} split={plan.ws is not None}")
     # e4m3
     B, Hq, Hkv, N, D = 1, 2, 1, 384, 128
     q, k, v = rnd((B, Hq, N, D), 5), rnd((B, Hkv, N, D), 6), rnd((B, Hkv, N, D), 7)
