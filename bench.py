@@ -83,6 +83,7 @@ CONFIGS = {
 }
 DEFAULT_CONFIG = "llama8k_causal"
 METRIC = "fused-attention bf16 TFLOP/s & % tensor peak; box throughput at 1/2/4/8 GPUs"
+READ_CEILING_GBS = 7398.7  # tools/ubench/bulk_read.cu, B200, r02 (HBM read-only stream through TMA)
 
 
 def load_peaks():
@@ -581,9 +582,13 @@ def run_ours(args, cfg, rank, world, dist):
         achieved = w["local_bytes"] / (ms_kernel_local * 1e-3) / 1e9
         peak = peaks["hbm_gbs"]
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})",
+                "traffic": traffic, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src}; a copy: read + write)",
+                # the decode stream only reads: its ceiling is the TMA read rate, measured with
+                # tools/ubench/bulk_read.cu on this pool's B200 (r02: 7398 GB/s, 192 KB in flight per SM)
+                "read_ceiling_gbs": READ_CEILING_GBS, "frac_of_read_ceiling": achieved / READ_CEILING_GBS,
                 "algorithmic_bytes_per_launch": w["local_bytes"],
-                "kernel": "decode_split_kernel<paged> + combine" if cfg.get("page_size") else "decode_split_kernel + combine"}
+                "kernel": ("decode_split_kernel<paged> (FMA-pipe dots) + combine" if cfg.get("page_size")
+                           else "decode_tc_kernel (tcgen05 dots) + combine")}
     else:
         achieved = w["local_flops"] / (ms_kernel_local * 1e-3) / 1e12
         peak = peaks["bf16_tflops"] * (2.0 if w.get("e4m3") else 1.0)

@@ -83,6 +83,30 @@ int make_map_4d(CUtensorMap* m, const void* ptr, int64_t D, int64_t S, int64_t H
   return NT_OK;
 }
 
+// rank-4 map with an explicit box (dims innermost first, strides in elements for dims 1-3)
+int make_map_4d_box(CUtensorMap* m, const void* ptr, const int64_t dims[4], const int64_t strides[3],
+                    const int box[4], size_t elem) {
+  EncodeFn enc = get_encode();
+  if (!enc) return set_error(NT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if (reinterpret_cast<uintptr_t>(ptr) % 16) return set_error(NT_ERR_INVALID, "tensor base not 16B aligned");
+  cuuint64_t d[4], st[3];
+  cuuint32_t bx[4], estr[4] = {1, 1, 1, 1};
+  for (int i = 0; i < 4; ++i) {
+    d[i] = (cuuint64_t)dims[i];
+    bx[i] = (cuuint32_t)box[i];
+  }
+  for (int i = 0; i < 3; ++i) {
+    st[i] = (cuuint64_t)(strides[i] * elem);
+    if (st[i] % 16) return set_error(NT_ERR_INVALID, "tensor strides must be multiples of 16 bytes");
+    if (st[i] == 0) st[i] = 16;
+  }
+  CUresult r = enc(m, elem == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+                   const_cast<void*>(ptr), d, st, bx, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(NT_ERR_INVALID, "cuTensorMapEncodeTiled(4d box) failed (" + std::to_string((int)r) + ")");
+  return NT_OK;
+}
+
 int make_map_2d(CUtensorMap* m, const void* ptr, int64_t inner, int64_t outer, int64_t ld, int box_inner,
                 int box_outer, size_t elem, CUtensorMapSwizzle swz) {
   EncodeFn enc = get_encode();

@@ -15,6 +15,8 @@ int num_sms();  // SMs of the current device (persistent grids)
 int make_map_4d(CUtensorMap* m, const void* ptr, int64_t D, int64_t S, int64_t H, int64_t B, int64_t sS,
                 int64_t sH, int64_t sB, int box_rows, size_t elem, int box_inner = 0,
                 CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B);
+int make_map_4d_box(CUtensorMap* m, const void* ptr, const int64_t dims[4], const int64_t strides[3],
+                    const int box[4], size_t elem);
 int make_map_pages_5d(CUtensorMap* m, const void* ptr, int64_t page_size, int64_t heads, int64_t pages,
                       int64_t token_stride, int64_t head_stride, int64_t page_stride, int rows);
 int make_map_2d(CUtensorMap* m, const void* ptr, int64_t inner, int64_t outer, int64_t ld, int box_inner,

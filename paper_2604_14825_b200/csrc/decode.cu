@@ -7,6 +7,7 @@
 #include "../../include/nautilus_b200.h"
 #include "common_host.h"
 #include "decode.cuh"
+#include "decode_tc.cuh"
 
 using namespace nt;
 
@@ -67,6 +68,36 @@ int dispatch(int R, const CUtensorMap& mk, const CUtensorMap& mv, DecodeParams& 
     default: return launch<8, PG>(mk, mv, p, st);
   }
 }
+// K2b (tensor-core dots) for dense K/V; NT_DECODE_FMA=1 keeps K2 (A/B experiments)
+bool use_tc_decode() {
+  static const bool fma = getenv("NT_DECODE_FMA") && atoi(getenv("NT_DECODE_FMA")) != 0;
+  return !fma;
+}
+
+template <int R>
+int launch_tc(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, DecodeParams& p, cudaStream_t st) {
+  int rc;
+  constexpr auto kern = decode_tc_kernel<R>;
+  if ((rc = configure_smem<kern>(kDtcSmem, "cudaFuncSetAttribute(decode_tc)"))) return rc;
+  dim3 grid(p.splits, p.B * p.Hkv);
+  kern<<<grid, kDtcThreads, kDtcSmem, st>>>(mq, mk, mv, p);
+  g_launches++;
+  if ((rc = check_cuda(cudaGetLastError(), "decode_tc launch"))) return rc;
+  const int rows = p.B * p.Hkv * R;
+  decode_combine_kernel<<<(rows + 3) / 4, 128, 0, st>>>(p, R);
+  g_launches++;
+  return check_cuda(cudaGetLastError(), "decode_combine launch");
+}
+
+int dispatch_tc(int R, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, DecodeParams& p,
+                cudaStream_t st) {
+  switch (R) {
+    case 1: return launch_tc<1>(mq, mk, mv, p, st);
+    case 2: return launch_tc<2>(mq, mk, mv, p, st);
+    case 4: return launch_tc<4>(mq, mk, mv, p, st);
+    default: return launch_tc<8>(mq, mk, mv, p, st);
+  }
+}
 }  // namespace
 
 extern "C" int64_t nt_decode_workspace_bytes(int32_t batch, int32_t heads_kv, int32_t rows_per_group,
@@ -110,6 +141,22 @@ extern "C" int nt_attn_decode(const nt_decode_args* a, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   CUtensorMap mk, mv;
   int rc;
+  if (use_tc_decode()) {
+    // K2b: 128-key tiles; the group's R query rows as one 4-D box {64, Nq, g, 1}
+    p.keys_per_split = ((a->seq_kv + p.splits - 1) / p.splits + kDtcTile - 1) / kDtcTile * kDtcTile;
+    CUtensorMap mq;
+    const int64_t qd[4] = {a->head_dim, a->seq_q, a->heads_q, a->batch};
+    const int64_t qs[3] = {a->q.stride_s, a->q.stride_h, a->q.stride_b};
+    const int qb[4] = {64, a->seq_q, g, 1};
+    if ((rc = make_map_4d_box(&mq, a->q.ptr, qd, qs, qb, 2))) return rc;
+    if ((rc = make_map_pages_5d(&mk, a->k.ptr, a->seq_kv, a->heads_kv, a->batch, a->k.stride_s, a->k.stride_h,
+                                a->k.stride_b, kDtcTile)))
+      return rc;
+    if ((rc = make_map_pages_5d(&mv, a->v.ptr, a->seq_kv, a->heads_kv, a->batch, a->v.stride_s, a->v.stride_h,
+                                a->v.stride_b, kDtcTile)))
+      return rc;
+    return dispatch_tc(R, mq, mk, mv, p, st);
+  }
   // one 5-D box {64 dims, 64 keys, 2 panels} per K or V tile (a batch entry is a "page"
   // of seq_kv tokens): both 64-dim panels in one TMA, laid out [panel][64 keys][128 B]
   if ((rc = make_map_pages_5d(&mk, a->k.ptr, a->seq_kv, a->heads_kv, a->batch, a->k.stride_s, a->k.stride_h,

@@ -1,0 +1,240 @@
+// K2b: split-KV decode attention on the tensor cores -- HBM-bound.
+//
+// Same work decomposition and partial format as K2 (decode.cuh): one CTA per
+// (split, batch x kv-head group), the group's R = (Hq/Hkv) * Nq query rows run
+// the rolling-update recurrence over the split's key range and leave an fp32
+// partial (O unnormalised, m, l) for decode_combine_kernel (the repair law,
+// tilecc/schedule/repair.py:80-88).  K2 does the dots on the FMA pipe and
+// measured issue-bound (ncu: FFMA2 / FADD / SHF / LOP3 carry ~55 % of the stall
+// samples; 5.6 TB/s against a 7.4 TB/s TMA read ceiling, tools/ubench/bulk_read.cu).
+// Here the dots are tcgen05 MMAs with the R rows padded to M = 128:
+//   S(t)  = Q (128 x 128, rows >= R zero) . K(t)^T      SS, 8 x (M128 N128 K16)
+//   O    += P(t) (TMEM, bf16) . V(t)                     TS, 8 x (M128 N128 K16)
+// 1024 tensor clocks per 128-key K/V tile pair (64 KB) against ~2500 clocks of HBM
+// time per SM.  S is double-buffered in TMEM and P has its own columns, so S(t+1)
+// is computed while the softmax warp works on S(t): the per-tile chain is the
+// softmax alone (~1200 clk: one warp, MUFU-bound), not S + softmax + PV (a first
+// version with P aliasing S measured 5.80 TB/s, this chain ~2900 clk per tile).
+//   warp 0  softmax (TMEM lanes 0-31; lane = row, lanes < R matter), epilogue
+//   warp 1  TMA producer: Q once, then K(t), V(t) through a kDtcStages ring
+//   warp 2  MMA issuer (one thread): S(t+1) ahead, PV(t) when P(t) is ready
+//   warp 3  idle
+// TMEM: S_0 [0,128) S_1 [128,256) P [256,320) O [384,512).
+#pragma once
+#include "attn_fwd.cuh"
+#include "decode.cuh"
+
+namespace nt {
+
+constexpr int kDtcTile = 128;                            // keys per K/V tile
+constexpr int kDtcTileBytes = kDtcTile * kDecodeD * 2;   // 32 KB, two 64-dim SW128 panels
+constexpr int kDtcHalf = kDtcTile * 128;                 // one panel (16 KB)
+constexpr int kDtcStages = 3;                            // K+V tile pairs in flight (192 KB)
+constexpr int kDtcThreads = 128;
+constexpr int kDtcSmem = kDtcTileBytes /* Q */ + kDtcStages * 2 * kDtcTileBytes + 1024 /* align */ + 256;
+
+template <int R>
+__global__ void __launch_bounds__(kDtcThreads, 1)
+    decode_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                     const __grid_constant__ CUtensorMap tmV, const DecodeParams p) {
+  constexpr int D = kDecodeD;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_u32 = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw_u32 + 1023u) & ~1023u) - raw_u32);
+  uint8_t* sQ = smem;
+  uint8_t* sKV = smem + kDtcTileBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + kDtcStages * 2 * kDtcTileBytes);
+  uint64_t* bar_q = bars;
+  uint64_t* full = bars + 1;                 // [2 * stages]: K(t) / V(t) landed
+  uint64_t* empty = full + 2 * kDtcStages;   // [2 * stages]
+  uint64_t* bar_s = empty + 2 * kDtcStages;  // [2] S(t) in S_{t%2}
+  uint64_t* bar_sf = bar_s + 2;              // [2] S_{t%2} loaded into registers (reusable)
+  uint64_t* bar_p = bar_sf + 2;              // P(t) in TMEM
+  uint64_t* bar_pv = bar_p + 1;              // PV(t) done (P and O reusable)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_pv + 1);
+
+  const int s = blockIdx.x;
+  const int grp = blockIdx.y;  // b * Hkv + hkv
+  const int b = grp / p.Hkv, hkv = grp % p.Hkv;
+  const int warp = __shfl_sync(0xffffffffu, threadIdx.x / 32, 0);
+  const int lane = threadIdx.x & 31;
+  const int j0 = s * p.keys_per_split;  // multiple of kDtcTile
+  const int j1 = min(p.M, j0 + p.keys_per_split);
+  const int ntiles = (j1 > j0) ? (j1 - j0 + kDtcTile - 1) / kDtcTile : 0;
+
+  // rows >= R of the padded Q tile are zero (S, P, O rows >= R are never read)
+  for (int i = threadIdx.x; i < kDtcTileBytes / 16; i += kDtcThreads)
+    reinterpret_cast<uint4*>(sQ)[i] = make_uint4(0, 0, 0, 0);
+  fence_proxy_async_smem();
+  if (warp == 1 && lane == 0) {
+    prefetch_tmap(&tmQ);
+    prefetch_tmap(&tmK);
+    prefetch_tmap(&tmV);
+    mbar_init(bar_q, 1);
+    for (int i = 0; i < 2 * kDtcStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bar_s[i], 1);
+      mbar_init(&bar_sf[i], 1);
+    }
+    mbar_init(bar_p, 1);
+    mbar_init(bar_pv, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  constexpr uint32_t kColP = 256, kColO = 384;
+
+  if (warp == 1) {
+    // ================= TMA producer
+    if (lane == 0 && ntiles > 0) {
+      mbar_arrive_expect_tx(bar_q, R * D * 2);
+      // the group's R rows: box {64 dims, Nq rows, g heads, 1} per 64-dim panel
+#pragma unroll
+      for (int h = 0; h < 2; ++h) tma_load_4d(sQ + h * kDtcHalf, &tmQ, bar_q, h * 64, 0, hkv * p.g, b);
+      for (int it = 0; it < 2 * ntiles; ++it) {
+        const int slot = it % (2 * kDtcStages);
+        mbar_wait(&empty[slot], ((it / (2 * kDtcStages)) & 1) ^ 1, p.err, 1);
+        mbar_arrive_expect_tx(&full[slot], kDtcTileBytes);
+        // one 5-D box {64 dims, 128 keys, 2 panels} = [panel][128 keys][128 B]
+        tma_load_5d(sKV + slot * kDtcTileBytes, (it & 1) ? &tmV : &tmK, &full[slot], 0, j0 + (it >> 1) * kDtcTile,
+                    0, hkv, b);
+      }
+    }
+  } else if (warp == 2) {
+    // ================= MMA issuer
+    if (lane == 0 && ntiles > 0) {
+      constexpr uint32_t idS = idesc_bf16(128, 128, 0, 0);
+      constexpr uint32_t idO = idesc_bf16(128, D, 0, 1);
+      const uint32_t sQa = smem_u32(sQ), sKVa = smem_u32(sKV);
+      mbar_wait(bar_q, 0, p.err, 2);
+      auto issue_s = [&](int t) {
+        const int gk = 2 * t, slotK = gk % (2 * kDtcStages);
+        mbar_wait(&full[slotK], (gk / (2 * kDtcStages)) & 1, p.err, 3);
+        if (t >= 2) mbar_wait(&bar_sf[t & 1], ((t >> 1) - 1) & 1, p.err, 6);  // softmax(t-2) read S_{t%2}
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = (k >> 2) * kDtcHalf + (k & 3) * 32;
+          umma_ss(tmem + (t & 1) * 128, sdesc_sw128(sQa + off, 16, 1024),
+                  sdesc_sw128(sKVa + slotK * kDtcTileBytes + off, 16, 1024), idS, k > 0 ? 1u : 0u);
+        }
+        umma_commit(&bar_s[t & 1]);
+        umma_commit(&empty[slotK]);
+      };
+      issue_s(0);
+      for (int t = 0; t < ntiles; ++t) {
+        if (t + 1 < ntiles) issue_s(t + 1);
+        // PV(t): P from its own TMEM columns, V MN-major from shared memory
+        const int gv = 2 * t + 1, slotV = gv % (2 * kDtcStages);
+        mbar_wait(bar_p, t & 1, p.err, 4);
+        mbar_wait(&full[slotV], (gv / (2 * kDtcStages)) & 1, p.err, 5);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < kDtcTile / 16; ++k) {
+          const uint64_t bd = sdesc_sw128(sKVa + slotV * kDtcTileBytes + k * 16 * 128, kDtcHalf, 1024);
+          umma_ts(tmem + kColO, tmem + kColP + k * 8, bd, idO, (t > 0 || k > 0) ? 1u : 0u);
+        }
+        umma_commit(bar_pv);
+        umma_commit(&empty[slotV]);
+      }
+    }
+  } else if (warp == 0) {
+    // ================= softmax: one TMEM lane (= query row) per thread
+    const float NINF = f_ninf();
+    const float sc = p.scale_log2;
+    const uint32_t tO = tmem + kColO, tP = tmem + kColP;  // warp 0: lanes 0-31
+    float m_run = NINF, l_run = 0.f;
+    for (int t = 0; t < ntiles; ++t) {
+      mbar_wait(&bar_s[t & 1], (t >> 1) & 1, p.err, 8);
+      tc_fence_after();
+      uint32_t sv[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld32(tmem + (t & 1) * 128 + c * 32, sv + c * 32);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_sf[t & 1]);  // S_{t%2} may take S(t+2)
+      const int kv0 = j0 + t * kDtcTile;
+      if (kv0 + kDtcTile > j1) {
+#pragma unroll
+        for (int c = 0; c < 128; ++c)
+          if (kv0 + c >= j1) sv[c] = __float_as_uint(NINF);
+      }
+      float a0 = __uint_as_float(sv[0]), a1 = __uint_as_float(sv[1]);
+      float a2 = __uint_as_float(sv[2]), a3 = __uint_as_float(sv[3]);
+#pragma unroll
+      for (int c = 4; c + 8 <= 128; c += 8) {
+        a0 = fmax3(a0, __uint_as_float(sv[c]), __uint_as_float(sv[c + 1]));
+        a1 = fmax3(a1, __uint_as_float(sv[c + 2]), __uint_as_float(sv[c + 3]));
+        a2 = fmax3(a2, __uint_as_float(sv[c + 4]), __uint_as_float(sv[c + 5]));
+        a3 = fmax3(a3, __uint_as_float(sv[c + 6]), __uint_as_float(sv[c + 7]));
+      }
+      a0 = fmax3(a0, __uint_as_float(sv[124]), __uint_as_float(sv[125]));
+      a1 = fmax3(a1, __uint_as_float(sv[126]), __uint_as_float(sv[127]));
+      const float mx = fmaxf(fmax3(a0, a1, a2), a3);
+      const float m_new = fmaxf(m_run, mx * sc);
+      float alpha = 1.0f;
+      const bool rescale = __any_sync(0xffffffffu, m_new > m_run + kRescaleLog2);
+      if (rescale) {
+        alpha = (m_new == NINF) ? 1.0f : ex2(m_run - m_new);
+        l_run *= alpha;
+        m_run = m_new;
+      }
+      const float m_use = (m_run == NINF) ? 0.f : m_run;
+      uint32_t pk[64];
+      l_run += attn_exp_pass<false, false>(sv, sc, m_use, tP, pk);  // exps into registers
+      if (t > 0) {
+        // PV(t-1) read P(t-1) and wrote O: now P(t) may overwrite it and O be rescaled
+        mbar_wait(bar_pv, (t - 1) & 1, p.err, 10);
+        tc_fence_after();
+        if (rescale) attn_rescale_o<D>(tO, alpha);
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_st16(tP + c * 16, pk + c * 16);
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_p);
+    }
+    // ---- epilogue: rows < R -> partial (O unnormalised, m, l) in the workspace
+    float* w = p.ws + ((long long)grp * p.splits + s) * R * (D + 2);
+    if (ntiles > 0) {
+      mbar_wait(bar_pv, (ntiles - 1) & 1, p.err, 9);  // the last PV
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t o[32];
+        tmem_ld32(tO + c * 32, o);
+        tmem_wait_ld();
+        if (lane < R) {  // partial rows are D + 2 floats: 8-byte aligned
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            *reinterpret_cast<float2*>(w + lane * (D + 2) + c * 32 + 2 * q) =
+                make_float2(__uint_as_float(o[2 * q]), __uint_as_float(o[2 * q + 1]));
+        }
+      }
+    } else if (lane < R) {
+      for (int c = 0; c < D; ++c) w[lane * (D + 2) + c] = 0.f;  // empty split: weight 0, finite O
+    }
+    if (lane < R) {
+      w[lane * (D + 2) + D] = m_run;
+      w[lane * (D + 2) + D + 1] = l_run;
+    }
+  }
+
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+}  // namespace nt

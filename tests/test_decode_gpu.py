@@ -104,8 +104,9 @@ def test_paged_decode_vs_fp64(page_size, layout):
         _check(got[b:b + 1], ref)
 
 
-def test_paged_decode_matches_dense_kernel_bitwise_when_splits_match():
-    """Same splits, same keys: the paged gather changes only where tiles come from."""
+def test_paged_decode_matches_dense_kernel_when_splits_match():
+    """Same splits, same keys: paged K2 (FMA-pipe dots, fp32 P) and dense K2b (tcgen05,
+    P rounded to bf16) agree to the P rounding, and both match fp64."""
     from paper_2604_14825_b200.runtime import DecodePlan, PagedDecodePlan
 
     B, Hq, Hkv, Nq, M, D = 2, 8, 2, 1, 4096, 128
@@ -122,7 +123,10 @@ def test_paged_decode_matches_dense_kernel_bitwise_when_splits_match():
                     torch.from_numpy(bt).cuda(), torch.full((B,), M, dtype=torch.int32, device="cuda"), o2,
                     0.088, max_seq_kv=M, num_splits=6).launch()
     torch.cuda.synchronize()
-    assert torch.equal(o1, o2)
+    assert float((o1 - o2).abs().max()) < 5e-3
+    ref = reference_math.attention_batched_fp64(q.float().cpu().numpy(), k, v, 0.088, False)
+    _check(o1.cpu().numpy(), ref)
+    _check(o2.cpu().numpy(), ref)
 
 
 @pytest.mark.parametrize("Hq,Hkv,Nq,page_size", [(8, 8, 1, 32), (16, 2, 1, 16), (4, 4, 2, 128), (8, 4, 1, 8)])
