@@ -587,8 +587,8 @@ def run_ours(args, cfg, rank, world, dist):
                 # tools/ubench/bulk_read.cu on this pool's B200 (r02: 7398 GB/s, 192 KB in flight per SM)
                 "read_ceiling_gbs": READ_CEILING_GBS, "frac_of_read_ceiling": achieved / READ_CEILING_GBS,
                 "algorithmic_bytes_per_launch": w["local_bytes"],
-                "kernel": ("decode_split_kernel<paged> (FMA-pipe dots) + combine" if cfg.get("page_size")
-                           else "decode_tc_kernel (tcgen05 dots) + combine")}
+                "kernel": ("decode_tc_kernel<paged> (tcgen05 dots, page-slice TMA gathers) + combine"
+                           if cfg.get("page_size") else "decode_tc_kernel (tcgen05 dots) + combine")}
     else:
         achieved = w["local_flops"] / (ms_kernel_local * 1e-3) / 1e12
         peak = peaks["bf16_tflops"] * (2.0 if w.get("e4m3") else 1.0)

@@ -74,10 +74,10 @@ bool use_tc_decode() {
   return !fma;
 }
 
-template <int R>
+template <int R, int PG>
 int launch_tc(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, DecodeParams& p, cudaStream_t st) {
   int rc;
-  constexpr auto kern = decode_tc_kernel<R>;
+  constexpr auto kern = decode_tc_kernel<R, PG>;
   if ((rc = configure_smem<kern>(kDtcSmem, "cudaFuncSetAttribute(decode_tc)"))) return rc;
   dim3 grid(p.splits, p.B * p.Hkv);
   kern<<<grid, kDtcThreads, kDtcSmem, st>>>(mq, mk, mv, p);
@@ -89,14 +89,22 @@ int launch_tc(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& m
   return check_cuda(cudaGetLastError(), "decode_combine launch");
 }
 
+template <int PG>
 int dispatch_tc(int R, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, DecodeParams& p,
                 cudaStream_t st) {
   switch (R) {
-    case 1: return launch_tc<1>(mq, mk, mv, p, st);
-    case 2: return launch_tc<2>(mq, mk, mv, p, st);
-    case 4: return launch_tc<4>(mq, mk, mv, p, st);
-    default: return launch_tc<8>(mq, mk, mv, p, st);
+    case 1: return launch_tc<1, PG>(mq, mk, mv, p, st);
+    case 2: return launch_tc<2, PG>(mq, mk, mv, p, st);
+    case 4: return launch_tc<4, PG>(mq, mk, mv, p, st);
+    default: return launch_tc<8, PG>(mq, mk, mv, p, st);
   }
+}
+
+int make_q_map(CUtensorMap* mq, const nt_tensor4& q, int B, int Hq, int Nq, int g) {
+  const int64_t qd[4] = {kDecodeD, Nq, Hq, B};
+  const int64_t qs[3] = {q.stride_s, q.stride_h, q.stride_b};
+  const int qb[4] = {64, Nq, g, 1};
+  return make_map_4d_box(mq, q.ptr, qd, qs, qb, 2);
 }
 }  // namespace
 
@@ -145,17 +153,14 @@ extern "C" int nt_attn_decode(const nt_decode_args* a, void* stream) {
     // K2b: 128-key tiles; the group's R query rows as one 4-D box {64, Nq, g, 1}
     p.keys_per_split = ((a->seq_kv + p.splits - 1) / p.splits + kDtcTile - 1) / kDtcTile * kDtcTile;
     CUtensorMap mq;
-    const int64_t qd[4] = {a->head_dim, a->seq_q, a->heads_q, a->batch};
-    const int64_t qs[3] = {a->q.stride_s, a->q.stride_h, a->q.stride_b};
-    const int qb[4] = {64, a->seq_q, g, 1};
-    if ((rc = make_map_4d_box(&mq, a->q.ptr, qd, qs, qb, 2))) return rc;
+    if ((rc = make_q_map(&mq, a->q, a->batch, a->heads_q, a->seq_q, g))) return rc;
     if ((rc = make_map_pages_5d(&mk, a->k.ptr, a->seq_kv, a->heads_kv, a->batch, a->k.stride_s, a->k.stride_h,
                                 a->k.stride_b, kDtcTile)))
       return rc;
     if ((rc = make_map_pages_5d(&mv, a->v.ptr, a->seq_kv, a->heads_kv, a->batch, a->v.stride_s, a->v.stride_h,
                                 a->v.stride_b, kDtcTile)))
       return rc;
-    return dispatch_tc(R, mq, mk, mv, p, st);
+    return dispatch_tc<0>(R, mq, mk, mv, p, st);
   }
   // one 5-D box {64 dims, 64 keys, 2 panels} per K or V tile (a batch entry is a "page"
   // of seq_kv tokens): both 64-dim panels in one TMA, laid out [panel][64 keys][128 B]
@@ -204,6 +209,29 @@ extern "C" int nt_attn_decode_paged(const nt_decode_paged_args* a, void* stream)
   p.seq_lens = a->seq_lens;
   CUtensorMap mk, mv;
   int rc;
+  if (use_tc_decode() && (kDtcTile % ps == 0 || ps % kDtcTile == 0)) {
+    // K2b over the page pool: 128-key tiles gathered page slice by page slice
+    p.keys_per_split = ((a->max_seq_kv + p.splits - 1) / p.splits + kDtcTile - 1) / kDtcTile * kDtcTile;
+    CUtensorMap mq;
+    if ((rc = make_q_map(&mq, a->q, a->batch, a->heads_q, a->seq_q, g))) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (ps % kDtcTile == 0) {
+      if ((rc = make_map_pages_5d(&mk, a->k_pages, ps, a->heads_kv, a->num_pages, a->token_stride, a->head_stride,
+                                  a->page_stride, kDtcTile)))
+        return rc;
+      if ((rc = make_map_pages_5d(&mv, a->v_pages, ps, a->heads_kv, a->num_pages, a->token_stride, a->head_stride,
+                                  a->page_stride, kDtcTile)))
+        return rc;
+      return dispatch_tc<1>(R, mq, mk, mv, p, st);
+    }
+    if ((rc = make_map_4d(&mk, a->k_pages, kDecodeD, ps, a->heads_kv, a->num_pages, a->token_stride, a->head_stride,
+                          a->page_stride, ps, 2)))
+      return rc;
+    if ((rc = make_map_4d(&mv, a->v_pages, kDecodeD, ps, a->heads_kv, a->num_pages, a->token_stride, a->head_stride,
+                          a->page_stride, ps, 2)))
+      return rc;
+    return dispatch_tc<2>(R, mq, mk, mv, p, st);
+  }
   const int rows = std::min(ps, kDecodeTile);
   if (rows < kDecodeTile) {  // small pages: one 5-D box per page slice (both 64-dim panels)
     if ((rc = make_map_pages_5d(&mk, a->k_pages, ps, a->heads_kv, a->num_pages, a->token_stride, a->head_stride,

@@ -33,7 +33,12 @@ constexpr int kDtcStages = 3;                            // K+V tile pairs in fl
 constexpr int kDtcThreads = 128;
 constexpr int kDtcSmem = kDtcTileBytes /* Q */ + kDtcStages * 2 * kDtcTileBytes + 1024 /* align */ + 256;
 
-template <int R>
+// PG: 0 dense K/V ([B, Hkv, M, D] viewed as 5-D pages of M tokens); 1 paged cache with
+// page_size a multiple of 128 (one 5-D box {64, 128 tokens, 2 panels} per tile);
+// 2 paged with 8/16/32/64-token pages (per page slice and 64-dim panel one 4-D box
+// {64, page_size} straight into the canonical [panel][128 keys][128 B] tile -- one
+// lane per box, the page ids of the next tile fetched while this one is issued)
+template <int R, int PG = 0>
 __global__ void __launch_bounds__(kDtcThreads, 1)
     decode_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                      const __grid_constant__ CUtensorMap tmV, const DecodeParams p) {
@@ -59,7 +64,8 @@ __global__ void __launch_bounds__(kDtcThreads, 1)
   const int warp = __shfl_sync(0xffffffffu, threadIdx.x / 32, 0);
   const int lane = threadIdx.x & 31;
   const int j0 = s * p.keys_per_split;  // multiple of kDtcTile
-  const int j1 = min(p.M, j0 + p.keys_per_split);
+  const int seq_len = PG ? min(p.M, p.seq_lens[b]) : p.M;
+  const int j1 = min(seq_len, j0 + p.keys_per_split);
   const int ntiles = (j1 > j0) ? (j1 - j0 + kDtcTile - 1) / kDtcTile : 0;
 
   // rows >= R of the padded Q tile are zero (S, P, O rows >= R are never read)
@@ -92,18 +98,56 @@ __global__ void __launch_bounds__(kDtcThreads, 1)
 
   if (warp == 1) {
     // ================= TMA producer
-    if (lane == 0 && ntiles > 0) {
-      mbar_arrive_expect_tx(bar_q, R * D * 2);
-      // the group's R rows: box {64 dims, Nq rows, g heads, 1} per 64-dim panel
+    if (ntiles > 0) {
+      if (lane == 0) {
+        mbar_arrive_expect_tx(bar_q, R * D * 2);
+        // the group's R rows: box {64 dims, Nq rows, g heads, 1} per 64-dim panel
 #pragma unroll
-      for (int h = 0; h < 2; ++h) tma_load_4d(sQ + h * kDtcHalf, &tmQ, bar_q, h * 64, 0, hkv * p.g, b);
-      for (int it = 0; it < 2 * ntiles; ++it) {
-        const int slot = it % (2 * kDtcStages);
-        mbar_wait(&empty[slot], ((it / (2 * kDtcStages)) & 1) ^ 1, p.err, 1);
-        mbar_arrive_expect_tx(&full[slot], kDtcTileBytes);
-        // one 5-D box {64 dims, 128 keys, 2 panels} = [panel][128 keys][128 B]
-        tma_load_5d(sKV + slot * kDtcTileBytes, (it & 1) ? &tmV : &tmK, &full[slot], 0, j0 + (it >> 1) * kDtcTile,
-                    0, hkv, b);
+        for (int h = 0; h < 2; ++h) tma_load_4d(sQ + h * kDtcHalf, &tmQ, bar_q, h * 64, 0, hkv * p.g, b);
+      }
+      if constexpr (PG == 0) {
+        if (lane == 0)
+          for (int it = 0; it < 2 * ntiles; ++it) {
+            const int slot = it % (2 * kDtcStages);
+            mbar_wait(&empty[slot], ((it / (2 * kDtcStages)) & 1) ^ 1, p.err, 1);
+            mbar_arrive_expect_tx(&full[slot], kDtcTileBytes);
+            // one 5-D box {64 dims, 128 keys, 2 panels} = [panel][128 keys][128 B]
+            tma_load_5d(sKV + slot * kDtcTileBytes, (it & 1) ? &tmV : &tmK, &full[slot], 0,
+                        j0 + (it >> 1) * kDtcTile, 0, hkv, b);
+          }
+      } else {
+        const int ps = p.page_size;
+        const int* bt = p.block_table + (long long)b * p.bt_stride;
+        const int last_page = (seq_len - 1) / ps;
+        // PG 2: lane = (page slice, panel); PG 1: lane 0 only
+        const int nsub = (PG == 2) ? kDtcTile / ps : 1;
+        const int sub = lane >> 1, panel = lane & 1;
+        const bool active = (PG == 2) ? (lane < 2 * nsub) : (lane == 0);
+        auto page_of = [&](int t) -> int2 {  // (physical page, token within it) of this lane's slice
+          const int tok = j0 + t * kDtcTile + ((PG == 2) ? sub * ps : 0);
+          const int pg = tok / ps;
+          const int lp = min(pg, last_page);  // past the sequence end: its last page (masked)
+          return make_int2(__ldg(bt + lp), tok - pg * ps);
+        };
+        int2 cur = active ? page_of(0) : make_int2(0, 0);
+        for (int t = 0; t < ntiles; ++t) {
+          const int2 nxt = (active && t + 1 < ntiles) ? page_of(t + 1) : make_int2(0, 0);
+          for (int kv = 0; kv < 2; ++kv) {
+            const int it = 2 * t + kv, slot = it % (2 * kDtcStages);
+            if (lane == 0) {
+              mbar_wait(&empty[slot], ((it / (2 * kDtcStages)) & 1) ^ 1, p.err, 1);
+              mbar_arrive_expect_tx(&full[slot], kDtcTileBytes);
+            }
+            __syncwarp();
+            if (active) {
+              uint8_t* dst = sKV + slot * kDtcTileBytes;
+              const CUtensorMap* m = kv ? &tmV : &tmK;
+              if constexpr (PG == 1) tma_load_5d(dst, m, &full[slot], 0, cur.y, 0, hkv, cur.x);
+              else tma_load_4d(dst + panel * kDtcHalf + sub * ps * 128, m, &full[slot], panel * 64, cur.y, hkv, cur.x);
+            }
+          }
+          cur = nxt;
+        }
       }
     }
   } else if (warp == 2) {
