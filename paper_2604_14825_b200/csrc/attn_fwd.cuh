@@ -168,7 +168,7 @@ struct AttnCfg {
   // NQ = 1 (two CTAs per SM, tight shared memory), 16 columns (64-byte rows,
   // SWIZZLE_64B); bf16 boxes are 32 columns of 64-byte rows
   static constexpr int F32_BOX_COLS = NQ == 1 ? 16 : 32;
-  static constexpr int OBOX = ((OUT_F32 || SPLIT) && NQ == 2) ? 32 * 32 * 4 : 32 * 32 * 2;
+  static constexpr int OBOX = (OUT_F32 && NQ == 2) ? 32 * 32 * 4 : 32 * 32 * 2;  // split partials are bf16
   static constexpr int SMEM_O = SMEM_KV + STAGES * TKV;
   static constexpr int SMEM_BAR = SMEM_O + 4 * NQ * OBOX;
   static constexpr int NBAR = 4 * QB + 2 * STAGES + 2 + 2 + 2 + 2 + 2 + 2 * kItemRing;
@@ -678,7 +678,7 @@ __global__ void __launch_bounds__(attn_threads<NQ>(), NQ == 2 ? 1 : 2)
     bool pend = false;
     int pend_li = 0, pend_row0 = 0, pend_hq = 0, pend_b = 0;
     float pend_inv = 0.f;
-    bool pend_part = false;  // split-KV unit: O goes unnormalised to the fp32 partial map (row pend_row0)
+    bool pend_part = false;  // split-KV unit: O / l_unit goes to the bf16 partial map (row pend_row0)
     auto store_o = [&]() {
       // O / l from TMEM -> swizzled smem box (one row per lane) -> TMA store of
       // 32 rows x 32 columns per warp (rows past N are clipped)
@@ -692,7 +692,7 @@ __global__ void __launch_bounds__(attn_threads<NQ>(), NQ == 2 ? 1 : 2)
         uint32_t o[32];
         tmem_ld32(tO + c * 32, o);
         tmem_wait_ld();
-        const bool f32box = OUT_F32 || (SPLIT && pend_part);
+        const bool f32box = OUT_F32 && !(SPLIT && pend_part);
         if (C::F32_BOX_COLS == 16 && f32box) {
           // two 16-column fp32 boxes: 64-byte rows, chunk q at q ^ ((row >> 1) & 3) (SWIZZLE_64B)
 #pragma unroll
@@ -906,10 +906,11 @@ __global__ void __launch_bounds__(attn_threads<NQ>(), NQ == 2 ? 1 : 2)
       pend_li = li;
       pend_part = SPLIT && itm.split;
       if (SPLIT && itm.split) {
-        // partial of a split item: (m, l) per row now, O unnormalised (store_o);
-        // a KV range can legitimately miss a causal row (l = 0): the combine checks
+        // partial of a split item: (m, l) per row now, O / l as bf16 (store_o) -- half
+        // the bytes of an unnormalised fp32 partial (1-group 8K: 128 KB -> 64 KB per
+        // unit); a KV range can legitimately miss a causal row (l = 0): the combine checks
         p.part_ml[(long long)itm.unit * ROWS + t * 128 + r] = make_float2(m_run, l_run);
-        pend_inv = 1.0f;
+        pend_inv = (l_run > 0.f) ? 1.0f / l_run : 0.f;
         pend_row0 = itm.unit * ROWS + t * 128 + wq * 32;
       } else {
         if (valid && !(l_run > 0.f) && p.err) atomicOr(p.err, 1);
@@ -956,7 +957,8 @@ __global__ void __launch_bounds__(attn_threads<NQ>(), NQ == 2 ? 1 : 2)
 // before the FMAs.
 constexpr int kCombineRowsPerWarp = 4;
 template <int D, int MASK, bool OUT_F32, int ROWS = 256>
-__global__ void __launch_bounds__(256) attn_combine_kernel(const float* __restrict__ part_o, const AttnFwdParams p) {
+__global__ void __launch_bounds__(256) attn_combine_kernel(const __nv_bfloat16* __restrict__ part_o,
+                                                           const AttnFwdParams p) {
   const int mbi = blockIdx.z, bh = blockIdx.y;
   const int mb = (MASK == MASK_CAUSAL) ? (p.n_mblocks - 1 - mbi) : mbi;
   const int n_full = attn_mb_nkv<MASK, ROWS>(p, mb);
@@ -965,9 +967,19 @@ __global__ void __launch_bounds__(256) attn_combine_kernel(const float* __restri
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int BH = p.B * p.Hq;
   const int u0 = p.unit_prefix[mbi] + bh;
-  constexpr int CPL = D / 32;  // columns per lane
+  constexpr int CPL = D / 32;  // columns per lane (4 bf16 = 8 bytes at D=128)
   const long long cstride = (long long)BH * ROWS * D;
   const int b = bh / p.Hq, hq = bh % p.Hq;
+  auto load = [&](const __nv_bfloat16* src, float (&v)[CPL]) {
+    if constexpr (CPL == 4) {
+      const uint2 x = __ldg(reinterpret_cast<const uint2*>(src));
+      v[0] = __uint_as_float(x.x << 16); v[1] = __uint_as_float(x.x & 0xffff0000u);
+      v[2] = __uint_as_float(x.y << 16); v[3] = __uint_as_float(x.y & 0xffff0000u);
+    } else {
+      const uint32_t x = __ldg(reinterpret_cast<const uint32_t*>(src));
+      v[0] = __uint_as_float(x << 16); v[1] = __uint_as_float(x & 0xffff0000u);
+    }
+  };
 #pragma unroll 1
   for (int rr = 0; rr < kCombineRowsPerWarp; ++rr) {
     const int row = blockIdx.x * (8 * kCombineRowsPerWarp) + warp * kCombineRowsPerWarp + rr;  // within the m-block
@@ -980,24 +992,17 @@ __global__ void __launch_bounds__(256) attn_combine_kernel(const float* __restri
       mc = ml.x;
       lc = ml.y;
     }
-    const float* base = part_o + ((long long)u0 * ROWS + row) * D + lane * CPL;
-    // the first chunks' O rows are loaded while the (m, l) reduction runs
-    float v0[4][CPL];
+    const __nv_bfloat16* base = part_o + ((long long)u0 * ROWS + row) * D + lane * CPL;
+    float v0[4][CPL];  // the first chunks' rows load while the (m, l) reduction runs
 #pragma unroll
     for (int k = 0; k < 4; ++k)
-      if (k < nc) {
-#pragma unroll
-        for (int i = 0; i < CPL; i += 2) {
-          const float2 x = __ldg(reinterpret_cast<const float2*>(base + k * cstride + i));
-          v0[k][i] = x.x;
-          v0[k][i + 1] = x.y;
-        }
-      }
+      if (k < nc) load(base + k * cstride, v0[k]);
     float m = mc;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-    const float wgt = (lane < nc && mc != f_ninf()) ? ex2(mc - m) : 0.f;
-    float lsum = wgt * lc;
+    // chunk weight w_c l_c: the partials are O_c / l_c
+    const float wgt = (lane < nc && mc != f_ninf()) ? ex2(mc - m) * lc : 0.f;
+    float lsum = wgt;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, off);
     float acc[CPL];
@@ -1015,14 +1020,7 @@ __global__ void __launch_bounds__(256) attn_combine_kernel(const float* __restri
       float v[4][CPL];
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        if (c0 + k < nc) {
-#pragma unroll
-          for (int i = 0; i < CPL; i += 2) {
-            const float2 x = __ldg(reinterpret_cast<const float2*>(base + (c0 + k) * cstride + i));
-            v[k][i] = x.x;
-            v[k][i + 1] = x.y;
-          }
-        }
+        if (c0 + k < nc) load(base + (c0 + k) * cstride, v[k]);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const float w = __shfl_sync(0xffffffffu, wgt, (c0 + k) & 31);

@@ -12,8 +12,8 @@ namespace nt {
 
 struct AttnMaps {
   CUtensorMap q, k, v, o;
-  CUtensorMap p;   // split KV: fp32 partial O [units * rows, D]
-  float* part_o;   // its base
+  CUtensorMap p;   // split KV: bf16 partial O / l [units * rows, D]
+  const __nv_bfloat16* part_o;  // its base
 };
 
 // nt_attn_prepare: everything but the launch (set per call in capi.cu); the

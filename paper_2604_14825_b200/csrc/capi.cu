@@ -212,7 +212,7 @@ static AttnSplit attn_split_plan(const nt_attn_args* a) {
   const int64_t prefix_bytes = ((int64_t)(nmb + 1) * 4 + 255) / 256 * 256;
   sp.off_ml = prefix_bytes;
   sp.off_o = sp.off_ml + ((int64_t)units * rows * 8 + 255) / 256 * 256;
-  sp.bytes = sp.off_o + (int64_t)units * rows * a->head_dim * 4;
+  sp.bytes = sp.off_o + (int64_t)units * rows * a->head_dim * 2;  // bf16 partials
   return sp;
 }
 
@@ -324,9 +324,8 @@ static int attn_build(const nt_attn_args* a, AttnMaps& m, AttnFwdParams& p, int&
     p.n_split_mb = sp.n_split_mb;
     p.unit_prefix = reinterpret_cast<int*>(ws);
     p.part_ml = reinterpret_cast<float2*>(ws + sp.off_ml);
-    m.part_o = reinterpret_cast<float*>(ws + sp.off_o);
-    if ((rc = make_map_2d(&m.p, m.part_o, D, (int64_t)sp.n_units * rows, D, f32_cols, 32, 4,
-                          f32_cols == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B)))
+    m.part_o = reinterpret_cast<const __nv_bfloat16*>(ws + sp.off_o);
+    if ((rc = make_map_2d(&m.p, m.part_o, D, (int64_t)sp.n_units * rows, D, 32, 32, 2, CU_TENSOR_MAP_SWIZZLE_64B)))
       return rc;
   } else {
     m.p = m.o;  // unused (no split)

@@ -356,7 +356,8 @@ def test_full_size_decode_properties():
     plan.launch()
     torch.cuda.synchronize()
     plan.check_errors()
-    assert float((o - 1).abs().max()) < 1e-5  # fp32 P on the FMA pipe: O = sum(P)/sum(P)
+    # K2b: O = sum(bf16(P)) / sum(P) -- only P's round-to-nearest bf16 rounding, averaged
+    assert float((o - 1).abs().max()) < 2e-3
 
 
 # ---------------------------------------------------------------- e4m3 (FP8) K1

@@ -54,7 +54,7 @@ def _plan(B, Hq, N, M, D, causal):
     units = sum((n + S - 1) // S for n in nk) * BH
     prefix = ((nmb + 1) * 4 + 255) // 256 * 256
     ml = (units * rows * 8 + 255) // 256 * 256
-    return S, units, prefix + ml + units * rows * D * 4
+    return S, units, prefix + ml + units * rows * D * 2  # bf16 partials
 
 
 def _units(B, Hq, N, M, causal, S):
