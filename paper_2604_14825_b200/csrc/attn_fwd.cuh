@@ -682,6 +682,7 @@ __global__ void __launch_bounds__(attn_threads<NQ>(), NQ == 2 ? 1 : 2)
     auto store_o = [&]() {
       // O / l from TMEM -> swizzled smem box (one row per lane) -> TMA store of
       // 32 rows x 32 columns per warp (rows past N are clipped)
+      if (t == 0 && wq == 0 && lane == 0 && pend_li < 16) NT_STAMP(3, 32 + pend_li, 2);  // store_o entry (trace)
       mbar_wait(&bar_o_full[t], pend_li & 1, p.err, 9);
       if (t == 0 && wq == 0 && lane == 0 && pend_li < 15) NT_STAMP(3, 48 + pend_li, 6);  // trace: O complete
       tc_fence_after();
@@ -894,6 +895,7 @@ __global__ void __launch_bounds__(attn_threads<NQ>(), NQ == 2 ? 1 : 2)
         if (lane == 0) mbar_arrive(&bar_p_full[t]);
       }
 
+      if (t == 0 && wq == 0 && lane == 0 && li < 16) NT_STAMP(3, 32 + li, 0);  // last tile done (trace)
       pv_base += itm.n_kv;
       if (kPack == 2) l_run *= 1.0f / kTruncScale;  // P was pre-biased by kTruncScale before truncation
 
@@ -919,6 +921,7 @@ __global__ void __launch_bounds__(attn_threads<NQ>(), NQ == 2 ? 1 : 2)
       }
       pend_hq = itm.hq;
       pend_b = itm.b;
+      if (t == 0 && wq == 0 && lane == 0 && li < 16) NT_STAMP(3, 32 + li, 1);  // epilogue prepared (trace)
       if (!C::SEP_P) {
         store_o();
         pend = false;

@@ -58,6 +58,13 @@ for role, name in enumerate(["mma", "softmax0", "softmax1", "producer"]):
 os.makedirs(os.path.dirname(a.out), exist_ok=True)
 json.dump(res, open(a.out, "w"))
 print("kernel entry", int(t[3, 63, 7] - base) if t[3, 63, 7] > 0 else None)
+# per item (role 3 rows 32+li / 48+li): last tile done, epilogue prepared, store_o entry,
+# O complete, item start, item end; producer reach/publish, MMA has Q, softmax ask/get
+for li in range(8):
+    r32, r48 = t[3, 32 + li], t[3, 48 + li]
+    f = lambda x: int(x - base) if x > 0 else None
+    print(f"item {li}: start {f(r32[6])} last-tile {f(r32[0])} prepared {f(r32[1])} store_o {f(r32[2])} "
+          f"O-complete {f(r48[6])} end {f(r32[7])} | ask {f(r48[4])} got {f(r48[5])} mma-Q {f(r48[3])}")
 print("items (start, end) of tile 0:", [(int(t[3, 32 + i, 6] - base), int(t[3, 32 + i, 7] - base))
                                        for i in range(16) if t[3, 32 + i, 6] > 0])
 print("per item [producer reaches, published, -, Q landed, softmax asks, softmax gets, O complete]:")
