@@ -121,6 +121,9 @@ def _context(args):
     binding = _parse_bind(args.bind)
     device, opts = resolve_device(args.device)  # None | "b200" | profile path
     bound, base = frontend(text, binding)
+    if args.upstream_fixes:
+        from . import upstream
+        upstream.apply()  # for the whole command: tune / check re-schedule probes too
     seeds = run_autoscheduler(base, device, replace(opts, max_seeds=args.max_seeds))
     if not seeds:
         raise SystemExit("error: auto-scheduler produced no viable seeds")
@@ -225,6 +228,8 @@ def build_argparser() -> argparse.ArgumentParser:
         p.add_argument("--seed", type=int, default=0, help="rng seed")
         p.add_argument("--max-seeds", type=int, default=16)
         p.add_argument("--backend", default="simt", choices=["auto", "simt", "tcgen05"])
+        p.add_argument("--upstream-fixes", action="store_true",
+                       help="schedule with the transitive consumer-reduced-axes fix (upstream.py)")
 
     p = sub.add_parser("check", help="differential gate against the oracle (device execution)")
     common(p)

@@ -85,12 +85,13 @@ def device_profile(**overrides):
 
 
 def compile_program(program: str, binding: dict, device=None, seed_index: int = 0,
-                    assignment: Optional[dict] = None, options=None):
+                    assignment: Optional[dict] = None, options=None, upstream_fixes: bool = False):
     """Run the reference pipeline; return (mirrored MA module, tilecc LoweredSeed, seeds).
 
     ``program`` is ``.te`` text or a key of ``programs.PROGRAMS``; ``device`` is
     None (reference default), ``"b200"`` (``b200.device`` + sm100a-only options),
-    a profile path or a VirtualDevice.
+    a profile path or a VirtualDevice; ``upstream_fixes`` schedules with
+    ``upstream.apply()`` (scale / mask after the sum).
     """
     import_tilecc()
     from tilecc.autosched.scheduler import SchedulerOptions, run_autoscheduler
@@ -99,7 +100,12 @@ def compile_program(program: str, binding: dict, device=None, seed_index: int = 
     text = PROGRAMS.get(program, program)
     device, default_opts = resolve_device(device)
     bound, base = frontend(text, binding)
-    seeds = run_autoscheduler(base, device, options or default_opts)
+    if upstream_fixes:
+        from . import upstream
+        with upstream.fixed():
+            seeds = run_autoscheduler(base, device, options or default_opts)
+    else:
+        seeds = run_autoscheduler(base, device, options or default_opts)
     if not seeds:
         from .errors import UnsupportedMA
         raise UnsupportedMA("the auto-scheduler found no viable seeds")

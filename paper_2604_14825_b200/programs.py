@@ -68,10 +68,45 @@ output Y
 
 LLAMA_SCALE = 0.08838834764831845  # 1/sqrt(128), exactly as SURVEY.md A.3 writes it
 
+# Natural spellings the reference scheduler cannot fuse without upstream.apply()
+# (scale / mask applied after the sum): the reference's own
+# CAUSAL_SRC (tests/conftest.py:28-39) and the post-sum scale.
+CAUSAL_NATURAL = """\
+tensor Q[fp32](N, D)
+tensor K[fp32](M, D)
+tensor V[fp32](M, D)
+tensor Mask[fp32](N, M)
+S(i, j) = sum(k, Q(i, k) * K(j, k)) + Mask(i, j)
+m(i) = max(j, S(i, j))
+P(i, j) = exp(S(i, j) - m(i))
+l(i) = sum(j, P(i, j))
+O(i, d) = sum(j, P(i, j) * V(j, d)) / l(i)
+output O
+"""
+
+
+def scaled_post(c: float, masked: bool = False) -> str:
+    mask_decl = "tensor Mask[fp32](N, M)\n" if masked else ""
+    mask_add = " + Mask(i, j)" if masked else ""
+    return f"""\
+tensor Q[fp32](N, D)
+tensor K[fp32](M, D)
+tensor V[fp32](M, D)
+{mask_decl}S(i, j) = sum(k, Q(i, k) * K(j, k)) * {c!r}{mask_add}
+m(i) = max(j, S(i, j))
+P(i, j) = exp(S(i, j) - m(i))
+l(i) = sum(j, P(i, j))
+O(i, d) = sum(j, P(i, j) * V(j, d)) / l(i)
+output O
+"""
+
 PROGRAMS = {
     "attention": ATTENTION,
     "scaled_0p125": scaled_attention(0.125),
     "llama": scaled_attention(LLAMA_SCALE),
     "llama_causal": masked_attention(LLAMA_SCALE),
     "gemm2": GEMM2,
+    "causal_natural": CAUSAL_NATURAL,
+    "scaled_post_0p125": scaled_post(0.125),
+    "llama_causal_natural": scaled_post(LLAMA_SCALE, masked=True),
 }

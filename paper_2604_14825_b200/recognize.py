@@ -344,10 +344,19 @@ def recognize_attention(module: ir.Module, kernel: ir.Kernel, sym: _Sym, pre, lo
     s = s_masked
     if s[0] == "bin" and s[1] == "add" and _is_tile(s[3]):
         s, mask_tile = s[2], s[3]
+    # S = dot(...) * c: the post-sum scale spelling (schedulable with upstream.apply())
+    post_scale = None
+    if s[0] == "bin" and s[1] == "mul":
+        if s[2][0] == "dot" and s[3][0] == "lit":
+            s, post_scale = s[2], s[3][1]
+        elif s[3][0] == "dot" and s[2][0] == "lit":
+            s, post_scale = s[3], s[2][1]
     if s[0] != "dot" or s[3] is not None or s[2][0] != "T":
         raise UnsupportedMA("S is not dot(Q, K^T)")
     q_tile = s[1]
     k_tile, scale = _strip_scale(s[2][1])
+    if post_scale is not None:
+        scale = post_scale if scale is None else scale * post_scale
     if not _is_tile(q_tile):
         raise UnsupportedMA("Q operand is not an input tile")
     alpha = ("un", "exp2", ("scale", ("bin", "sub", ("carry", m_acc), m_new)))

@@ -114,6 +114,14 @@ CASES = [
          io=False, profile="b200"),
     dict(name="b200_causal8k", prog="llama_causal", bind=dict(N=8192, M=8192, D=128), seeds=[0], io=False,
          profile="b200"),
+    # natural spellings (mask / scale after the sum) scheduled with the upstream fix
+    # (paper_2604_14825_b200/upstream.py; the unfixed scheduler raises IterationMismatch)
+    dict(name="fix_causal_natural256", prog="causal_natural", bind=dict(N=256, M=256, D=64), seeds=[0], io=True,
+         mask="causal", fixes=True),
+    dict(name="fix_scaled_post512", prog="scaled_post_0p125", bind=dict(N=512, M=512, D=64), seeds=[0], io=True,
+         fixes=True),
+    dict(name="fix_llama_causal_natural512", prog="llama_causal_natural", bind=dict(N=512, M=512, D=128), seeds=[0],
+         io=True, mask="causal", fixes=True),
 ]
 
 
@@ -134,13 +142,22 @@ def main():
         if case.get("device"):
             device = replace(device, **case["device"])
         bound, base = frontend(src, case["bind"])
-        seeds = run_autoscheduler(base, device, opts)
+        if case.get("fixes"):
+            from paper_2604_14825_b200 import upstream
+            upstream.apply()
+        try:
+            seeds = run_autoscheduler(base, device, opts)
+        finally:
+            if case.get("fixes"):
+                upstream.restore()
         which = range(len(seeds)) if case["seeds"] == "all" else case["seeds"]
         entry = {"program": case["prog"], "binding": case["bind"], "n_seeds": len(seeds),
                  "seeds": list(which), "assignment": case.get("assign"),
                  "device": case.get("device"), "io": case["io"], "mask": case.get("mask")}
         if case.get("profile"):
             entry["profile"] = case["profile"]
+        if case.get("fixes"):
+            entry["upstream_fixes"] = True
         for k in which:
             sd = seeds[k]
             assignment = None
