@@ -83,6 +83,7 @@ CASES = [
     dict(name="decode4", prog="llama", bind=dict(N=4, M=2048, D=128), seeds=[0], io=True),
     dict(name="decode1", prog="llama", bind=dict(N=1, M=1024, D=128), seeds=[0], io=True),
     dict(name="decode4_32k", prog="llama", bind=dict(N=4, M=32768, D=128), seeds=[0], io=False),
+    dict(name="decode4_128k", prog="llama", bind=dict(N=4, M=131072, D=128), seeds=[0], io=False),
     dict(name="gemm_v6", prog="gemm2", bind=dict(N=256, K=256, F=512, E=128), seeds=[0], io=True,
          scales={"W1": 1 / 16.0, "W2": 1 / math.sqrt(512)}),
     dict(name="gemm_v5", prog="gemm2", bind=dict(N=128, K=1024, F=256, E=128), seeds=[0], io=True,
