@@ -112,7 +112,9 @@ int nt_attn_resident_ctas(const nt_attn_args* args);
  * (validation, the five tensor maps, split plan, instantiation choice, kernel
  * load) done once; nt_attn_plan_launch is then one kernel launch (plus the
  * split-KV merge).  The plan keeps the pointers of `args`; the caller keeps the
- * buffers alive.  Not tied to a stream; launches on one stream are ordered. */
+ * buffers alive.  Not tied to a stream (launches on one stream are ordered), but to
+ * the device current at creation: launching with another device current is
+ * NT_ERR_INVALID. */
 typedef struct nt_attn_plan nt_attn_plan;
 int nt_attn_plan_create(const nt_attn_args* args, nt_attn_plan** plan);
 int nt_attn_plan_launch(const nt_attn_plan* plan, void* stream);

@@ -380,6 +380,10 @@ extern "C" int nt_attn_plan_create(const nt_attn_args* a, nt_attn_plan** out) {
 
 extern "C" int nt_attn_plan_launch(const nt_attn_plan* pl, void* stream) {
   if (!pl) return set_error(NT_ERR_INVALID, "null plan");
+  int dev = -1;
+  if (cudaGetDevice(&dev) == cudaSuccess && dev != pl->device)
+    return set_error(NT_ERR_INVALID, "attention plan created on device " + std::to_string(pl->device) +
+                                         ", launched with device " + std::to_string(dev) + " current");
   return pl->fn(pl->maps, pl->params, static_cast<cudaStream_t>(stream));
 }
 

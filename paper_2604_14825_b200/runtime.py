@@ -131,7 +131,10 @@ class AttentionPlan:
     def __del__(self):
         plan = getattr(self, "_plan", None)
         if plan is not None and plan.value:
-            self._destroy(plan)
+            try:
+                self._destroy(plan)
+            except Exception:  # interpreter shutdown: the library may already be gone
+                pass
             self._plan = None
 
     def flops(self) -> float:
