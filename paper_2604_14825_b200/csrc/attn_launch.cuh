@@ -8,6 +8,10 @@
 #include "attn_fwd.cuh"
 #include "common_host.h"
 
+#ifndef NT_COMBINE_PDL
+#define NT_COMBINE_PDL 1
+#endif
+
 namespace nt {
 
 struct AttnMaps {
@@ -96,12 +100,23 @@ int launch_attn(const AttnMaps& m, const AttnFwdParams& p, cudaStream_t st) {
     if (p.kv_split > 0) {
       int rc = launch_attn_kernel<D, MASK, F32, KVS, FP8, true, NQ>(m, p, st);
       if (rc || g_prepare_only) return rc;
-      // split-KV items: merge the fp32 partials
+      // split-KV items: merge the bf16 partials.  Programmatic dependent launch: the
+      // merge grid is launched while K1 runs (its CTAs take the SMs K1's finished
+      // CTAs free) and waits in griddepcontrol.wait for K1's completion and memory
       constexpr int ROWS = 128 * NQ;
-      attn_combine_kernel<D, MASK, F32, ROWS>
-          <<<dim3(ROWS / (8 * kCombineRowsPerWarp), p.B * p.Hq, p.n_split_mb), 256, 0, st>>>(m.part_o, p);
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(ROWS / (8 * kCombineRowsPerWarp), p.B * p.Hq, p.n_split_mb);
+      cfg.blockDim = dim3(256);
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = NT_COMBINE_PDL;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      const int rc2 = check_cuda(cudaLaunchKernelEx(&cfg, attn_combine_kernel<D, MASK, F32, ROWS>, m.part_o, p),
+                                 "attn_combine launch");
       g_launches++;
-      return check_cuda(cudaGetLastError(), "attn_combine launch");
+      return rc2;
     }
   }
   return launch_attn_kernel<D, MASK, F32, KVS, FP8, false, NQ>(m, p, st);
