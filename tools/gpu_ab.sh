@@ -1,3 +1,5 @@
+# A/B of library builds on one box: bash tools/gpu_ab.sh <variant> ... runs bench configs with
+# NT_LIB_PATH=ab/lib_<variant>.so (build them with build.build(defines=[...], out="ab/lib_<v>.so")), twice each.
 mkdir -p gpurun_out/ab
 for rep in 1 2; do
 for v in "$@"; do
