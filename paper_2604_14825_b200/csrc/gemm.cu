@@ -11,6 +11,10 @@
 #include "common_host.h"
 #include "gemm.cuh"
 
+#ifndef NT_GEMM_PDL
+#define NT_GEMM_PDL 1
+#endif
+
 #ifndef NT_GEMM_GROUP
 #define NT_GEMM_GROUP 0  // experiment: raster group rows (0 = default 8)
 #endif
@@ -18,6 +22,24 @@
 using namespace nt;
 
 namespace {
+// cudaLaunchKernelEx with programmatic stream serialization (the kernel calls
+// griddepcontrol.wait before it reads anything an earlier kernel wrote)
+template <typename Kern, typename... Args>
+int launch_pdl(Kern kern, dim3 grid, dim3 block, int smem, cudaStream_t st, const char* what, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = NT_GEMM_PDL;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const int rc = check_cuda(cudaLaunchKernelEx(&cfg, kern, args...), what);
+  g_launches++;
+  return rc;
+}
 int sm_count() {
   static int n = 0;
   if (!n) {
@@ -56,15 +78,15 @@ int launch_gemm(const nt_gemm_args* a, cudaStream_t st) {
   if ((rc = configure_smem<kern>(smem, "cudaFuncSetAttribute(gemm)"))) return rc;
   const int tiles = p.tiles_m * p.tiles_n * p.k_splits;
   const int grid = std::min(tiles, sm_count());
-  kern<<<grid, kGemmThreads, smem, st>>>(ma, mb, p);
-  g_launches++;
-  if ((rc = check_cuda(cudaGetLastError(), "gemm launch"))) return rc;
+  // programmatic dependent launches: this GEMM's prologue (barriers, TMEM) overlaps the
+  // previous kernel's tail -- e.g. the chain's T = X.W1 -- and griddepcontrol.wait
+  // inside holds every read of its inputs until that kernel's memory is visible
+  if ((rc = launch_pdl(kern, dim3(grid), dim3(kGemmThreads), smem, st, "gemm launch", ma, mb, p))) return rc;
   if (p.k_splits > 1) {
     const long long n4 = (long long)a->m * a->n / 4;
     const int blocks = (int)std::min<long long>((n4 + 255) / 256, 4LL * sm_count());
-    gemm_splitk_reduce<<<blocks, 256, 0, st>>>(p.ws, p.k_splits, a->m, a->n, a->c, a->ldc, F32);
-    g_launches++;
-    rc = check_cuda(cudaGetLastError(), "gemm split-K reduce");
+    rc = launch_pdl(gemm_splitk_reduce, dim3(blocks), dim3(256), 0, st, "gemm split-K reduce", (const float*)p.ws,
+                    p.k_splits, a->m, a->n, a->c, (long long)a->ldc, F32);
   }
   return rc;
 }
@@ -95,9 +117,7 @@ int launch_gemm2(const nt_gemm_args* a, cudaStream_t st) {
   if ((rc = configure_smem<kern>(smem, "cudaFuncSetAttribute(gemm2)"))) return rc;
   const int tiles = p.tiles_m * p.tiles_n;
   const int grid = 2 * std::min(tiles, sm_count() / 2);  // one CTA pair per tile, persistent
-  kern<<<grid, kGemmThreads, smem, st>>>(ma, mb, mc, p);
-  g_launches++;
-  return check_cuda(cudaGetLastError(), "gemm2 launch");
+  return launch_pdl(kern, dim3(grid), dim3(kGemmThreads), smem, st, "gemm2 launch", ma, mb, mc, p);
 }
 
 // F split so that row_blocks x splits ~ fills the SMs

@@ -62,6 +62,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const GemmParams p) {
   using C = GemmCfg<BN>;
+  asm volatile("griddepcontrol.launch_dependents;");  // the split-K reduce may be scheduled
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_u32 = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_u32 + 1023u) & ~1023u) - raw_u32);
@@ -95,6 +96,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // programmatic dependent launch: nothing is read or written before the preceding
+  // kernel on the stream has completed and its memory is visible
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
@@ -206,6 +210,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 // C = sum over k_splits of the fp32 partials (N % 4 == 0), cast to bf16 / fp32
 __global__ void gemm_splitk_reduce(const float* __restrict__ ws, int splits, int M, int N, void* c, long long ldc,
                                    bool out_f32) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // launched as a dependent of gemm_kernel
   const long long n4 = (long long)M * N / 4;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
     float4 acc = reinterpret_cast<const float4*>(ws)[i];
@@ -275,6 +280,7 @@ template <bool OUT_F32>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmC, const GemmParams p) {
+  asm volatile("griddepcontrol.launch_dependents;");  // a PDL-launched successor may stage its prologue
   using C = Gemm2Cfg<OUT_F32>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_u32 = smem_u32(smem_raw);
@@ -312,6 +318,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: inputs / outputs only after the predecessor
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
