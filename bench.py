@@ -69,6 +69,9 @@ CONFIGS = {
                       golden="decode4_32k", scale=LLAMA_SCALE),
     # the long end of config 5 (KV 128K: 34.4 GB of K/V; e2e skipped -- the pinned host
     # copy alone would be 34 GB per step)
+    # the same decode over an FP8 (e4m3) KV cache: half the bytes per key (kind::f8f6f4 dots)
+    "decode32k_e4m3": dict(kind="decode", prog="llama", B=64, Hq=32, Hkv=8, N=1, M=32768, D=128, causal=False,
+                           golden="decode4_32k", scale=LLAMA_SCALE, in_dtype="e4m3"),
     "decode128k": dict(kind="decode", prog="llama", B=64, Hq=32, Hkv=8, N=1, M=131072, D=128, causal=False,
                        golden="decode4_128k", scale=LLAMA_SCALE, no_e2e=True),
     # the same decode over a paged KV cache (16-token pages, shuffled block table)
@@ -415,12 +418,28 @@ def build_workload(cfg, spec, rank, world, dev):
             plan = PagedDecodePlan(q, pools[0], pools[1], block_table, seq_lens, o, spec.scale, layout=layout,
                                    max_seq_kv=M)
             w["pools"] = pools
-        kv_bytes = 2 * Bl * Hkvl * M * D * 2
+        esz = 2
+        host_inputs = {spec.q: q, spec.k: k, spec.v: v}
+        if cfg.get("in_dtype") == "e4m3":
+            # per-tensor e4m3 quantisation (descale = amax / 448) of the same q/k/v
+            ts, ds = [], []
+            for t in (q, k, v):
+                d = float(t.abs().max().float()) / 448.0
+                ts.append((t.float() / d).to(torch.float8_e4m3fn))
+                ds.append(d)
+            q, k, v = ts
+            del ts
+            plan = DecodePlan(q, k, v, o, spec.scale, q_descale=ds[0], k_descale=ds[1], v_descale=ds[2])
+            host_inputs = {"q": q, "k": k, "v": v}
+            esz = 1
+            w["e4m3"] = True
+        kv_bytes = 2 * Bl * Hkvl * M * D * esz
+        # O is written in bf16 (2 bytes) whatever the input type
         w.update(plan=plan, out=o, local_flops=4.0 * Bl * Hkvl * g * N * M * D,
                  total_flops=4.0 * cfg["B"] * cfg["Hq"] * N * M * D, bound="hbm",
-                 local_bytes=kv_bytes + 2 * q.numel() * 2, host_inputs={spec.q: q, spec.k: k, spec.v: v},
+                 local_bytes=kv_bytes + q.numel() * esz + o.numel() * 2, host_inputs=host_inputs,
                  outer=(Bl, Hkvl, Hkvl), mask_kind="none",
-                 in_bytes=(q.numel() + k.numel() + v.numel()) * 2)
+                 in_bytes=(q.numel() + k.numel() + v.numel()) * esz)
         return w
     Hql = Hkvl * g
     q = torch.randn((Bl, Hql, N, D), generator=gen, device=dev).to(torch.bfloat16)
@@ -581,7 +600,9 @@ def measure_e2e(args, cfg, w, plan, o, mod, stream, flush, world, dist, total_fl
         em = float(t[0])
     e2e = {"value": total_flops / (em * 1e-3) / 1e12, "unit": "TFLOP/s",
            "h2d_bytes_per_step": int(w["in_bytes"] * world), "d2h_bytes_per_step": int(o.numel() * 2 * world),
-           "ms_per_step": em, "api": ("AttentionPlan / nt_attn_fwd (pinned host e4m3 q/k/v -> device, O -> pinned host)"
+           "ms_per_step": em, "api": ("DecodePlan / nt_attn_decode (pinned host e4m3 q/k/v -> device, O -> pinned host)"
+                                     if w.get("e4m3") and w["kind"] == "decode" else
+                                     "AttentionPlan / nt_attn_fwd (pinned host e4m3 q/k/v -> device, O -> pinned host)"
                                      if w.get("e4m3") else
                                      "paper_2604_14825_b200.execute_ma(pinned host q/k/v, out=pinned host O): chunked H2D/kernel/D2H streams")}
 
@@ -609,7 +630,9 @@ def emit(args, cfg, w, plan, world, ma_src, ms_step, ms_kernel, ms_kernel_local,
                 "read_ceiling_gbs": READ_CEILING_GBS, "frac_of_read_ceiling": achieved / READ_CEILING_GBS,
                 "algorithmic_bytes_per_launch": w["local_bytes"],
                 "kernel": ("decode_tc_kernel<paged> (tcgen05 dots, page-slice TMA gathers) + combine"
-                           if cfg.get("page_size") else "decode_tc_kernel (tcgen05 dots) + combine")}
+                           if cfg.get("page_size") else
+                           "decode_tc_kernel<e4m3> (tcgen05 kind::f8f6f4 dots) + combine" if w.get("e4m3") else
+                           "decode_tc_kernel (tcgen05 dots) + combine")}
     else:
         achieved = w["local_flops"] / (ms_kernel_local * 1e-3) / 1e12
         peak = peaks["bf16_tflops"] * (2.0 if w.get("e4m3") else 1.0)

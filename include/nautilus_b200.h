@@ -30,7 +30,7 @@ extern "C" {
 
 /* 2: workspace_bytes in the decode / gemm / chain argument structs (the library
  *    rejects a workspace smaller than the launch needs instead of writing past it) */
-#define NT_ABI_VERSION 3
+#define NT_ABI_VERSION 4
 
 /* status codes (mapped by the host onto tilecc.errors CompilerError subclasses) */
 #define NT_OK 0
@@ -137,6 +137,11 @@ typedef struct nt_decode_args {
   void* workspace;
   int32_t* err_flag;
   int64_t workspace_bytes; /* size of `workspace`; < nt_decode_workspace_bytes(...) -> NT_ERR_INVALID */
+  /* q/k/v element type (ABI 4): NT_DTYPE_BF16 (0) or NT_DTYPE_E4M3 -- an FP8 KV
+   * cache; q is e4m3 too (one kind::f8f6f4 MMA for S and for PV, P in e4m3).
+   * Descales (0 reads as 1): S = (q k^T) q_descale k_descale scale, O = v_descale P V / l. */
+  int32_t in_dtype;
+  float q_descale, k_descale, v_descale;
 } nt_decode_args;
 /* rows_per_group = (heads_q / heads_kv) * seq_q; workspace = fp32 (O, m, l) per split */
 int64_t nt_decode_workspace_bytes(int32_t batch, int32_t heads_kv, int32_t rows_per_group, int32_t head_dim,

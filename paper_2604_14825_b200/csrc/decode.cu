@@ -74,13 +74,14 @@ bool use_tc_decode() {
   return !fma;
 }
 
-template <int R, int PG>
+template <int R, int PG, bool FP8>
 int launch_tc(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, DecodeParams& p, cudaStream_t st) {
   int rc;
-  constexpr auto kern = decode_tc_kernel<R, PG>;
-  if ((rc = configure_smem<kern>(kDtcSmem, "cudaFuncSetAttribute(decode_tc)"))) return rc;
+  constexpr auto kern = decode_tc_kernel<R, PG, FP8>;
+  constexpr int smem = DtcCfg<FP8>::SMEM;
+  if ((rc = configure_smem<kern>(smem, "cudaFuncSetAttribute(decode_tc)"))) return rc;
   dim3 grid(p.splits, p.B * p.Hkv);
-  kern<<<grid, kDtcThreads, kDtcSmem, st>>>(mq, mk, mv, p);
+  kern<<<grid, kDtcThreads, smem, st>>>(mq, mk, mv, p);
   g_launches++;
   if ((rc = check_cuda(cudaGetLastError(), "decode_tc launch"))) return rc;
   const int rows = p.B * p.Hkv * R;
@@ -89,22 +90,23 @@ int launch_tc(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& m
   return check_cuda(cudaGetLastError(), "decode_combine launch");
 }
 
-template <int PG>
+template <int PG, bool FP8 = false>
 int dispatch_tc(int R, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, DecodeParams& p,
                 cudaStream_t st) {
   switch (R) {
-    case 1: return launch_tc<1, PG>(mq, mk, mv, p, st);
-    case 2: return launch_tc<2, PG>(mq, mk, mv, p, st);
-    case 4: return launch_tc<4, PG>(mq, mk, mv, p, st);
-    default: return launch_tc<8, PG>(mq, mk, mv, p, st);
+    case 1: return launch_tc<1, PG, FP8>(mq, mk, mv, p, st);
+    case 2: return launch_tc<2, PG, FP8>(mq, mk, mv, p, st);
+    case 4: return launch_tc<4, PG, FP8>(mq, mk, mv, p, st);
+    default: return launch_tc<8, PG, FP8>(mq, mk, mv, p, st);
   }
 }
 
-int make_q_map(CUtensorMap* mq, const nt_tensor4& q, int B, int Hq, int Nq, int g) {
+// the group's rows as one box {64 bf16 | 128 e4m3 dims, Nq, g, 1} (one 128-byte panel)
+int make_q_map(CUtensorMap* mq, const nt_tensor4& q, int B, int Hq, int Nq, int g, size_t elem = 2) {
   const int64_t qd[4] = {kDecodeD, Nq, Hq, B};
   const int64_t qs[3] = {q.stride_s, q.stride_h, q.stride_b};
-  const int qb[4] = {64, Nq, g, 1};
-  return make_map_4d_box(mq, q.ptr, qd, qs, qb, 2);
+  const int qb[4] = {(int)(128 / elem), Nq, g, 1};
+  return make_map_4d_box(mq, q.ptr, qd, qs, qb, elem);
 }
 }  // namespace
 
@@ -124,9 +126,14 @@ extern "C" int nt_attn_decode(const nt_decode_args* a, void* stream) {
   if (!a->workspace || a->workspace_bytes < nt_decode_workspace_bytes(a->batch, a->heads_kv, R, a->head_dim,
                                                                       std::max(1, a->num_splits)))
     return set_error(NT_ERR_INVALID, "workspace missing or smaller than nt_decode_workspace_bytes(...)");
+  const bool fp8 = a->in_dtype == NT_DTYPE_E4M3;
+  if (a->in_dtype != NT_DTYPE_BF16 && !fp8) return set_error(NT_ERR_INVALID, "in_dtype must be bf16 or e4m3");
+  if (fp8 && !use_tc_decode()) return set_error(NT_ERR_UNSUPPORTED, "e4m3 decode runs on the tensor-core kernel only");
+  const int align = fp8 ? 16 : 8;  // strides in elements: 16 bytes either way
   for (const nt_tensor4* t : {&a->q, &a->k, &a->v})
-    if (reinterpret_cast<uintptr_t>(t->ptr) % 16 || t->stride_s % 8 || t->stride_h % 8 || t->stride_b % 8)
-      return set_error(NT_ERR_INVALID, "q/k/v must be 16-byte aligned with strides % 8 == 0");
+    if (reinterpret_cast<uintptr_t>(t->ptr) % 16 || t->stride_s % align || t->stride_h % align ||
+        t->stride_b % align)
+      return set_error(NT_ERR_INVALID, "q/k/v must be 16-byte aligned with 16-byte strides");
   DecodeParams p{};
   p.q = static_cast<const __nv_bfloat16*>(a->q.ptr);
   p.q_sb = a->q.stride_b; p.q_sh = a->q.stride_h; p.q_sn = a->q.stride_s;
@@ -138,7 +145,9 @@ extern "C" int nt_attn_decode(const nt_decode_args* a, void* stream) {
   p.o_sb = a->o.stride_b; p.o_sh = a->o.stride_h; p.o_sn = a->o.stride_s;
   p.out_f32 = a->out_dtype == NT_DTYPE_F32;
   p.B = a->batch; p.Hq = a->heads_q; p.Hkv = a->heads_kv; p.Nq = a->seq_q; p.M = a->seq_kv; p.g = g;
-  p.scale_log2 = a->scale * 1.4426950408889634f;
+  auto ds = [](float d) { return d == 0.f ? 1.f : d; };
+  p.scale_log2 = a->scale * 1.4426950408889634f * (fp8 ? ds(a->q_descale) * ds(a->k_descale) : 1.f);
+  p.o_scale = fp8 ? ds(a->v_descale) : 1.f;
   p.splits = std::max(1, a->num_splits);
   // key ranges are whole 64-key TMA tiles
   p.keys_per_split = ((a->seq_kv + p.splits - 1) / p.splits + kDecodeTile - 1) / kDecodeTile * kDecodeTile;
@@ -153,7 +162,16 @@ extern "C" int nt_attn_decode(const nt_decode_args* a, void* stream) {
     // K2b: 128-key tiles; the group's R query rows as one 4-D box {64, Nq, g, 1}
     p.keys_per_split = ((a->seq_kv + p.splits - 1) / p.splits + kDtcTile - 1) / kDtcTile * kDtcTile;
     CUtensorMap mq;
-    if ((rc = make_q_map(&mq, a->q, a->batch, a->heads_q, a->seq_q, g))) return rc;
+    if ((rc = make_q_map(&mq, a->q, a->batch, a->heads_q, a->seq_q, g, fp8 ? 1 : 2))) return rc;
+    if (fp8) {  // one 128-byte panel per key: box {128 dims, 128 keys, 1, 1}
+      if ((rc = make_map_4d(&mk, a->k.ptr, kDecodeD, a->seq_kv, a->heads_kv, a->batch, a->k.stride_s, a->k.stride_h,
+                            a->k.stride_b, kDtcTile, 1, 0, CU_TENSOR_MAP_SWIZZLE_128B)))
+        return rc;
+      if ((rc = make_map_4d(&mv, a->v.ptr, kDecodeD, a->seq_kv, a->heads_kv, a->batch, a->v.stride_s, a->v.stride_h,
+                            a->v.stride_b, kDtcTile, 1, 0, CU_TENSOR_MAP_SWIZZLE_128B)))
+        return rc;
+      return dispatch_tc<0, true>(R, mq, mk, mv, p, st);
+    }
     if ((rc = make_map_pages_5d(&mk, a->k.ptr, a->seq_kv, a->heads_kv, a->batch, a->k.stride_s, a->k.stride_h,
                                 a->k.stride_b, kDtcTile)))
       return rc;
@@ -199,6 +217,7 @@ extern "C" int nt_attn_decode_paged(const nt_decode_paged_args* a, void* stream)
   p.out_f32 = a->out_dtype == NT_DTYPE_F32;
   p.B = a->batch; p.Hq = a->heads_q; p.Hkv = a->heads_kv; p.Nq = a->seq_q; p.M = a->max_seq_kv; p.g = g;
   p.scale_log2 = a->scale * 1.4426950408889634f;
+  p.o_scale = 1.f;
   p.splits = std::max(1, a->num_splits);
   p.keys_per_split = ((a->max_seq_kv + p.splits - 1) / p.splits + kDecodeTile - 1) / kDecodeTile * kDecodeTile;
   p.ws = static_cast<float*>(a->workspace);

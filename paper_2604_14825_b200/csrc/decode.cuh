@@ -31,6 +31,7 @@ struct DecodeParams {
   int out_f32;
   int B, Hq, Hkv, Nq, M, g;  // rows per group R = g * Nq
   float scale_log2;
+  float o_scale;  // K2b e4m3: V's descale, applied to the partial O (1 otherwise)
   int splits, keys_per_split;
   float* ws;  // [B*Hkv, splits, R, D + 2]  (O, m, l)
   int* err;

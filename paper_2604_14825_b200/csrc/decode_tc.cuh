@@ -32,27 +32,60 @@ constexpr int kDtcHalf = kDtcTile * 128;                 // one panel (16 KB)
 constexpr int kDtcStages = 3;                            // K+V tile pairs in flight (192 KB)
 constexpr int kDtcThreads = 128;
 constexpr int kDtcSmem = kDtcTileBytes /* Q */ + kDtcStages * 2 * kDtcTileBytes + 1024 /* align */ + 256;
+// e4m3 K/V (FP8 KV cache): a 128-key tile is one 128-byte panel (16 KB), so twice
+// the stages fit -- the same 192 KB in flight
+template <bool FP8>
+struct DtcCfg {
+  static constexpr int TILE = kDtcTile * kDecodeD * (FP8 ? 1 : 2);
+  static constexpr int STAGES = FP8 ? 6 : kDtcStages;
+  static constexpr int KSTEP = FP8 ? 32 : 16;  // K per tcgen05.mma (kind::f8f6f4 | kind::f16)
+  static constexpr int SMEM = TILE + STAGES * 2 * TILE + 1024 + (FP8 ? 512 : 256);  // + barriers
+};
 
 // PG: 0 dense K/V ([B, Hkv, M, D] viewed as 5-D pages of M tokens); 1 paged cache with
 // page_size a multiple of 128 (one 5-D box {64, 128 tokens, 2 panels} per tile);
 // 2 paged with 8/16/32/64-token pages (per page slice and 64-dim panel one 4-D box
 // {64, page_size} straight into the canonical [panel][128 keys][128 B] tile -- one
 // lane per box, the page ids of the next tile fetched while this one is issued)
-template <int R, int PG = 0>
+// exps of one thread's 64 keys (a half row): P packed as 32 bf16 pairs | 16 e4m3
+// quads in key order, the sum of the exps returned
+template <bool FP8>
+__device__ __forceinline__ float dtc_exp_pass(const uint32_t (&s)[64], float sc, float m, uint32_t (&pk)[32]) {
+  const float2 sc2 = make_float2(sc, sc), nm2 = make_float2(-m, -m);
+  float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+  float2 prev = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const float2 x = ffma2(make_float2(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])), sc2, nm2);
+    const float2 e = make_float2(ex2(x.x), ex2(x.y));
+    sum2[i & 1] = fadd2(sum2[i & 1], e);
+    if constexpr (FP8) {
+      if (i & 1) pk[i >> 1] = pack_e4m3x4(prev.x, prev.y, e.x, e.y);
+      prev = e;
+    } else {
+      pk[i] = pack_bf16(e.x, e.y);
+    }
+  }
+  return (sum2[0].x + sum2[0].y) + (sum2[1].x + sum2[1].y);
+}
+
+template <int R, int PG = 0, bool FP8 = false>
 __global__ void __launch_bounds__(kDtcThreads, 1)
     decode_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                      const __grid_constant__ CUtensorMap tmV, const DecodeParams p) {
   constexpr int D = kDecodeD;
+  using DC = DtcCfg<FP8>;
+  constexpr int kTile = DC::TILE, kStages = DC::STAGES;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_u32 = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_u32 + 1023u) & ~1023u) - raw_u32);
   uint8_t* sQ = smem;
-  uint8_t* sKV = smem + kDtcTileBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + kDtcStages * 2 * kDtcTileBytes);
+  uint8_t* sKV = smem + kTile;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + kStages * 2 * kTile);
   uint64_t* bar_q = bars;
-  uint64_t* full = bars + 1;                 // [2 * stages]: K(t) / V(t) landed
-  uint64_t* empty = full + 2 * kDtcStages;   // [2 * stages]
-  uint64_t* bar_s = empty + 2 * kDtcStages;  // [2] S(t) in S_{t%2}
+  uint64_t* full = bars + 1;               // [2 * stages]: K(t) / V(t) landed
+  uint64_t* empty = full + 2 * kStages;    // [2 * stages]
+  uint64_t* bar_s = empty + 2 * kStages;   // [2] S(t) in S_{t%2}
   uint64_t* bar_sf = bar_s + 2;              // [2] S_{t%2} loaded into registers (reusable)
   uint64_t* bar_p = bar_sf + 2;              // P(t) in TMEM
   uint64_t* bar_pv = bar_p + 1;              // PV(t) done (P and O reusable)
@@ -69,7 +102,7 @@ __global__ void __launch_bounds__(kDtcThreads, 1)
   const int ntiles = (j1 > j0) ? (j1 - j0 + kDtcTile - 1) / kDtcTile : 0;
 
   // rows >= R of the padded Q tile are zero (S, P, O rows >= R are never read)
-  for (int i = threadIdx.x; i < kDtcTileBytes / 16; i += kDtcThreads)
+  for (int i = threadIdx.x; i < kTile / 16; i += kDtcThreads)
     reinterpret_cast<uint4*>(sQ)[i] = make_uint4(0, 0, 0, 0);
   fence_proxy_async_smem();
   if (warp == 1 && lane == 0) {
@@ -77,7 +110,7 @@ __global__ void __launch_bounds__(kDtcThreads, 1)
     prefetch_tmap(&tmK);
     prefetch_tmap(&tmV);
     mbar_init(bar_q, 1);
-    for (int i = 0; i < 2 * kDtcStages; ++i) {
+    for (int i = 0; i < 2 * kStages; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
@@ -100,20 +133,23 @@ __global__ void __launch_bounds__(kDtcThreads, 1)
     // ================= TMA producer
     if (ntiles > 0) {
       if (lane == 0) {
-        mbar_arrive_expect_tx(bar_q, R * D * 2);
-        // the group's R rows: box {64 dims, Nq rows, g heads, 1} per 64-dim panel
+        mbar_arrive_expect_tx(bar_q, R * D * (FP8 ? 1 : 2));
+        // the group's R rows: box {64 dims (bf16) | 128 dims (e4m3), Nq rows, g heads, 1} per panel
 #pragma unroll
-        for (int h = 0; h < 2; ++h) tma_load_4d(sQ + h * kDtcHalf, &tmQ, bar_q, h * 64, 0, hkv * p.g, b);
+        for (int h = 0; h < (FP8 ? 1 : 2); ++h) tma_load_4d(sQ + h * kDtcHalf, &tmQ, bar_q, h * 64, 0, hkv * p.g, b);
       }
       if constexpr (PG == 0) {
         if (lane == 0)
           for (int it = 0; it < 2 * ntiles; ++it) {
-            const int slot = it % (2 * kDtcStages);
-            mbar_wait(&empty[slot], ((it / (2 * kDtcStages)) & 1) ^ 1, p.err, 1);
-            mbar_arrive_expect_tx(&full[slot], kDtcTileBytes);
-            // one 5-D box {64 dims, 128 keys, 2 panels} = [panel][128 keys][128 B]
-            tma_load_5d(sKV + slot * kDtcTileBytes, (it & 1) ? &tmV : &tmK, &full[slot], 0,
-                        j0 + (it >> 1) * kDtcTile, 0, hkv, b);
+            const int slot = it % (2 * kStages);
+            mbar_wait(&empty[slot], ((it / (2 * kStages)) & 1) ^ 1, p.err, 1);
+            mbar_arrive_expect_tx(&full[slot], kTile);
+            if constexpr (FP8)  // one 4-D box {128 e4m3 dims, 128 keys} = one 128-byte panel
+              tma_load_4d(sKV + slot * kTile, (it & 1) ? &tmV : &tmK, &full[slot], 0, j0 + (it >> 1) * kDtcTile,
+                          hkv, b);
+            else  // one 5-D box {64 dims, 128 keys, 2 panels} = [panel][128 keys][128 B]
+              tma_load_5d(sKV + slot * kTile, (it & 1) ? &tmV : &tmK, &full[slot], 0, j0 + (it >> 1) * kDtcTile,
+                          0, hkv, b);
           }
       } else {
         const int ps = p.page_size;
@@ -133,14 +169,14 @@ __global__ void __launch_bounds__(kDtcThreads, 1)
         for (int t = 0; t < ntiles; ++t) {
           const int2 nxt = (active && t + 1 < ntiles) ? page_of(t + 1) : make_int2(0, 0);
           for (int kv = 0; kv < 2; ++kv) {
-            const int it = 2 * t + kv, slot = it % (2 * kDtcStages);
+            const int it = 2 * t + kv, slot = it % (2 * kStages);
             if (lane == 0) {
-              mbar_wait(&empty[slot], ((it / (2 * kDtcStages)) & 1) ^ 1, p.err, 1);
-              mbar_arrive_expect_tx(&full[slot], kDtcTileBytes);
+              mbar_wait(&empty[slot], ((it / (2 * kStages)) & 1) ^ 1, p.err, 1);
+              mbar_arrive_expect_tx(&full[slot], kTile);
             }
             __syncwarp();
             if (active) {
-              uint8_t* dst = sKV + slot * kDtcTileBytes;
+              uint8_t* dst = sKV + slot * kTile;
               const CUtensorMap* m = kv ? &tmV : &tmK;
               if constexpr (PG == 1) tma_load_5d(dst, m, &full[slot], 0, cur.y, 0, hkv, cur.x);
               else tma_load_4d(dst + panel * kDtcHalf + sub * ps * 128, m, &full[slot], panel * 64, cur.y, hkv, cur.x);
@@ -153,20 +189,22 @@ __global__ void __launch_bounds__(kDtcThreads, 1)
   } else if (warp == 2) {
     // ================= MMA issuer
     if (lane == 0 && ntiles > 0) {
-      constexpr uint32_t idS = idesc_bf16(128, 128, 0, 0);
-      constexpr uint32_t idO = idesc_bf16(128, D, 0, 1);
+      constexpr uint32_t idS = FP8 ? idesc_e4m3(128, 128, 0, 0) : idesc_bf16(128, 128, 0, 0);
+      constexpr uint32_t idO = FP8 ? idesc_e4m3(128, D, 0, 1) : idesc_bf16(128, D, 0, 1);
       const uint32_t sQa = smem_u32(sQ), sKVa = smem_u32(sKV);
       mbar_wait(bar_q, 0, p.err, 2);
       auto issue_s = [&](int t) {
-        const int gk = 2 * t, slotK = gk % (2 * kDtcStages);
-        mbar_wait(&full[slotK], (gk / (2 * kDtcStages)) & 1, p.err, 3);
+        const int gk = 2 * t, slotK = gk % (2 * kStages);
+        mbar_wait(&full[slotK], (gk / (2 * kStages)) & 1, p.err, 3);
         if (t >= 2) mbar_wait(&bar_sf[t & 1], ((t >> 1) - 1) & 1, p.err, 6);  // softmax(t-2) read S_{t%2}
         tc_fence_after();
 #pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
+        for (int k = 0; k < D / DC::KSTEP; ++k) {
+          // 32 bytes of K per instruction, 4 per 128-byte panel row
           const uint32_t off = (k >> 2) * kDtcHalf + (k & 3) * 32;
-          umma_ss(tmem + (t & 1) * 128, sdesc_sw128(sQa + off, 16, 1024),
-                  sdesc_sw128(sKVa + slotK * kDtcTileBytes + off, 16, 1024), idS, k > 0 ? 1u : 0u);
+          const uint64_t ad = sdesc_sw128(sQa + off, 16, 1024), bd = sdesc_sw128(sKVa + slotK * kTile + off, 16, 1024);
+          if constexpr (FP8) umma_ss_f8(tmem + (t & 1) * 128, ad, bd, idS, k > 0 ? 1u : 0u);
+          else umma_ss(tmem + (t & 1) * 128, ad, bd, idS, k > 0 ? 1u : 0u);
         }
         umma_commit(&bar_s[t & 1]);
         umma_commit(&empty[slotK]);
@@ -175,53 +213,56 @@ __global__ void __launch_bounds__(kDtcThreads, 1)
       for (int t = 0; t < ntiles; ++t) {
         if (t + 1 < ntiles) issue_s(t + 1);
         // PV(t): P from its own TMEM columns, V MN-major from shared memory
-        const int gv = 2 * t + 1, slotV = gv % (2 * kDtcStages);
+        const int gv = 2 * t + 1, slotV = gv % (2 * kStages);
         mbar_wait(bar_p, t & 1, p.err, 4);
-        mbar_wait(&full[slotV], (gv / (2 * kDtcStages)) & 1, p.err, 5);
+        mbar_wait(&full[slotV], (gv / (2 * kStages)) & 1, p.err, 5);
         tc_fence_after();
 #pragma unroll
-        for (int k = 0; k < kDtcTile / 16; ++k) {
-          const uint64_t bd = sdesc_sw128(sKVa + slotV * kDtcTileBytes + k * 16 * 128, kDtcHalf, 1024);
-          umma_ts(tmem + kColO, tmem + kColP + k * 8, bd, idO, (t > 0 || k > 0) ? 1u : 0u);
+        for (int k = 0; k < kDtcTile / DC::KSTEP; ++k) {
+          // KSTEP keys of V (MN-major, 128-byte rows) x P's 8 TMEM columns (bf16 pairs | e4m3 quads)
+          const uint64_t bd = sdesc_sw128(sKVa + slotV * kTile + k * DC::KSTEP * 128, kDtcHalf, 1024);
+          if constexpr (FP8) umma_ts_f8(tmem + kColO, tmem + kColP + k * 8, bd, idO, (t > 0 || k > 0) ? 1u : 0u);
+          else umma_ts(tmem + kColO, tmem + kColP + k * 8, bd, idO, (t > 0 || k > 0) ? 1u : 0u);
         }
         umma_commit(bar_pv);
         umma_commit(&empty[slotV]);
       }
     }
   } else if (warp == 0) {
-    // ================= softmax: one TMEM lane (= query row) per thread
+    // ================= softmax: two threads per query row (R <= 8 rows live in
+    // TMEM lanes 0-15): thread t holds row t % 16, keys (t / 16) * 64 + [0, 64)
+    // of each tile, through the .16x32bx2 fragment -- half the exps per thread
+    // of a one-row-per-thread loop, which on a 1-group-per-CTA decode is the chain
     const float NINF = f_ninf();
     const float sc = p.scale_log2;
     const uint32_t tO = tmem + kColO, tP = tmem + kColP;  // warp 0: lanes 0-31
+    const int half = lane >> 4;
     float m_run = NINF, l_run = 0.f;
     for (int t = 0; t < ntiles; ++t) {
       mbar_wait(&bar_s[t & 1], (t >> 1) & 1, p.err, 8);
       tc_fence_after();
-      uint32_t sv[128];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld32(tmem + (t & 1) * 128 + c * 32, sv + c * 32);
+      uint32_t sv[64];
+      tmem_ld32_x2<64>(tmem + (t & 1) * 128, sv);
+      tmem_ld32_x2<64>(tmem + (t & 1) * 128 + 32, sv + 32);
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_sf[t & 1]);  // S_{t%2} may take S(t+2)
-      const int kv0 = j0 + t * kDtcTile;
-      if (kv0 + kDtcTile > j1) {
+      const int kv0 = j0 + t * kDtcTile + half * 64;
+      if (kv0 + 64 > j1) {
 #pragma unroll
-        for (int c = 0; c < 128; ++c)
+        for (int c = 0; c < 64; ++c)
           if (kv0 + c >= j1) sv[c] = __float_as_uint(NINF);
       }
       float a0 = __uint_as_float(sv[0]), a1 = __uint_as_float(sv[1]);
-      float a2 = __uint_as_float(sv[2]), a3 = __uint_as_float(sv[3]);
 #pragma unroll
-      for (int c = 4; c + 8 <= 128; c += 8) {
+      for (int c = 2; c + 4 <= 64; c += 4) {
         a0 = fmax3(a0, __uint_as_float(sv[c]), __uint_as_float(sv[c + 1]));
         a1 = fmax3(a1, __uint_as_float(sv[c + 2]), __uint_as_float(sv[c + 3]));
-        a2 = fmax3(a2, __uint_as_float(sv[c + 4]), __uint_as_float(sv[c + 5]));
-        a3 = fmax3(a3, __uint_as_float(sv[c + 6]), __uint_as_float(sv[c + 7]));
       }
-      a0 = fmax3(a0, __uint_as_float(sv[124]), __uint_as_float(sv[125]));
-      a1 = fmax3(a1, __uint_as_float(sv[126]), __uint_as_float(sv[127]));
-      const float mx = fmaxf(fmax3(a0, a1, a2), a3);
+      a0 = fmax3(a0, a1, __uint_as_float(sv[62]));
+      float mx = fmaxf(a0, __uint_as_float(sv[63]));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));  // the row's other half
       const float m_new = fmaxf(m_run, mx * sc);
       float alpha = 1.0f;
       const bool rescale = __any_sync(0xffffffffu, m_new > m_run + kRescaleLog2);
@@ -231,21 +272,27 @@ __global__ void __launch_bounds__(kDtcThreads, 1)
         m_run = m_new;
       }
       const float m_use = (m_run == NINF) ? 0.f : m_run;
-      uint32_t pk[64];
-      l_run += attn_exp_pass<false, false>(sv, sc, m_use, tP, pk);  // exps into registers
+      uint32_t pk[32];
+      l_run += dtc_exp_pass<FP8>(sv, sc, m_use, pk);  // exps into registers (this half's l)
       if (t > 0) {
         // PV(t-1) read P(t-1) and wrote O: now P(t) may overwrite it and O be rescaled
         mbar_wait(bar_pv, (t - 1) & 1, p.err, 10);
         tc_fence_after();
+        // 32x32b: lane t's row; lanes 16-31 are rows past R (nothing reads them)
         if (rescale) attn_rescale_o<D>(tO, alpha);
       }
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_st16(tP + c * 16, pk + c * 16);
+      if constexpr (FP8) {
+        tmem_st16_x2<16>(tP, pk);  // e4m3 quads: columns half * 16 + [0, 16)
+      } else {
+        tmem_st16_x2<32>(tP, pk);  // bf16 pairs: columns half * 32 + [0, 32)
+        tmem_st16_x2<32>(tP + 16, pk + 16);
+      }
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_p);
     }
+    l_run += __shfl_xor_sync(0xffffffffu, l_run, 16);  // both halves' sums (same m_run)
     // ---- epilogue: rows < R -> partial (O unnormalised, m, l) in the workspace
     float* w = p.ws + ((long long)grp * p.splits + s) * R * (D + 2);
     if (ntiles > 0) {
@@ -260,7 +307,7 @@ __global__ void __launch_bounds__(kDtcThreads, 1)
 #pragma unroll
           for (int q = 0; q < 16; ++q)
             *reinterpret_cast<float2*>(w + lane * (D + 2) + c * 32 + 2 * q) =
-                make_float2(__uint_as_float(o[2 * q]), __uint_as_float(o[2 * q + 1]));
+                make_float2(__uint_as_float(o[2 * q]) * p.o_scale, __uint_as_float(o[2 * q + 1]) * p.o_scale);
         }
       }
     } else if (lane < R) {

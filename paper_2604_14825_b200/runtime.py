@@ -185,14 +185,24 @@ def _causal_pairs(N: int, M: int, off: int) -> int:
 
 
 class DecodePlan:
-    """K2 split-KV decode over [B, Hq, Nq, 128] queries ((Hq/Hkv) * Nq in {1, 2, 4, 8} rows per kv group)."""
+    """K2 split-KV decode over [B, Hq, Nq, 128] queries ((Hq/Hkv) * Nq in {1, 2, 4, 8} rows per kv group).
+
+    An FP8 KV cache: q, k, v all ``torch.float8_e4m3fn`` with per-tensor
+    descales, S = (q k^T) q_descale k_descale scale, O = v_descale softmax(S) V
+    (the same contract as AttentionPlan's e4m3 inputs; P rounded to e4m3).
+    """
 
     def __init__(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor,
-                 scale: Optional[float], num_splits: int = 0, err_flag: Optional[torch.Tensor] = None):
+                 scale: Optional[float], num_splits: int = 0, err_flag: Optional[torch.Tensor] = None,
+                 q_descale: float = 1.0, k_descale: float = 1.0, v_descale: float = 1.0):
         q, k, v, o = _as4(q), _as4(k), _as4(v), _as4(o)
+        e4m3 = q.dtype == torch.float8_e4m3fn
+        want = torch.float8_e4m3fn if e4m3 else torch.bfloat16
         for name, t in (("q", q), ("k", k), ("v", v)):
-            if t.dtype != torch.bfloat16 or not t.is_cuda:
-                raise InvalidArguments(f"{name} must be a CUDA bf16 tensor")
+            if t.dtype != want or not t.is_cuda:
+                raise InvalidArguments(f"{name} must be a CUDA bf16 tensor (or q, k, v all float8_e4m3fn)")
+        if o.dtype not in (torch.bfloat16, torch.float32):
+            raise InvalidArguments("o must be bf16 or fp32")
         B, Hq, Nq, D = q.shape
         _, Hkv, M, _ = k.shape
         if tuple(v.shape) != (B, Hkv, M, D) or tuple(o.shape) != (B, Hq, Nq, D) or Hq % Hkv:
@@ -212,9 +222,12 @@ class DecodePlan:
         a.workspace = self.ws.data_ptr()
         a.workspace_bytes = self.ws.numel() * 4
         a.err_flag = self.err.data_ptr()
+        a.in_dtype = _lib.NT_DTYPE_E4M3 if e4m3 else _lib.NT_DTYPE_BF16
+        a.q_descale, a.k_descale, a.v_descale = float(q_descale), float(k_descale), float(v_descale)
         self.args, self.splits = a, splits
         self.tensors = (q, k, v, o)
         self.shape = (B, Hq, Hkv, Nq, M, D)
+        self.elem_bytes = 1 if e4m3 else 2
         self._fn = L.nt_attn_decode
         self._ref = C.byref(a)
         self.mask_kind = "none"
@@ -230,7 +243,7 @@ class DecodePlan:
 
     def kv_bytes(self) -> int:
         B, _, Hkv, _, M, D = self.shape
-        return 2 * B * Hkv * M * D * 2
+        return 2 * B * Hkv * M * D * self.elem_bytes
 
     def check_errors(self) -> None:
         if int(self.err.item()) & 1:

@@ -24,7 +24,7 @@ def test_library_loads_and_exports_all_symbols():
     L = _lib.lib()
     for name in declared_symbols():
         assert hasattr(L, name), name
-    assert L.nt_abi_version() == 3
+    assert L.nt_abi_version() == 4
     assert L.nt_launch_count() >= 0
 
 

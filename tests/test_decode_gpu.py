@@ -200,3 +200,74 @@ def test_workspace_smaller_than_required_is_rejected():
     torch.cuda.synchronize()
     ref = a.float() @ b.float()
     assert float((c - ref).abs().max()) < 2e-2
+
+
+# ------------------------------------------------------------ e4m3 (FP8) KV cache
+# K2b with kind::f8f6f4: q, k, v in e4m3 with per-tensor descales, P rounded to
+# e4m3 before P.V.  Checked, like K1's e4m3 path (test_attention_gpu.py), against
+# the fp64 attention of the DEQUANTISED inputs: the bound covers P's 3-bit
+# mantissa and fp32 accumulation only.
+E4M3_MAX_ABS = 8e-2
+E4M3_REL_L2 = 4e-2
+
+
+def _quant_e4m3(x, amax_target=448.0):
+    t = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32))
+    descale = float(t.abs().max()) / amax_target
+    q = (t / descale).to(torch.float8_e4m3fn)
+    return q, descale, (q.float() * descale).double().numpy()
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,Nq,M,splits,out_dtype", [
+    (2, 8, 2, 1, 4096, 0, torch.float32),
+    (3, 4, 4, 2, 3000, 0, torch.bfloat16),   # ragged tail tile
+    (1, 16, 2, 1, 20000, 7, torch.float32),  # 8 rows per group, explicit splits
+    (2, 4, 1, 1, 777, 3, torch.float32),
+    (1, 2, 2, 1, 64, 0, torch.float32),      # one partial tile
+])
+def test_e4m3_decode_vs_fp64_of_dequantised_inputs(B, Hq, Hkv, Nq, M, splits, out_dtype):
+    from paper_2604_14825_b200.runtime import DecodePlan
+
+    D = 128
+    g = np.random.default_rng(7 * B + M)
+    q8, qd, qf = _quant_e4m3(g.standard_normal((B, Hq, Nq, D)) * 1.5)
+    k8, kd, kf = _quant_e4m3(g.standard_normal((B, Hkv, M, D)))
+    v8, vd, vf = _quant_e4m3(g.standard_normal((B, Hkv, M, D)))
+    o = torch.empty((B, Hq, Nq, D), dtype=out_dtype, device="cuda")
+    plan = DecodePlan(q8.cuda(), k8.cuda(), v8.cuda(), o, 1 / np.sqrt(D), num_splits=splits,
+                      q_descale=qd, k_descale=kd, v_descale=vd)
+    plan.launch()
+    torch.cuda.synchronize()
+    plan.check_errors()
+    ref = reference_math.attention_batched_fp64(qf, kf, vf, 1 / np.sqrt(D), False)
+    _check(o.float().cpu().numpy(), ref, max_abs=E4M3_MAX_ABS, rel=E4M3_REL_L2)
+
+
+def test_e4m3_decode_128k_single_sequence():
+    """One long sequence: every split holds ~1K keys, the combine merges ~128 partials."""
+    from paper_2604_14825_b200.runtime import DecodePlan
+
+    B, Hq, Hkv, M, D = 1, 8, 1, 131072, 128
+    g = np.random.default_rng(11)
+    q8, qd, qf = _quant_e4m3(g.standard_normal((B, Hq, 1, D)))
+    k8, kd, kf = _quant_e4m3(g.standard_normal((B, Hkv, M, D)))
+    v8, vd, vf = _quant_e4m3(g.standard_normal((B, Hkv, M, D)))
+    o = torch.empty((B, Hq, 1, D), dtype=torch.float32, device="cuda")
+    plan = DecodePlan(q8.cuda(), k8.cuda(), v8.cuda(), o, 1 / np.sqrt(D), q_descale=qd, k_descale=kd,
+                      v_descale=vd)
+    assert plan.kv_bytes() == 2 * M * D
+    plan.launch()
+    torch.cuda.synchronize()
+    ref = reference_math.attention_batched_fp64(qf, kf, vf, 1 / np.sqrt(D), False)
+    _check(o.cpu().numpy(), ref, max_abs=E4M3_MAX_ABS, rel=E4M3_REL_L2)
+
+
+def test_e4m3_decode_rejects_mixed_dtypes():
+    from paper_2604_14825_b200.errors import InvalidArguments
+    from paper_2604_14825_b200.runtime import DecodePlan
+
+    q = torch.zeros((1, 2, 1, 128), dtype=torch.float8_e4m3fn, device="cuda")
+    k = torch.zeros((1, 2, 256, 128), dtype=torch.bfloat16, device="cuda")
+    o = torch.empty((1, 2, 1, 128), dtype=torch.float32, device="cuda")
+    with pytest.raises(InvalidArguments):
+        DecodePlan(q, k, k, o, 0.1)
