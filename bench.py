@@ -72,6 +72,9 @@ CONFIGS = {
     # the same decode over an FP8 (e4m3) KV cache: half the bytes per key (kind::f8f6f4 dots)
     "decode32k_e4m3": dict(kind="decode", prog="llama", B=64, Hq=32, Hkv=8, N=1, M=32768, D=128, causal=False,
                            golden="decode4_32k", scale=LLAMA_SCALE, in_dtype="e4m3"),
+    "decode32k_e4m3_paged16": dict(kind="decode", prog="llama", B=64, Hq=32, Hkv=8, N=1, M=32768, D=128,
+                                   causal=False, golden="decode4_32k", scale=LLAMA_SCALE, in_dtype="e4m3",
+                                   page_size=16),
     "decode128k": dict(kind="decode", prog="llama", B=64, Hq=32, Hkv=8, N=1, M=131072, D=128, causal=False,
                        golden="decode4_128k", scale=LLAMA_SCALE, no_e2e=True),
     # the same decode over a paged KV cache (16-token pages, shuffled block table)
@@ -395,7 +398,22 @@ def build_workload(cfg, spec, rank, world, dev):
         k = torch.randn((Bl, Hkvl, M, D), generator=gen, device=dev).to(torch.bfloat16)
         v = torch.randn((Bl, Hkvl, M, D), generator=gen, device=dev).to(torch.bfloat16)
         o = torch.empty((Bl, Hkvl, g * N, D), dtype=torch.bfloat16, device=dev)
-        plan = DecodePlan(q, k, v, o, spec.scale)
+        esz, kw = 2, {}
+        host_inputs = {spec.q: q, spec.k: k, spec.v: v}
+        if cfg.get("in_dtype") == "e4m3":
+            # per-tensor e4m3 quantisation (descale = amax / 448) of the same q/k/v: an FP8 KV cache
+            ts, ds = [], []
+            for t in (q, k, v):
+                d = float(t.abs().max().float()) / 448.0
+                ts.append((t.float() / d).to(torch.float8_e4m3fn))
+                ds.append(d)
+            q, k, v = ts
+            del ts
+            kw = dict(q_descale=ds[0], k_descale=ds[1], v_descale=ds[2])
+            host_inputs = {"q": q, "k": k, "v": v}
+            esz = 1
+            w["e4m3"] = True
+        plan = DecodePlan(q, k, v, o, spec.scale, **kw)
         if cfg.get("page_size"):
             # NHD page pools [pages, page_size, Hkv, D] in a shuffled physical order
             from paper_2604_14825_b200.runtime import PagedDecodePlan
@@ -405,34 +423,23 @@ def build_workload(cfg, spec, rank, world, dev):
             layout = cfg.get("page_layout", "NHD")
             pools = []
             for t in (k, v):
+                # scatter as raw bytes / bf16 (index_put has no float8 kernel)
+                tb = t.view(torch.uint8) if esz == 1 else t
                 if layout == "NHD":
-                    pool = torch.empty((Bl * npp, ps, Hkvl, D), dtype=torch.bfloat16, device=dev)
-                    pool[perm.long()] = t.permute(0, 2, 1, 3).reshape(Bl * npp, ps, Hkvl, D)
+                    pool = torch.empty((Bl * npp, ps, Hkvl, D), dtype=tb.dtype, device=dev)
+                    pool[perm.long()] = tb.permute(0, 2, 1, 3).reshape(Bl * npp, ps, Hkvl, D)
                 else:
-                    pool = torch.empty((Bl * npp, Hkvl, ps, D), dtype=torch.bfloat16, device=dev)
-                    pool[perm.long()] = t.reshape(Bl, Hkvl, npp, ps, D).permute(0, 2, 1, 3, 4).reshape(
+                    pool = torch.empty((Bl * npp, Hkvl, ps, D), dtype=tb.dtype, device=dev)
+                    pool[perm.long()] = tb.reshape(Bl, Hkvl, npp, ps, D).permute(0, 2, 1, 3, 4).reshape(
                         Bl * npp, Hkvl, ps, D)
-                pools.append(pool)
+                pools.append(pool.view(t.dtype))
             block_table = perm.reshape(Bl, npp).contiguous()
             seq_lens = torch.full((Bl,), M, dtype=torch.int32, device=dev)
             plan = PagedDecodePlan(q, pools[0], pools[1], block_table, seq_lens, o, spec.scale, layout=layout,
-                                   max_seq_kv=M)
+                                   max_seq_kv=M, **kw)
             w["pools"] = pools
-        esz = 2
-        host_inputs = {spec.q: q, spec.k: k, spec.v: v}
-        if cfg.get("in_dtype") == "e4m3":
-            # per-tensor e4m3 quantisation (descale = amax / 448) of the same q/k/v
-            ts, ds = [], []
-            for t in (q, k, v):
-                d = float(t.abs().max().float()) / 448.0
-                ts.append((t.float() / d).to(torch.float8_e4m3fn))
-                ds.append(d)
-            q, k, v = ts
-            del ts
-            plan = DecodePlan(q, k, v, o, spec.scale, q_descale=ds[0], k_descale=ds[1], v_descale=ds[2])
-            host_inputs = {"q": q, "k": k, "v": v}
-            esz = 1
-            w["e4m3"] = True
+            if esz == 1:  # e2e: the e4m3 page pools are what a serving runtime ships
+                host_inputs = {"q": q, "k": pools[0], "v": pools[1]}
         kv_bytes = 2 * Bl * Hkvl * M * D * esz
         # O is written in bf16 (2 bytes) whatever the input type
         w.update(plan=plan, out=o, local_flops=4.0 * Bl * Hkvl * g * N * M * D,
@@ -600,7 +607,10 @@ def measure_e2e(args, cfg, w, plan, o, mod, stream, flush, world, dist, total_fl
         em = float(t[0])
     e2e = {"value": total_flops / (em * 1e-3) / 1e12, "unit": "TFLOP/s",
            "h2d_bytes_per_step": int(w["in_bytes"] * world), "d2h_bytes_per_step": int(o.numel() * 2 * world),
-           "ms_per_step": em, "api": ("DecodePlan / nt_attn_decode (pinned host e4m3 q/k/v -> device, O -> pinned host)"
+           "ms_per_step": em, "api": ("PagedDecodePlan / nt_attn_decode_paged (pinned host e4m3 q + page pools -> "
+                                      "device, O -> pinned host)"
+                                      if w.get("e4m3") and cfg.get("page_size") else
+                                      "DecodePlan / nt_attn_decode (pinned host e4m3 q/k/v -> device, O -> pinned host)"
                                      if w.get("e4m3") and w["kind"] == "decode" else
                                      "AttentionPlan / nt_attn_fwd (pinned host e4m3 q/k/v -> device, O -> pinned host)"
                                      if w.get("e4m3") else
@@ -629,10 +639,9 @@ def emit(args, cfg, w, plan, world, ma_src, ms_step, ms_kernel, ms_kernel_local,
                 # tools/ubench/bulk_read.cu on this pool's B200 (r02: 7398 GB/s, 192 KB in flight per SM)
                 "read_ceiling_gbs": READ_CEILING_GBS, "frac_of_read_ceiling": achieved / READ_CEILING_GBS,
                 "algorithmic_bytes_per_launch": w["local_bytes"],
-                "kernel": ("decode_tc_kernel<paged> (tcgen05 dots, page-slice TMA gathers) + combine"
-                           if cfg.get("page_size") else
-                           "decode_tc_kernel<e4m3> (tcgen05 kind::f8f6f4 dots) + combine" if w.get("e4m3") else
-                           "decode_tc_kernel (tcgen05 dots) + combine")}
+                "kernel": ("decode_tc_kernel" + ("<paged" if cfg.get("page_size") else "<dense")
+                           + (", e4m3> (tcgen05 kind::f8f6f4 dots" if w.get("e4m3") else "> (tcgen05 kind::f16 dots")
+                           + (", page-slice TMA gathers) + combine" if cfg.get("page_size") else ") + combine"))}
     else:
         achieved = w["local_flops"] / (ms_kernel_local * 1e-3) / 1e12
         peak = peaks["bf16_tflops"] * (2.0 if w.get("e4m3") else 1.0)

@@ -164,7 +164,7 @@ int nt_attn_decode(const nt_decode_args* args, void* stream);
  */
 typedef struct nt_decode_paged_args {
   nt_tensor4 q, o;                /* [batch, heads_q, seq_q, 128] */
-  const void* k_pages;            /* bf16 page pools */
+  const void* k_pages;            /* bf16 (or e4m3, in_dtype) page pools */
   const void* v_pages;
   int64_t page_stride, token_stride, head_stride; /* element strides, same for K and V */
   int32_t num_pages, page_size;
@@ -178,6 +178,10 @@ typedef struct nt_decode_paged_args {
   void* workspace;
   int32_t* err_flag;
   int64_t workspace_bytes; /* size of `workspace`; too small -> NT_ERR_INVALID */
+  /* ABI 4: e4m3 page pools + q (NT_DTYPE_E4M3; page_size dividing or a multiple of
+   * 128), descales as in nt_decode_args */
+  int32_t in_dtype;
+  float q_descale, k_descale, v_descale;
 } nt_decode_paged_args;
 int nt_attn_decode_paged(const nt_decode_paged_args* args, void* stream);
 

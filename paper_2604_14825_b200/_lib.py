@@ -64,7 +64,9 @@ class DecodePagedArgs(C.Structure):
                 ("batch", C.c_int32), ("heads_q", C.c_int32), ("heads_kv", C.c_int32),
                 ("seq_q", C.c_int32), ("max_seq_kv", C.c_int32), ("head_dim", C.c_int32),
                 ("scale", C.c_float), ("num_splits", C.c_int32), ("out_dtype", C.c_int32),
-                ("workspace", C.c_void_p), ("err_flag", C.c_void_p), ("workspace_bytes", C.c_int64)]
+                ("workspace", C.c_void_p), ("err_flag", C.c_void_p), ("workspace_bytes", C.c_int64),
+                ("in_dtype", C.c_int32), ("q_descale", C.c_float), ("k_descale", C.c_float),
+                ("v_descale", C.c_float)]
 
 
 class GemmArgs(C.Structure):

@@ -206,9 +206,14 @@ extern "C" int nt_attn_decode_paged(const nt_decode_paged_args* a, void* stream)
   if (a->workspace_bytes < nt_decode_workspace_bytes(a->batch, a->heads_kv, R, a->head_dim, std::max(1, a->num_splits)))
     return set_error(NT_ERR_INVALID, "workspace smaller than nt_decode_workspace_bytes(...)");
   if (a->max_seq_kv <= 0 || a->num_pages <= 0) return set_error(NT_ERR_INVALID, "empty cache");
-  for (const nt_tensor4* t : {&a->q})
-    if (reinterpret_cast<uintptr_t>(t->ptr) % 16 || t->stride_s % 8 || t->stride_h % 8 || t->stride_b % 8)
-      return set_error(NT_ERR_INVALID, "q must be 16-byte aligned with strides % 8 == 0");
+  const bool fp8 = a->in_dtype == NT_DTYPE_E4M3;
+  if (a->in_dtype != NT_DTYPE_BF16 && !fp8) return set_error(NT_ERR_INVALID, "in_dtype must be bf16 or e4m3");
+  if (fp8 && (!use_tc_decode() || (kDtcTile % ps && ps % kDtcTile)))
+    return set_error(NT_ERR_UNSUPPORTED, "e4m3 paged decode: tensor-core kernel, page_size dividing or a multiple of 128");
+  const int align = fp8 ? 16 : 8;  // element strides of 16 bytes
+  if (reinterpret_cast<uintptr_t>(a->q.ptr) % 16 || a->q.stride_s % align || a->q.stride_h % align ||
+      a->q.stride_b % align)
+    return set_error(NT_ERR_INVALID, "q must be 16-byte aligned with 16-byte strides");
   DecodeParams p{};
   p.q = static_cast<const __nv_bfloat16*>(a->q.ptr);
   p.q_sb = a->q.stride_b; p.q_sh = a->q.stride_h; p.q_sn = a->q.stride_s;
@@ -216,8 +221,9 @@ extern "C" int nt_attn_decode_paged(const nt_decode_paged_args* a, void* stream)
   p.o_sb = a->o.stride_b; p.o_sh = a->o.stride_h; p.o_sn = a->o.stride_s;
   p.out_f32 = a->out_dtype == NT_DTYPE_F32;
   p.B = a->batch; p.Hq = a->heads_q; p.Hkv = a->heads_kv; p.Nq = a->seq_q; p.M = a->max_seq_kv; p.g = g;
-  p.scale_log2 = a->scale * 1.4426950408889634f;
-  p.o_scale = 1.f;
+  auto ds = [](float d) { return d == 0.f ? 1.f : d; };
+  p.scale_log2 = a->scale * 1.4426950408889634f * (fp8 ? ds(a->q_descale) * ds(a->k_descale) : 1.f);
+  p.o_scale = fp8 ? ds(a->v_descale) : 1.f;
   p.splits = std::max(1, a->num_splits);
   p.keys_per_split = ((a->max_seq_kv + p.splits - 1) / p.splits + kDecodeTile - 1) / kDecodeTile * kDecodeTile;
   p.ws = static_cast<float*>(a->workspace);
@@ -232,8 +238,18 @@ extern "C" int nt_attn_decode_paged(const nt_decode_paged_args* a, void* stream)
     // K2b over the page pool: 128-key tiles gathered page slice by page slice
     p.keys_per_split = ((a->max_seq_kv + p.splits - 1) / p.splits + kDtcTile - 1) / kDtcTile * kDtcTile;
     CUtensorMap mq;
-    if ((rc = make_q_map(&mq, a->q, a->batch, a->heads_q, a->seq_q, g))) return rc;
+    if ((rc = make_q_map(&mq, a->q, a->batch, a->heads_q, a->seq_q, g, fp8 ? 1 : 2))) return rc;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (fp8) {  // one 128-byte panel per token: box {128 dims, min(page, 128) tokens}
+      const int rows = std::min(ps, kDtcTile);
+      if ((rc = make_map_4d(&mk, a->k_pages, kDecodeD, ps, a->heads_kv, a->num_pages, a->token_stride,
+                            a->head_stride, a->page_stride, rows, 1, 0, CU_TENSOR_MAP_SWIZZLE_128B)))
+        return rc;
+      if ((rc = make_map_4d(&mv, a->v_pages, kDecodeD, ps, a->heads_kv, a->num_pages, a->token_stride,
+                            a->head_stride, a->page_stride, rows, 1, 0, CU_TENSOR_MAP_SWIZZLE_128B)))
+        return rc;
+      return ps % kDtcTile == 0 ? dispatch_tc<1, true>(R, mq, mk, mv, p, st) : dispatch_tc<2, true>(R, mq, mk, mv, p, st);
+    }
     if (ps % kDtcTile == 0) {
       if ((rc = make_map_pages_5d(&mk, a->k_pages, ps, a->heads_kv, a->num_pages, a->token_stride, a->head_stride,
                                   a->page_stride, kDtcTile)))

@@ -155,10 +155,10 @@ __global__ void __launch_bounds__(kDtcThreads, 1)
         const int ps = p.page_size;
         const int* bt = p.block_table + (long long)b * p.bt_stride;
         const int last_page = (seq_len - 1) / ps;
-        // PG 2: lane = (page slice, panel); PG 1: lane 0 only
+        // PG 2: lane = (page slice, panel) -- e4m3: one panel, lane = slice; PG 1: lane 0 only
         const int nsub = (PG == 2) ? kDtcTile / ps : 1;
-        const int sub = lane >> 1, panel = lane & 1;
-        const bool active = (PG == 2) ? (lane < 2 * nsub) : (lane == 0);
+        const int sub = FP8 ? lane : lane >> 1, panel = FP8 ? 0 : lane & 1;
+        const bool active = (PG == 2) ? (lane < (FP8 ? 1 : 2) * nsub) : (lane == 0);
         auto page_of = [&](int t) -> int2 {  // (physical page, token within it) of this lane's slice
           const int tok = j0 + t * kDtcTile + ((PG == 2) ? sub * ps : 0);
           const int pg = tok / ps;
@@ -178,7 +178,8 @@ __global__ void __launch_bounds__(kDtcThreads, 1)
             if (active) {
               uint8_t* dst = sKV + slot * kTile;
               const CUtensorMap* m = kv ? &tmV : &tmK;
-              if constexpr (PG == 1) tma_load_5d(dst, m, &full[slot], 0, cur.y, 0, hkv, cur.x);
+              if constexpr (PG == 1 && FP8) tma_load_4d(dst, m, &full[slot], 0, cur.y, hkv, cur.x);
+              else if constexpr (PG == 1) tma_load_5d(dst, m, &full[slot], 0, cur.y, 0, hkv, cur.x);
               else tma_load_4d(dst + panel * kDtcHalf + sub * ps * 128, m, &full[slot], panel * 64, cur.y, hkv, cur.x);
             }
           }

@@ -258,16 +258,21 @@ class PagedDecodePlan:
     (any strides with the head dim contiguous).  ``block_table``: int32
     [B, max_pages]; ``seq_lens``: int32 [B] keys per sequence.  ``q`` / ``o``:
     [B, Hq, Nq, 128].  The MA program is the dense decode kernel; paging is how
-    a serving runtime lays out its K/V buffers.
+    a serving runtime lays out its K/V buffers.  An FP8 cache: q and both pools
+    ``torch.float8_e4m3fn`` with per-tensor descales (DecodePlan's contract), page
+    sizes dividing or a multiple of 128.
     """
 
     def __init__(self, q: torch.Tensor, k_pages: torch.Tensor, v_pages: torch.Tensor, block_table: torch.Tensor,
                  seq_lens: torch.Tensor, o: torch.Tensor, scale: Optional[float], layout: str = "NHD",
-                 max_seq_kv: Optional[int] = None, num_splits: int = 0, err_flag: Optional[torch.Tensor] = None):
+                 max_seq_kv: Optional[int] = None, num_splits: int = 0, err_flag: Optional[torch.Tensor] = None,
+                 q_descale: float = 1.0, k_descale: float = 1.0, v_descale: float = 1.0):
         q, o = _as4(q), _as4(o)
+        e4m3 = q.dtype == torch.float8_e4m3fn
+        want = torch.float8_e4m3fn if e4m3 else torch.bfloat16
         for name, t in (("q", q), ("k_pages", k_pages), ("v_pages", v_pages)):
-            if t.dtype != torch.bfloat16 or not t.is_cuda:
-                raise InvalidArguments(f"{name} must be a CUDA bf16 tensor")
+            if t.dtype != want or not t.is_cuda:
+                raise InvalidArguments(f"{name} must be a CUDA bf16 tensor (or q and both pools float8_e4m3fn)")
         if k_pages.shape != v_pages.shape or k_pages.stride() != v_pages.stride() or k_pages.dim() != 4:
             raise InvalidArguments("k_pages / v_pages must be rank-4 pools of identical shape and strides")
         if block_table.dtype != torch.int32 or seq_lens.dtype != torch.int32:
@@ -307,6 +312,9 @@ class PagedDecodePlan:
         a.workspace = self.ws.data_ptr()
         a.workspace_bytes = self.ws.numel() * 4
         a.err_flag = self.err.data_ptr()
+        a.in_dtype = _lib.NT_DTYPE_E4M3 if e4m3 else _lib.NT_DTYPE_BF16
+        a.q_descale, a.k_descale, a.v_descale = float(q_descale), float(k_descale), float(v_descale)
+        self.elem_bytes = 1 if e4m3 else 2
         self.args, self.splits = a, splits
         self.tensors = (q, k_pages, v_pages, bt, seq_lens, o)
         self.shape = (B, Hq, Hkv, Nq, M, D)
@@ -322,7 +330,7 @@ class PagedDecodePlan:
     def kv_bytes(self) -> int:
         """K+V bytes the launch streams: every sequence's keys (seq_lens, read on the host)."""
         _, _, Hkv, _, _, D = self.shape
-        return int(self.tensors[4].sum().item()) * Hkv * D * 2 * 2
+        return int(self.tensors[4].sum().item()) * Hkv * D * 2 * self.elem_bytes
 
     def check_errors(self) -> None:
         if int(self.err.item()) & 1:

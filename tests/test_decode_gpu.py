@@ -271,3 +271,58 @@ def test_e4m3_decode_rejects_mixed_dtypes():
     o = torch.empty((1, 2, 1, 128), dtype=torch.float32, device="cuda")
     with pytest.raises(InvalidArguments):
         DecodePlan(q, k, k, o, 0.1)
+
+
+def _paged_e4m3(k8, v8, page_size, layout, seed):
+    """e4m3 page pools (as uint8 bytes through the fp32 scatter, then reinterpreted)."""
+    kp, vp, bt = _paged_cache(k8.view(torch.uint8).numpy().astype(np.float32),
+                              v8.view(torch.uint8).numpy().astype(np.float32), page_size, layout, seed)
+    as8 = lambda x: torch.from_numpy(x.astype(np.uint8)).view(torch.float8_e4m3fn).cuda()  # noqa: E731
+    return as8(kp), as8(vp), torch.from_numpy(bt).cuda()
+
+
+@pytest.mark.parametrize("page_size,layout", [(16, "NHD"), (64, "HND"), (128, "NHD"), (256, "HND")])
+def test_e4m3_paged_decode_vs_fp64(page_size, layout):
+    """FP8 paged cache, ragged sequence lengths, vs fp64 of the dequantised inputs."""
+    from paper_2604_14825_b200.runtime import PagedDecodePlan
+
+    B, Hq, Hkv, Nq, M, D = 4, 16, 4, 1, 2304, 128
+    g = np.random.default_rng(100 + page_size)
+    q8, qd, qf = _quant_e4m3(g.standard_normal((B, Hq, Nq, D)))
+    k8, kd, kf = _quant_e4m3(g.standard_normal((B, Hkv, M, D)))
+    v8, vd, vf = _quant_e4m3(g.standard_normal((B, Hkv, M, D)))
+    lens = np.array([M, 1, 777, 1500], dtype=np.int32)
+    kp, vp, bt = _paged_e4m3(k8, v8, page_size, layout, seed=9)
+    o = torch.empty((B, Hq, Nq, D), dtype=torch.float32, device="cuda")
+    plan = PagedDecodePlan(q8.cuda(), kp, vp, bt, torch.from_numpy(lens).cuda(), o, 1 / np.sqrt(D), layout=layout,
+                           max_seq_kv=M, q_descale=qd, k_descale=kd, v_descale=vd)
+    assert plan.kv_bytes() == int(lens.sum()) * Hkv * D * 2
+    plan.launch()
+    torch.cuda.synchronize()
+    plan.check_errors()
+    got = o.cpu().numpy()
+    for b in range(B):
+        n = int(lens[b])
+        ref = reference_math.attention_batched_fp64(qf[b:b + 1], kf[b:b + 1, :, :n], vf[b:b + 1, :, :n],
+                                                    1 / np.sqrt(D), False)
+        _check(got[b:b + 1], ref, max_abs=E4M3_MAX_ABS, rel=E4M3_REL_L2)
+
+
+def test_e4m3_paged_decode_is_bitwise_the_dense_decode():
+    """Same splits, same keys: the page gathers build the dense kernel's shared-memory tiles."""
+    from paper_2604_14825_b200.runtime import DecodePlan, PagedDecodePlan
+
+    B, Hq, Hkv, Nq, M, D = 2, 8, 2, 1, 4096, 128
+    g = np.random.default_rng(6)
+    q8, qd, _ = _quant_e4m3(g.standard_normal((B, Hq, Nq, D)))
+    k8, kd, _ = _quant_e4m3(g.standard_normal((B, Hkv, M, D)))
+    v8, vd, _ = _quant_e4m3(g.standard_normal((B, Hkv, M, D)))
+    kp, vp, bt = _paged_e4m3(k8, v8, 32, "NHD", seed=4)
+    o1 = torch.empty((B, Hq, Nq, D), dtype=torch.float32, device="cuda")
+    o2 = torch.empty_like(o1)
+    kw = dict(q_descale=qd, k_descale=kd, v_descale=vd)
+    DecodePlan(q8.cuda(), k8.cuda(), v8.cuda(), o1, 0.088, num_splits=6, **kw).launch()
+    PagedDecodePlan(q8.cuda(), kp, vp, bt, torch.full((B,), M, dtype=torch.int32, device="cuda"), o2, 0.088,
+                    max_seq_kv=M, num_splits=6, **kw).launch()
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2)
