@@ -75,6 +75,12 @@ CONFIGS = {
     "decode32k_e4m3_paged16": dict(kind="decode", prog="llama", B=64, Hq=32, Hkv=8, N=1, M=32768, D=128,
                                    causal=False, golden="decode4_32k", scale=LLAMA_SCALE, in_dtype="e4m3",
                                    page_size=16),
+    "decode32k_e4m3_paged16_hnd": dict(kind="decode", prog="llama", B=64, Hq=32, Hkv=8, N=1, M=32768, D=128,
+                                       causal=False, golden="decode4_32k", scale=LLAMA_SCALE, in_dtype="e4m3",
+                                       page_size=16, page_layout="HND"),
+    "decode32k_e4m3_paged64": dict(kind="decode", prog="llama", B=64, Hq=32, Hkv=8, N=1, M=32768, D=128,
+                                   causal=False, golden="decode4_32k", scale=LLAMA_SCALE, in_dtype="e4m3",
+                                   page_size=64),
     "decode128k": dict(kind="decode", prog="llama", B=64, Hq=32, Hkv=8, N=1, M=131072, D=128, causal=False,
                        golden="decode4_128k", scale=LLAMA_SCALE, no_e2e=True),
     # the same decode over a paged KV cache (16-token pages, shuffled block table)
@@ -555,7 +561,7 @@ def run_ours(args, cfg, rank, world, dist):
     clocks = clk.summary()
 
     # ---------------- e2e through the public API (pinned host in, host out)
-    e2e = None if cfg.get("no_e2e") else measure_e2e(args, cfg, w, plan, o, mod, stream, flush, world, dist,
+    e2e = None if (cfg.get("no_e2e") or args.no_e2e) else measure_e2e(args, cfg, w, plan, o, mod, stream, flush, world, dist,
                                                      total_flops)
     if rank != 0:
         return
@@ -702,6 +708,7 @@ def main():
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (A/B runs)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--item-rows", type=int, default=0, choices=[0, 128, 256],
                     help="K1 query rows per work item (0 = library choice)")

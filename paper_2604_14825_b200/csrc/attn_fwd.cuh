@@ -462,7 +462,13 @@ __global__ void __launch_bounds__(attn_threads<NQ>(), NQ == 2 ? 1 : 2)
           item_ring[slot_i] = w;
           mbar_arrive(&bar_item_full[slot_i]);
           if (li < 15) NT_STAMP(3, 48 + li, 1);  // trace: item li published
-          if (w >= p.n_items) break;
+          if (w >= p.n_items) {
+#ifdef NT_TRACE
+            if (g_nt_cta_times)  // units << 32 | KV steps this CTA ran
+              g_nt_cta_times[blockIdx.x * 3 + 2] = ((unsigned long long)li << 32) | (unsigned)(kv_base >> 1);
+#endif
+            break;
+          }
           const AttnItem itm = attn_unit<MASK, SPLIT, ROWS>(p, unit_prefix, w);
           // Q_t of this item may only land once the previous item's last S_t is
           // done; K(0) goes first, into the ring, so it is resident when Q is

@@ -10,7 +10,7 @@ ap.add_argument("--d", type=int, default=128); ap.add_argument("--b", type=int, 
 ap.add_argument("--hq", type=int, default=32); ap.add_argument("--hkv", type=int, default=8)
 a = ap.parse_args()
 L = _lib.lib(); L.nt_debug_set_cta_times.argtypes = [ctypes.c_void_p]
-buf = torch.zeros(2 * 148 * 3, dtype=torch.int64, device="cuda")
+buf = torch.zeros(2 * 148 * 3, dtype=torch.int64, device="cuda")  # [cta][entry, exit, units << 32 | steps]
 q = torch.randn(a.b, a.hq, a.n, a.d, device="cuda").bfloat16(); k = torch.randn(a.b, a.hkv, a.n, a.d, device="cuda").bfloat16()
 v = torch.randn(a.b, a.hkv, a.n, a.d, device="cuda").bfloat16(); o = torch.empty(a.b, a.hq, a.n, a.d, device="cuda").bfloat16()
 plan = AttentionPlan(q, k, v, o, a.d ** -0.5, "causal" if a.causal else "none")
@@ -29,3 +29,15 @@ print(f"event {e0.elapsed_time(e1)*1e3:.1f} us; CTAs {len(t)}; start spread {sta
 import numpy as np
 e = np.sort(end)
 print("end-time deciles (us):", " ".join(f"{x:.1f}" for x in np.percentile(e, [0, 10, 25, 50, 75, 90, 100])))
+units = t[:, 2] >> 32
+steps = t[:, 2] & 0xffffffff
+dur = (t[:, 1] - t[:, 0]) / 1e3
+ok = steps > 0
+print(f"units per CTA: min {units.min()} max {units.max()} total {units.sum()}; steps per CTA: min {steps.min()} "
+      f"median {int(np.median(steps))} max {steps.max()} total {steps.sum()}")
+print(f"us per step (CTA duration / steps): median {np.median(dur[ok] / steps[ok]):.3f} "
+      f"min {np.min(dur[ok] / steps[ok]):.3f} max {np.max(dur[ok] / steps[ok]):.3f}; "
+      f"fixed cost fit (dur = a + b*steps): ", end="")
+A = np.vstack([np.ones(ok.sum()), steps[ok], units[ok]]).T
+coef = np.linalg.lstsq(A, dur[ok], rcond=None)[0]
+print(f"a {coef[0]:.2f} us, b {coef[1]:.3f} us/step, c {coef[2]:.2f} us/unit")
