@@ -31,6 +31,11 @@ constexpr int kDtcTileBytes = kDtcTile * kDecodeD * 2;   // 32 KB, two 64-dim SW
 constexpr int kDtcHalf = kDtcTile * 128;                 // one panel (16 KB)
 constexpr int kDtcStages = 3;                            // K+V tile pairs in flight (192 KB)
 constexpr int kDtcThreads = 128;
+#ifdef NT_DTC_LOADONLY
+constexpr bool kDtcLoadOnly = true;
+#else
+constexpr bool kDtcLoadOnly = false;
+#endif
 constexpr int kDtcSmem = kDtcTileBytes /* Q */ + kDtcStages * 2 * kDtcTileBytes + 1024 /* align */ + 256;
 // e4m3 K/V (FP8 KV cache): a 128-key tile is one 128-byte panel (16 KB), so twice
 // the stages fit -- the same 192 KB in flight
@@ -189,7 +194,17 @@ __global__ void __launch_bounds__(kDtcThreads, 1)
     }
   } else if (warp == 2) {
     // ================= MMA issuer
+#ifdef NT_DTC_LOADONLY
+    // experiment (tools/decode_time.py): the producer's stream alone, slots released as they land
+    if (lane == 0)
+      for (int it = 0; it < 2 * ntiles; ++it) {
+        mbar_wait(&full[it % (2 * kStages)], (it / (2 * kStages)) & 1, p.err, 3);
+        mbar_arrive(&empty[it % (2 * kStages)]);
+      }
+    if (false) {
+#else
     if (lane == 0 && ntiles > 0) {
+#endif
       constexpr uint32_t idS = FP8 ? idesc_e4m3(128, 128, 0, 0) : idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t idO = FP8 ? idesc_e4m3(128, D, 0, 1) : idesc_bf16(128, D, 0, 1);
       const uint32_t sQa = smem_u32(sQ), sKVa = smem_u32(sKV);
@@ -229,7 +244,7 @@ __global__ void __launch_bounds__(kDtcThreads, 1)
         umma_commit(&empty[slotV]);
       }
     }
-  } else if (warp == 0) {
+  } else if (warp == 0 && !kDtcLoadOnly) {
     // ================= softmax: two threads per query row (R <= 8 rows live in
     // TMEM lanes 0-15): thread t holds row t % 16, keys (t / 16) * 64 + [0, 64)
     // of each tile, through the .16x32bx2 fragment -- half the exps per thread
