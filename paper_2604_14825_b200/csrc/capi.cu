@@ -7,6 +7,8 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <queue>
+#include <vector>
 #include <string>
 
 #include "../../include/nautilus_b200.h"
@@ -202,7 +204,40 @@ static AttnSplit attn_split_plan(const nt_attn_args* a) {
   static const double div = getenv("NT_ATTN_SPLIT_DIV") ? atof(getenv("NT_ATTN_SPLIT_DIV")) : 0.9;
   if (mx <= thresh * avg) return sp;
   // >= 4 tiles per unit; <= 32 units per item (the combine holds one chunk per lane)
-  const int S = std::max(std::max(4, (int)std::ceil(avg / div)), (mx + 31) / 32);
+  const int s_min = std::max(4, (mx + 31) / 32);
+  int S = std::max((int)std::ceil(avg / div), s_min);
+  if (!getenv("NT_ATTN_SPLIT_DIV")) {
+    // pick the chunk size whose greedy schedule (the device work counter hands the
+    // units out in LPT order to whichever CTA frees first) has the shortest makespan,
+    // each unit charged one extra step for its Q load, partial store and refill:
+    // one kv-group of Llama 8K, 148 CTAs -- S = 32 (the 0.9 rule) 33 steps, S = 30 32
+    const int ctas = num_sms() * (rows == 128 ? 2 : 1);
+    auto makespan = [&](int s) {
+      std::priority_queue<double, std::vector<double>, std::greater<double>> free_at;
+      for (int c = 0; c < ctas; ++c) free_at.push(0.0);
+      double end = 0.0;
+      for (int i = 0; i < nmb; ++i) {
+        const int n = nkv(a->mask_kind == NT_MASK_CAUSAL ? nmb - 1 - i : i);
+        const int nc = n > s ? (n + s - 1) / s : 1;
+        for (int c = 0; c < nc; ++c)
+          for (long long bh = 0; bh < BH; ++bh) {
+            const double t = free_at.top() + std::min(s, n - c * s) + 1.0;
+            free_at.pop();
+            free_at.push(t);
+            end = std::max(end, t);
+          }
+      }
+      return end;
+    };
+    double best = 1e30;
+    for (int s = std::max(s_min, (int)(0.8 * avg)); s <= std::max(s_min, (int)std::ceil(1.3 * avg)); ++s) {
+      const double m = makespan(s);
+      if (m < best - 1e-9) {
+        best = m;
+        S = s;
+      }
+    }
+  }
   if (S >= mx) return sp;
   long long units = 0;
   for (int mb = 0; mb < nmb; ++mb) {

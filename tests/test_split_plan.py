@@ -37,6 +37,21 @@ def _nkv(mb, N, M, causal, off=0, rows=256):
     return max(min(total, last_q // 128 + 1), 1)
 
 
+def _makespan(nk_lpt, BH, s, ctas):
+    """Greedy schedule of the units (LPT order) over `ctas` CTAs, one extra step per unit."""
+    import heapq
+    free = [0.0] * ctas
+    end = 0.0
+    for n in nk_lpt:
+        nc = (n + s - 1) // s if n > s else 1
+        for c in range(nc):
+            for _ in range(BH):
+                t = heapq.heappop(free) + min(s, n - c * s) + 1.0
+                heapq.heappush(free, t)
+                end = max(end, t)
+    return end
+
+
 def _plan(B, Hq, N, M, D, causal):
     """Restatement of attn_split_plan: (kv_split, n_units, workspace bytes)."""
     rows = _rows(B, Hq, N)
@@ -48,7 +63,14 @@ def _plan(B, Hq, N, M, D, causal):
     mx = max(nk)
     if nmb > 384 or mx <= 2.0 * avg:
         return 0, nmb * BH, 0
-    S = max(max(4, math.ceil(avg / 0.9)), (mx + 31) // 32)
+    s_min = max(4, (mx + 31) // 32)
+    S = max(math.ceil(avg / 0.9), s_min)
+    ctas = SMS * (2 if rows == 128 else 1)
+    best = None
+    for s in range(max(s_min, int(0.8 * avg)), max(s_min, math.ceil(1.3 * avg)) + 1):
+        m = _makespan(nk[::-1] if causal else nk, BH, s, ctas)
+        if best is None or m < best - 1e-9:
+            best, S = m, s
     if S >= mx:
         return 0, nmb * BH, 0
     units = sum((n + S - 1) // S for n in nk) * BH
