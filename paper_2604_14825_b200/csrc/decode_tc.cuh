@@ -148,6 +148,11 @@ __global__ void __launch_bounds__(kDtcThreads, 1)
           for (int it = 0; it < 2 * ntiles; ++it) {
             const int slot = it % (2 * kStages);
             mbar_wait(&empty[slot], ((it / (2 * kStages)) & 1) ^ 1, p.err, 1);
+#ifdef NT_DTC_COMPUTEONLY
+            // experiment (tools/decode_time.py): the consumers alone, on whatever the ring holds
+            mbar_arrive(&full[slot]);
+            continue;
+#endif
             mbar_arrive_expect_tx(&full[slot], kTile);
             if constexpr (FP8)  // one 4-D box {128 e4m3 dims, 128 keys} = one 128-byte panel
               tma_load_4d(sKV + slot * kTile, (it & 1) ? &tmV : &tmK, &full[slot], 0, j0 + (it >> 1) * kDtcTile,
