@@ -132,6 +132,35 @@ def k2():
         plan.launch()
         torch.cuda.synchronize()
         close(o.cpu().numpy(), ref, what=f"k2 paged {ps} {layout}")
+    # FP8 (e4m3) cache, dense and 32-token pages, checked against fp64 of the dequantised inputs
+    def q8(x):
+        t = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32))
+        d = float(t.abs().max()) / 448.0
+        t8 = (t / d).to(torch.float8_e4m3fn)
+        return t8, d, (t8.float() * d).double().numpy()
+    (q8_, qd, qf), (k8_, kd, kf), (v8_, vd, vf) = q8(q), q8(k), q8(v)
+    ref8 = reference_math.attention_batched_fp64(qf, kf, vf, 1 / np.sqrt(D), False)
+    o8 = nan_filled((B, Hq, 1, D), dtype=torch.float32, device=DEV)
+    kw = dict(q_descale=qd, k_descale=kd, v_descale=vd)
+    DecodePlan(q8_.to(DEV), k8_.to(DEV), v8_.to(DEV), o8, 1 / np.sqrt(D), num_splits=3, **kw).launch()
+    torch.cuda.synchronize()
+    close(o8.cpu().numpy(), ref8, tol=8e-2, what="k2 e4m3 dense")
+    ps = 32
+    npp = -(-M // ps)
+    kp8 = torch.zeros((B * npp, ps, Hkv, D), dtype=torch.uint8, device=DEV)
+    vp8 = torch.zeros_like(kp8)
+    for b in range(B):
+        for j in range(npp):
+            lo, hi = j * ps, min(M, (j + 1) * ps)
+            kp8[b * npp + j, : hi - lo] = k8_[b, :, lo:hi].view(torch.uint8).to(DEV).transpose(0, 1)
+            vp8[b * npp + j, : hi - lo] = v8_[b, :, lo:hi].view(torch.uint8).to(DEV).transpose(0, 1)
+    bt = torch.arange(B * npp, dtype=torch.int32, device=DEV).reshape(B, npp)
+    o8.fill_(float("nan"))
+    PagedDecodePlan(q8_.to(DEV), kp8.view(torch.float8_e4m3fn), vp8.view(torch.float8_e4m3fn), bt,
+                    torch.full((B,), M, dtype=torch.int32, device=DEV), o8, 1 / np.sqrt(D), max_seq_kv=M,
+                    **kw).launch()
+    torch.cuda.synchronize()
+    close(o8.cpu().numpy(), ref8, tol=8e-2, what="k2 e4m3 paged 32")
 
 
 def k3():
