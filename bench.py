@@ -44,6 +44,8 @@ CONFIGS = {
                            golden="causal8k", scale=LLAMA_SCALE),
     "llama2k_causal": dict(prog="llama_causal", B=1, Hq=32, Hkv=8, N=2048, D=128, causal=True,
                            golden="causal2k", scale=LLAMA_SCALE),
+    "llama4k_causal": dict(prog="llama_causal", B=1, Hq=32, Hkv=8, N=4096, D=128, causal=True,
+                           golden="causal4k", scale=LLAMA_SCALE),
     "llama16k_causal": dict(prog="llama_causal", B=1, Hq=32, Hkv=8, N=16384, D=128, causal=True,
                             golden="causal16k", scale=LLAMA_SCALE),
     # one GPU's share at 8 GPUs (batch x head sharding: one kv-group, 4 q-heads): few,
@@ -81,6 +83,8 @@ CONFIGS = {
     "decode32k_e4m3_paged64": dict(kind="decode", prog="llama", B=64, Hq=32, Hkv=8, N=1, M=32768, D=128,
                                    causal=False, golden="decode4_32k", scale=LLAMA_SCALE, in_dtype="e4m3",
                                    page_size=64),
+    "decode64k": dict(kind="decode", prog="llama", B=64, Hq=32, Hkv=8, N=1, M=65536, D=128, causal=False,
+                      golden="decode4_64k", scale=LLAMA_SCALE),
     "decode128k": dict(kind="decode", prog="llama", B=64, Hq=32, Hkv=8, N=1, M=131072, D=128, causal=False,
                        golden="decode4_128k", scale=LLAMA_SCALE, no_e2e=True),
     # the same decode over a paged KV cache (16-token pages, shuffled block table)

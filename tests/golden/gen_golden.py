@@ -83,6 +83,7 @@ CASES = [
     dict(name="decode4", prog="llama", bind=dict(N=4, M=2048, D=128), seeds=[0], io=True),
     dict(name="decode1", prog="llama", bind=dict(N=1, M=1024, D=128), seeds=[0], io=True),
     dict(name="decode4_32k", prog="llama", bind=dict(N=4, M=32768, D=128), seeds=[0], io=False),
+    dict(name="decode4_64k", prog="llama", bind=dict(N=4, M=65536, D=128), seeds=[0], io=False),
     dict(name="decode4_128k", prog="llama", bind=dict(N=4, M=131072, D=128), seeds=[0], io=False),
     dict(name="gemm_v6", prog="gemm2", bind=dict(N=256, K=256, F=512, E=128), seeds=[0], io=True,
          scales={"W1": 1 / 16.0, "W2": 1 / math.sqrt(512)}),
@@ -133,8 +134,13 @@ def b200_context():
 
 
 def main():
-    manifest = {}
+    # `gen_golden.py NAME ...` regenerates only those cases (merged into the manifest)
+    only = set(sys.argv[1:])
+    mpath = os.path.join(HERE, "manifest.json")
+    manifest = json.load(open(mpath)) if only and os.path.exists(mpath) else {}
     for case in CASES:
+        if only and case["name"] not in only:
+            continue
         name = case["name"]
         src = PROGRAMS[case["prog"]]
         device, opts = DEFAULT_DEVICE, SchedulerOptions()

@@ -6,7 +6,7 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gp
 timeout 1500 python -m pytest tests -m gpu -q --timeout 300 > gpurun_out/round/pytest_gpu.log 2>&1; echo pytest=$?
 tail -3 gpurun_out/round/pytest_gpu.log
 timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/round/smoke.log 2>&1; echo smoke=$?
-for c in llama8k_causal llama2k_causal llama16k_causal llama8k_causal_1group llama8k_causal_e4m3 llama4k_mask_bits llama4k_mask_f32 bert512 attn256 decode32k decode32k_paged16 decode32k_paged16_hnd decode32k_paged64 decode32k_e4m3 decode32k_e4m3_paged16 decode32k_e4m3_paged64 decode128k gemm_chain_e4096 gemm_chain_e128; do
+for c in llama8k_causal llama2k_causal llama4k_causal llama16k_causal llama8k_causal_1group llama8k_causal_e4m3 llama4k_mask_bits llama4k_mask_f32 bert512 attn256 decode32k decode32k_paged16 decode32k_paged16_hnd decode32k_paged64 decode32k_e4m3 decode32k_e4m3_paged16 decode32k_e4m3_paged64 decode64k decode128k gemm_chain_e4096 gemm_chain_e128; do
   timeout 600 python bench.py --config $c --steps 10 --warmup 3 > gpurun_out/round/bench_$c.json.log 2>&1; echo bench_$c=$?
 done
 timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/round/bench_reference.json.log 2>&1; echo ref=$?
