@@ -472,8 +472,12 @@ extern "C" int nt_cast_bf16_to_f32(const void* src, float* dst, int64_t n, void*
 
 #ifdef NT_TRACE
 // debug builds only: route the K1 pipeline timeline stamps of one CTA into `buf`
+namespace nt {
+void trace_set_decode(unsigned long long* buf, int cta);
+}
 extern "C" int nt_debug_set_trace(unsigned long long* buf, int cta, int item) {
   for (auto f : {trace_set_d64, trace_set_d128, trace_set_e4m3}) f(buf, cta, item, nullptr, 0);
+  nt::trace_set_decode(buf, cta);
   return check_cuda(cudaGetLastError(), "nt_debug_set_trace");
 }
 extern "C" int nt_debug_set_cta_times(unsigned long long* buf) {

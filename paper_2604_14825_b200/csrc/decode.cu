@@ -110,6 +110,16 @@ int make_q_map(CUtensorMap* mq, const nt_tensor4& q, int B, int Hq, int Nq, int 
 }
 }  // namespace
 
+#ifdef NT_TRACE
+namespace nt {
+// debug builds: this TU's copy of the trace symbols (attn_fwd.cuh) for the K2b timeline
+void trace_set_decode(unsigned long long* buf, int cta) {
+  cudaMemcpyToSymbol(g_nt_trace, &buf, sizeof(buf));
+  cudaMemcpyToSymbol(g_nt_trace_cta, &cta, sizeof(cta));
+}
+}  // namespace nt
+#endif
+
 extern "C" int64_t nt_decode_workspace_bytes(int32_t batch, int32_t heads_kv, int32_t rows_per_group,
                                              int32_t head_dim, int32_t num_splits) {
   return (int64_t)batch * heads_kv * num_splits * rows_per_group * (head_dim + 2) * (int64_t)sizeof(float);

@@ -105,6 +105,15 @@ __global__ void __launch_bounds__(kDtcThreads, 1)
   const int seq_len = PG ? min(p.M, p.seq_lens[b]) : p.M;
   const int j1 = min(seq_len, j0 + p.keys_per_split);
   const int ntiles = (j1 > j0) ? (j1 - j0 + kDtcTile - 1) / kDtcTile : 0;
+#ifdef NT_TRACE
+  // debug timeline (tools/trace_decode.py): clock64 per tile for split g_nt_trace_cta of group 0
+  unsigned long long* const tr =
+      (g_nt_trace && blockIdx.x == g_nt_trace_cta && blockIdx.y == 0) ? g_nt_trace : nullptr;
+#define DTC_STAMP(role, t, ev) \
+  do { if (tr && (t) < 64) tr[((role) * 64 + (t)) * 8 + (ev)] = clock64(); } while (0)
+#else
+#define DTC_STAMP(role, t, ev) do {} while (0)
+#endif
 
   // rows >= R of the padded Q tile are zero (S, P, O rows >= R are never read)
   for (int i = threadIdx.x; i < kTile / 16; i += kDtcThreads)
@@ -154,6 +163,7 @@ __global__ void __launch_bounds__(kDtcThreads, 1)
             continue;
 #endif
             mbar_arrive_expect_tx(&full[slot], kTile);
+            DTC_STAMP(3, it >> 1, it & 1);
             if constexpr (FP8)  // one 4-D box {128 e4m3 dims, 128 keys} = one 128-byte panel
               tma_load_4d(sKV + slot * kTile, (it & 1) ? &tmV : &tmK, &full[slot], 0, j0 + (it >> 1) * kDtcTile,
                           hkv, b);
@@ -229,6 +239,7 @@ __global__ void __launch_bounds__(kDtcThreads, 1)
         }
         umma_commit(&bar_s[t & 1]);
         umma_commit(&empty[slotK]);
+        DTC_STAMP(0, t, 0);
       };
       issue_s(0);
       for (int t = 0; t < ntiles; ++t) {
@@ -236,6 +247,7 @@ __global__ void __launch_bounds__(kDtcThreads, 1)
         // PV(t): P from its own TMEM columns, V MN-major from shared memory
         const int gv = 2 * t + 1, slotV = gv % (2 * kStages);
         mbar_wait(bar_p, t & 1, p.err, 4);
+        DTC_STAMP(0, t, 1);
         mbar_wait(&full[slotV], (gv / (2 * kStages)) & 1, p.err, 5);
         tc_fence_after();
 #pragma unroll
@@ -247,6 +259,7 @@ __global__ void __launch_bounds__(kDtcThreads, 1)
         }
         umma_commit(bar_pv);
         umma_commit(&empty[slotV]);
+        DTC_STAMP(0, t, 2);
       }
     }
   } else if (warp == 0 && !kDtcLoadOnly) {
@@ -261,6 +274,7 @@ __global__ void __launch_bounds__(kDtcThreads, 1)
     float m_run = NINF, l_run = 0.f;
     for (int t = 0; t < ntiles; ++t) {
       mbar_wait(&bar_s[t & 1], (t >> 1) & 1, p.err, 8);
+      if (lane == 0) DTC_STAMP(1, t, 0);
       tc_fence_after();
       uint32_t sv[64];
       tmem_ld32_x2<64>(tmem + (t & 1) * 128, sv);
@@ -269,6 +283,7 @@ __global__ void __launch_bounds__(kDtcThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_sf[t & 1]);  // S_{t%2} may take S(t+2)
+      if (lane == 0) DTC_STAMP(1, t, 1);
       const int kv0 = j0 + t * kDtcTile + half * 64;
       if (kv0 + 64 > j1) {
 #pragma unroll
@@ -295,9 +310,11 @@ __global__ void __launch_bounds__(kDtcThreads, 1)
       const float m_use = (m_run == NINF) ? 0.f : m_run;
       uint32_t pk[32];
       l_run += dtc_exp_pass<FP8>(sv, sc, m_use, pk);  // exps into registers (this half's l)
+      if (lane == 0) DTC_STAMP(1, t, 2);
       if (t > 0) {
         // PV(t-1) read P(t-1) and wrote O: now P(t) may overwrite it and O be rescaled
         mbar_wait(bar_pv, (t - 1) & 1, p.err, 10);
+        if (lane == 0) DTC_STAMP(1, t, 3);
         tc_fence_after();
         // 32x32b: lane t's row; lanes 16-31 are rows past R (nothing reads them)
         if (rescale) attn_rescale_o<D>(tO, alpha);
@@ -312,6 +329,7 @@ __global__ void __launch_bounds__(kDtcThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_p);
+      if (lane == 0) DTC_STAMP(1, t, 4);
     }
     l_run += __shfl_xor_sync(0xffffffffu, l_run, 16);  // both halves' sums (same m_run)
     // ---- epilogue: rows < R -> partial (O unnormalised, m, l) in the workspace
