@@ -39,13 +39,13 @@ torch.cuda.synchronize()
 L.nt_debug_set_trace(None, a.cta, 0)
 t = buf.view(4, 64, 8).cpu().numpy()
 base = t[t > 0].min()
-print("tile | MMA: S_iss P_seen PV_iss | SMX: S_seen S_ld exps PVw P_st | PROD: K V   (clk from first stamp)")
+print("tile | MMA: S_iss P_seen PV_iss Sfull Ssf Smma PVfull PVmma | SMX: S_seen S_ld exps PVw P_st | PROD: K V")
 for i in range(0, 64):
     m, sm, pr = t[0, i], t[1, i], t[3, i]
     if not (m > 0).any():
         continue
     f = lambda r, n: " ".join(f"{int(x - base):7d}" if x > 0 else "      -" for x in r[:n])  # noqa: E731
-    print(f"{i:4d} | {f(m, 3)} | {f(sm, 5)} | {f(pr, 2)}")
+    print(f"{i:4d} | {f(m, 8)} | {f(sm, 5)} | {f(pr, 2)}")
 per = [int(t[1, i + 1, 4] - t[1, i, 4]) for i in range(8, 40) if t[1, i, 4] > 0 and t[1, i + 1, 4] > 0]
 if per:
     print("softmax P-store period (tiles 8-40): median", sorted(per)[len(per) // 2], "clk")
