@@ -78,7 +78,7 @@ template <int R, int PG, bool FP8>
 int launch_tc(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, DecodeParams& p, cudaStream_t st) {
   int rc;
   constexpr auto kern = decode_tc_kernel<R, PG, FP8>;
-  constexpr int smem = DtcCfg<FP8>::SMEM;
+  constexpr int smem = DtcCfg<FP8, PG>::SMEM;
   if ((rc = configure_smem<kern>(smem, "cudaFuncSetAttribute(decode_tc)"))) return rc;
   dim3 grid(p.splits, p.B * p.Hkv);
   kern<<<grid, kDtcThreads, smem, st>>>(mq, mk, mv, p);
@@ -173,12 +173,14 @@ extern "C" int nt_attn_decode(const nt_decode_args* a, void* stream) {
     p.keys_per_split = ((a->seq_kv + p.splits - 1) / p.splits + kDtcTile - 1) / kDtcTile * kDtcTile;
     CUtensorMap mq;
     if ((rc = make_q_map(&mq, a->q, a->batch, a->heads_q, a->seq_q, g, fp8 ? 1 : 2))) return rc;
-    if (fp8) {  // one 128-byte panel per key: box {128 dims, 128 keys, 1, 1}
+    if (fp8) {  // one 128-byte panel per key: box {128 dims, KPS keys, 1, 1}
+      constexpr int kps = DtcCfg<true, 0>::KPS;
+      p.keys_per_split = ((a->seq_kv + p.splits - 1) / p.splits + kps - 1) / kps * kps;
       if ((rc = make_map_4d(&mk, a->k.ptr, kDecodeD, a->seq_kv, a->heads_kv, a->batch, a->k.stride_s, a->k.stride_h,
-                            a->k.stride_b, kDtcTile, 1, 0, CU_TENSOR_MAP_SWIZZLE_128B)))
+                            a->k.stride_b, kps, 1, 0, CU_TENSOR_MAP_SWIZZLE_128B)))
         return rc;
       if ((rc = make_map_4d(&mv, a->v.ptr, kDecodeD, a->seq_kv, a->heads_kv, a->batch, a->v.stride_s, a->v.stride_h,
-                            a->v.stride_b, kDtcTile, 1, 0, CU_TENSOR_MAP_SWIZZLE_128B)))
+                            a->v.stride_b, kps, 1, 0, CU_TENSOR_MAP_SWIZZLE_128B)))
         return rc;
       return dispatch_tc<0, true>(R, mq, mk, mv, p, st);
     }

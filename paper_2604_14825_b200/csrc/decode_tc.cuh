@@ -50,10 +50,21 @@ constexpr bool kDtcLoadOnly = false;
 constexpr int kDtcSmem = kDtcTileBytes /* Q */ + kDtcStages * 2 * kDtcTileBytes + 1024 /* align */ + 256;
 // e4m3 K/V (FP8 KV cache): a 128-key tile is one 128-byte panel (16 KB), so twice
 // the stages fit -- the same 192 KB in flight
-template <bool FP8>
+// NT_DTC_E4M3_KPS = 256 moves 256 keys per dense e4m3 ring slot (one 32 KB box: the
+// producer alone reads 6.80 TB/s in 16 KB boxes and 7.07 in 32 KB ones; the MMAs and
+// the softmax still step in 128-key tiles, SUB per slot).  Measured with the full
+// kernel (same box): decode 32K 644 -> 648 us, B=16 8K 89 -> 85 us -- a slot is held
+// until both its tiles are consumed, so fewer bytes are in flight; 128 stays default.
+#ifndef NT_DTC_E4M3_KPS
+#define NT_DTC_E4M3_KPS 128
+#endif
+template <bool FP8, int PG = 0>
 struct DtcCfg {
-  static constexpr int TILE = kDtcTile * kDecodeD * (FP8 ? 1 : 2);
-  static constexpr int STAGES = FP8 ? 6 : kDtcStages;
+  static constexpr int KPS = (FP8 && PG == 0) ? NT_DTC_E4M3_KPS : kDtcTile;  // keys per ring slot
+  static constexpr int SUB = KPS / kDtcTile;                                 // 128-key tiles per slot
+  static constexpr int TILE = KPS * kDecodeD * (FP8 ? 1 : 2);                // bytes per slot
+  static constexpr int SUBBYTES = kDtcTile * kDecodeD * (FP8 ? 1 : 2);
+  static constexpr int STAGES = (kDtcStages * 2 * kDtcTileBytes) / (2 * TILE);  // 192 KB in flight
   static constexpr int KSTEP = FP8 ? 32 : 16;  // K per tcgen05.mma (kind::f8f6f4 | kind::f16)
   static constexpr int SMEM = kDtcQBytes + STAGES * 2 * TILE + 1024 + 512 + kDtcMergeBytes;  // + align, barriers
 };
@@ -90,8 +101,8 @@ __global__ void __launch_bounds__(kDtcThreads, 1)
     decode_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                      const __grid_constant__ CUtensorMap tmV, const DecodeParams p) {
   constexpr int D = kDecodeD;
-  using DC = DtcCfg<FP8>;
-  constexpr int kTile = DC::TILE, kStages = DC::STAGES;
+  using DC = DtcCfg<FP8, PG>;
+  constexpr int kTile = DC::TILE, kStages = DC::STAGES, kSub = DC::SUB;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_u32 = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_u32 + 1023u) & ~1023u) - raw_u32);
@@ -117,6 +128,7 @@ __global__ void __launch_bounds__(kDtcThreads, 1)
   const int seq_len = PG ? min(p.M, p.seq_lens[b]) : p.M;
   const int j1 = min(seq_len, j0 + p.keys_per_split);
   const int ntiles = (j1 > j0) ? (j1 - j0 + kDtcTile - 1) / kDtcTile : 0;
+  const int nslots = (ntiles + kSub - 1) / kSub;  // K (and V) ring slots the split uses
 #ifdef NT_TRACE
   // debug timeline (tools/trace_decode.py): clock64 per tile for split g_nt_trace_cta of group 0
   unsigned long long* const tr =
@@ -168,7 +180,7 @@ __global__ void __launch_bounds__(kDtcThreads, 1)
       }
       if constexpr (PG == 0) {
         if (lane == 0)
-          for (int it = 0; it < 2 * ntiles; ++it) {
+          for (int it = 0; it < 2 * nslots; ++it) {
             const int slot = it % (2 * kStages);
             mbar_wait(&empty[slot], ((it / (2 * kStages)) & 1) ^ 1, p.err, 1);
 #ifdef NT_DTC_COMPUTEONLY
@@ -178,11 +190,11 @@ __global__ void __launch_bounds__(kDtcThreads, 1)
 #endif
             mbar_arrive_expect_tx(&full[slot], kTile);
             DTC_STAMP(3, it >> 1, it & 1);
-            if constexpr (FP8)  // one 4-D box {128 e4m3 dims, 128 keys} = one 128-byte panel
-              tma_load_4d(sKV + slot * kTile, (it & 1) ? &tmV : &tmK, &full[slot], 0, j0 + (it >> 1) * kDtcTile,
+            if constexpr (FP8)  // one 4-D box {128 e4m3 dims, KPS keys} = one 128-byte panel
+              tma_load_4d(sKV + slot * kTile, (it & 1) ? &tmV : &tmK, &full[slot], 0, j0 + (it >> 1) * DC::KPS,
                           hkv, b);
             else  // one 5-D box {64 dims, 128 keys, 2 panels} = [panel][128 keys][128 B]
-              tma_load_5d(sKV + slot * kTile, (it & 1) ? &tmV : &tmK, &full[slot], 0, j0 + (it >> 1) * kDtcTile,
+              tma_load_5d(sKV + slot * kTile, (it & 1) ? &tmV : &tmK, &full[slot], 0, j0 + (it >> 1) * DC::KPS,
                           0, hkv, b);
           }
       } else {
@@ -231,7 +243,7 @@ __global__ void __launch_bounds__(kDtcThreads, 1)
 #ifdef NT_DTC_LOADONLY
     // experiment (tools/decode_time.py): the producer's stream alone, slots released as they land
     if (lane == 0 && warp == 2)
-      for (int it = 0; it < 2 * ntiles; ++it) {
+      for (int it = 0; it < 2 * nslots; ++it) {
         mbar_wait(&full[it % (2 * kStages)], (it / (2 * kStages)) & 1, p.err, 3);
         mbar_arrive(&empty[it % (2 * kStages)]);
       }
@@ -242,8 +254,12 @@ __global__ void __launch_bounds__(kDtcThreads, 1)
       constexpr uint32_t idS = FP8 ? idesc_e4m3(128, 128, 0, 0) : idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t idO = FP8 ? idesc_e4m3(128, D, 0, 1) : idesc_bf16(128, D, 0, 1);
       const uint32_t sQa = smem_u32(sQ), sKVa = smem_u32(sKV);
+      // tile t lives in ring slot t / kSub at (t % kSub) x SUBBYTES; a slot is released
+      // by the commit after its last tile's MMAs
+      auto last_of_slot = [&](int t) { return t % kSub == kSub - 1 || t == ntiles - 1; };
       auto issue_s = [&](int t) {
-        const int gk = 2 * t, slotK = gk % (2 * kStages);
+        const int gk = 2 * (t / kSub), slotK = gk % (2 * kStages);
+        const uint32_t so = (t % kSub) * DC::SUBBYTES;
         mbar_wait(&full[slotK], (gk / (2 * kStages)) & 1, p.err, 3);
         DTC_STAMP(0, t, 3);
         if (t >= 2) mbar_wait(&bar_sf[t & 1], ((t >> 1) - 1) & 1, p.err, 6);  // softmax(t-2) read S_{t%2}
@@ -253,13 +269,13 @@ __global__ void __launch_bounds__(kDtcThreads, 1)
         for (int k = 0; k < D / DC::KSTEP; ++k) {
           // 32 bytes of K per instruction, 4 per 128-byte panel row
           const uint64_t ad = sdesc_sw128(sQa + (k >> 2) * 1024 + (k & 3) * 32, 16, 0);  // the Q atom, every row group
-          const uint64_t bd = sdesc_sw128(sKVa + slotK * kTile + (k >> 2) * kDtcHalf + (k & 3) * 32, 16, 1024);
+          const uint64_t bd = sdesc_sw128(sKVa + slotK * kTile + so + (k >> 2) * kDtcHalf + (k & 3) * 32, 16, 1024);
           if constexpr (FP8) umma_ss_f8(tmem + (t & 1) * 128, ad, bd, idS, k > 0 ? 1u : 0u);
           else umma_ss(tmem + (t & 1) * 128, ad, bd, idS, k > 0 ? 1u : 0u);
         }
         DTC_STAMP(0, t, 5);
         umma_commit(&bar_s[t & 1]);
-        umma_commit(&empty[slotK]);
+        if (last_of_slot(t)) umma_commit(&empty[slotK]);
         DTC_STAMP(0, t, 0);
       };
       if (warp == 2) {
@@ -267,7 +283,8 @@ __global__ void __launch_bounds__(kDtcThreads, 1)
         for (int t = 0; t < ntiles; ++t) issue_s(t);
       } else for (int t = 0; t < ntiles; ++t) {
         // PV(t): P from its own TMEM columns, V MN-major from shared memory
-        const int gv = 2 * t + 1, slotV = gv % (2 * kStages);
+        const int gv = 2 * (t / kSub) + 1, slotV = gv % (2 * kStages);
+        const uint32_t so = (t % kSub) * DC::SUBBYTES;
         mbar_wait(&bar_p[t & 1], (t >> 1) & 1, p.err, 4);
         DTC_STAMP(0, t, 1);
         mbar_wait(&full[slotV], (gv / (2 * kStages)) & 1, p.err, 5);
@@ -276,14 +293,14 @@ __global__ void __launch_bounds__(kDtcThreads, 1)
 #pragma unroll
         for (int k = 0; k < kDtcTile / DC::KSTEP; ++k) {
           // KSTEP keys of V (MN-major, 128-byte rows) x P's 8 TMEM columns (bf16 pairs | e4m3 quads)
-          const uint64_t bd = sdesc_sw128(sKVa + slotV * kTile + k * DC::KSTEP * 128, kDtcHalf, 1024);
+          const uint64_t bd = sdesc_sw128(sKVa + slotV * kTile + so + k * DC::KSTEP * 128, kDtcHalf, 1024);
           const uint32_t ta = tmem + kColP + (t & 1) * kPCols + k * 8;
           if constexpr (FP8) umma_ts_f8(tmem + kColO, ta, bd, idO, (t > 0 || k > 0) ? 1u : 0u);
           else umma_ts(tmem + kColO, ta, bd, idO, (t > 0 || k > 0) ? 1u : 0u);
         }
         DTC_STAMP(0, t, 7);
         umma_commit(&bar_pv[t & 1]);
-        umma_commit(&empty[slotV]);
+        if (last_of_slot(t)) umma_commit(&empty[slotV]);
         DTC_STAMP(0, t, 2);
       }
     }
