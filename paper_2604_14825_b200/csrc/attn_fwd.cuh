@@ -112,6 +112,9 @@ constexpr float kRescaleLog2 = 8.0f;
 #define NT_PACK_D128 0
 #endif
 // control warps (producer / MMA issuer) on the highest warp ids
+#ifndef NT_K1_TWO_ISSUERS
+#define NT_K1_TWO_ISSUERS 1
+#endif
 #ifndef NT_ROLES_HIGH
 #define NT_ROLES_HIGH 0  // A/B r02: 8K 447 -> 453 us, 2K 49.4 -> 50.1, BERT 57.1 -> 56.5, 1-group 86.8 -> 85.9: off
 #endif
@@ -374,6 +377,10 @@ __global__ void __launch_bounds__(attn_threads<NQ>(), NQ == 2 ? 1 : 2)
   // MMA issuer is not starved by the softmax warps sharing its SMSP.
   constexpr int kCtl = NT_ROLES_HIGH ? 4 * NQ : 0;   // producer kCtl, MMA kCtl + 1, helper kCtl + 2
   constexpr int kSm0 = NT_ROLES_HIGH ? 0 : 4;        // first softmax warp
+  // MMA-issuing warps: two only where S is computed ahead of the chain (SEP_P, D=64):
+  // with P aliasing S (D=128) each tile's PV+S group sits in its chain, and two issuers
+  // interleave the groups' MMAs so both finish later (8K 447 -> 550 us; BERT 56.8 -> 55.4)
+  constexpr int kIssuers = (NQ == 2 && C::SEP_P && NT_K1_TWO_ISSUERS) ? 2 : 1;
   NT_TRACE_INIT;
   if (threadIdx.x == 0) NT_STAMP(3, 63, 7);  // kernel entry (trace builds)
 #ifdef NT_TRACE
@@ -399,11 +406,11 @@ __global__ void __launch_bounds__(attn_threads<NQ>(), NQ == 2 ? 1 : 2)
     }
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&bar_kv_full[s], 1);
-      mbar_init(&bar_kv_empty[s], 1);
+      mbar_init(&bar_kv_empty[s], kIssuers);
     }
     for (int s = 0; s < kItemRing; ++s) {
       mbar_init(&bar_item_full[s], 1);
-      mbar_init(&bar_item_empty[s], 1 + 4 * NQ);
+      mbar_init(&bar_item_empty[s], kIssuers + 4 * NQ);
     }
     fence_barrier_init();
   }
@@ -502,8 +509,15 @@ __global__ void __launch_bounds__(attn_threads<NQ>(), NQ == 2 ? 1 : 2)
           kv_base += 2 * itm.n_kv;
         }
       }
-    } else if (warp == kCtl + 1) {
-      // ================= MMA issuer
+    } else if (warp == kCtl + 1 || (kIssuers == 2 && warp == kCtl + 3)) {
+      // ================= MMA issuer(s).  An issuing thread blocks on each MMA until the
+      // tensor pipe takes it and spends ~100 clk per mbarrier wait and ~60 per commit
+      // (tools/trace_decode.py, tools/ubench/umma_rate.cu); with kIssuers = 2 each
+      // query tile has its own issuer (warp kCtl + 1: tile 0, kCtl + 3: tile 1), so one
+      // tile's waits and commits overlap the other tile's MMAs.  The tiles only share
+      // K/V ring slots (released by both issuers' commits) and the item ring.
+      const int t_lo = (kIssuers == 2 && warp == kCtl + 3) ? 1 : 0;
+      const int t_hi = kIssuers == 2 ? t_lo + 1 : NQ;
       if (lane == 0) {
         constexpr uint32_t idS = FP8 ? idesc_e4m3(128, 128, 0, 0) : idesc_bf16(128, 128, 0, 0);
         constexpr uint32_t idO = FP8 ? idesc_e4m3(128, D, 0, 1) : idesc_bf16(128, D, 0, 1);
@@ -542,7 +556,7 @@ __global__ void __launch_bounds__(attn_threads<NQ>(), NQ == 2 ? 1 : 2)
         };
         auto wait_q = [&](int li) {
           qb = (li % C::QB) * NQ;
-          for (int t = 0; t < NQ; ++t) mbar_wait(&bar_q[qb + t], (li / C::QB) & 1, p.err, 2);
+          for (int t = t_lo; t < t_hi; ++t) mbar_wait(&bar_q[qb + t], (li / C::QB) & 1, p.err, 2);
           if (li < 15) NT_STAMP(3, 48 + li, 3);  // trace: MMA has Q of item li
         };
         // S_t(0) of an item from its K(0) at ring index g (both tiles)
@@ -550,7 +564,7 @@ __global__ void __launch_bounds__(attn_threads<NQ>(), NQ == 2 ? 1 : 2)
           const int slotK = g % C::STAGES;
           mbar_wait(&bar_kv_full[slotK], (g / C::STAGES) & 1, p.err, 3);
           tc_fence_after();
-          for (int t = 0; t < NQ; ++t) {
+          for (int t = t_lo; t < t_hi; ++t) {
             issue_s(t, slotK);
             umma_commit(&bar_s_full[t]);
             if (n_kv == 1) umma_commit(&bar_q_empty[qb + t]);
@@ -579,7 +593,7 @@ __global__ void __launch_bounds__(attn_threads<NQ>(), NQ == 2 ? 1 : 2)
             tc_fence_after();
             if constexpr (C::SEP_P) {
               // S_t(j) waits only until the softmax warps have read S_t(j-1) out of TMEM
-              for (int t = 0; t < NQ; ++t) {
+              for (int t = t_lo; t < t_hi; ++t) {
                 mbar_wait(&bar_s_free[t], sf_phase[t], p.err, 15);
                 sf_phase[t] ^= 1u;
                 tc_fence_after();
@@ -589,10 +603,10 @@ __global__ void __launch_bounds__(attn_threads<NQ>(), NQ == 2 ? 1 : 2)
                 if (j == n_kv - 1) umma_commit(&bar_q_empty[qb + t]);
               }
               umma_commit(&bar_kv_empty[slotK]);
-              for (int t = 0; t < NQ; ++t) {
+              for (int t = t_lo; t < t_hi; ++t) {
                 mbar_wait(&bar_p_full[t], p_phase[t], p.err, 4);
                 p_phase[t] ^= 1u;
-                if (t == 0) mbar_wait(&bar_kv_full[slotV], (gV / C::STAGES) & 1, p.err, 5);
+                if (t == t_lo) mbar_wait(&bar_kv_full[slotV], (gV / C::STAGES) & 1, p.err, 5);
                 tc_fence_after();
                 if (li == NT_TRACE_LI) NT_STAMP(0, j, 4 + t);
                 issue_pv(t, slotV, j - 1 > 0);
@@ -601,14 +615,14 @@ __global__ void __launch_bounds__(attn_threads<NQ>(), NQ == 2 ? 1 : 2)
               umma_commit(&bar_kv_empty[slotV]);
             } else {
               // P_t(j-1) aliases S_t: PV_t(j-1) then S_t(j), tile 0 then tile 1
-              for (int t = 0; t < NQ; ++t) {
+              for (int t = t_lo; t < t_hi; ++t) {
                 mbar_wait(&bar_p_full[t], p_phase[t], p.err, 4);
                 p_phase[t] ^= 1u;
                 if (li == NT_TRACE_LI) NT_STAMP(0, j, 2 + 2 * t);
-                if (t == 0) mbar_wait(&bar_kv_full[slotV], (gV / C::STAGES) & 1, p.err, 5);
+                if (t == t_lo) mbar_wait(&bar_kv_full[slotV], (gV / C::STAGES) & 1, p.err, 5);
                 tc_fence_after();
                 issue_pv(t, slotV, j - 1 > 0);
-                if (t == NQ - 1) umma_commit(&bar_kv_empty[slotV]);
+                if (t == t_hi - 1) umma_commit(&bar_kv_empty[slotV]);
                 issue_s(t, slotK);
                 umma_commit(&bar_s_full[t]);
                 if (j == n_kv - 1) umma_commit(&bar_q_empty[qb + t]);
@@ -624,7 +638,7 @@ __global__ void __launch_bounds__(attn_threads<NQ>(), NQ == 2 ? 1 : 2)
           const int slotV = gV % C::STAGES;
           const int gKn = kv_base + 2 * n_kv;  // ring index of the next item's K(0)
           if constexpr (C::SEP_P) {
-            for (int t = 0; t < NQ; ++t) {
+            for (int t = t_lo; t < t_hi; ++t) {
               mbar_wait(&bar_s_free[t], sf_phase[t], p.err, 16);
               sf_phase[t] ^= 1u;
             }
@@ -632,10 +646,10 @@ __global__ void __launch_bounds__(attn_threads<NQ>(), NQ == 2 ? 1 : 2)
               wait_q(li + 1);
               first_s(gKn, n_next);
             }
-            for (int t = 0; t < NQ; ++t) {
+            for (int t = t_lo; t < t_hi; ++t) {
               mbar_wait(&bar_p_full[t], p_phase[t], p.err, 6);
               p_phase[t] ^= 1u;
-              if (t == 0) mbar_wait(&bar_kv_full[slotV], (gV / C::STAGES) & 1, p.err, 7);
+              if (t == t_lo) mbar_wait(&bar_kv_full[slotV], (gV / C::STAGES) & 1, p.err, 7);
               tc_fence_after();
               issue_pv(t, slotV, n_kv - 1 > 0);
               umma_commit(&bar_pv_done[t]);
@@ -644,15 +658,15 @@ __global__ void __launch_bounds__(attn_threads<NQ>(), NQ == 2 ? 1 : 2)
             umma_commit(&bar_kv_empty[slotV]);
           } else {
             const int slotKn = gKn % C::STAGES;
-            for (int t = 0; t < NQ; ++t) {
+            for (int t = t_lo; t < t_hi; ++t) {
               mbar_wait(&bar_p_full[t], p_phase[t], p.err, 6);
               p_phase[t] ^= 1u;
-              if (t == 0) mbar_wait(&bar_kv_full[slotV], (gV / C::STAGES) & 1, p.err, 7);
+              if (t == t_lo) mbar_wait(&bar_kv_full[slotV], (gV / C::STAGES) & 1, p.err, 7);
               tc_fence_after();
               issue_pv(t, slotV, n_kv - 1 > 0);
               umma_commit(&bar_o_full[t]);
               if (wn >= 0) {
-                if (t == 0) {
+                if (t == t_lo) {
                   wait_q(li + 1);
                   mbar_wait(&bar_kv_full[slotKn], (gKn / C::STAGES) & 1, p.err, 3);
                   tc_fence_after();
