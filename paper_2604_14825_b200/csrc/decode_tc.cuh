@@ -11,15 +11,17 @@
 //   S(t)  = Q (128 x 128, rows >= R zero) . K(t)^T      SS, 8 x (M128 N128 K16)
 //   O    += P(t) (TMEM, bf16) . V(t)                     TS, 8 x (M128 N128 K16)
 // 1024 tensor clocks per 128-key K/V tile pair (64 KB) against ~2500 clocks of HBM
-// time per SM.  S is double-buffered in TMEM and P has its own columns, so S(t+1)
-// is computed while the softmax warp works on S(t): the per-tile chain is the
-// softmax alone (~1200 clk: one warp, MUFU-bound), not S + softmax + PV (a first
-// version with P aliasing S measured 5.80 TB/s, this chain ~2900 clk per tile).
-//   warp 0  softmax (TMEM lanes 0-31; lane = row, lanes < R matter), epilogue
-//   warp 1  TMA producer: Q once, then K(t), V(t) through a kDtcStages ring
-//   warp 2  MMA issuer (one thread): S(t+1) ahead, PV(t) when P(t) is ready
-//   warp 3  idle
-// TMEM: S_0 [0,128) S_1 [128,256) P [256,320) O [384,512).
+// time per SM (e4m3: kind::f8f6f4, K = 32, 4 + 4 MMAs, 16 KB tiles).  S and P are
+// double-buffered in TMEM, so S(t+1) is computed while the softmax works on S(t)
+// and P(t+1) is stored while PV(t) reads P(t).  An issuing thread blocks on each MMA
+// until the tensor pipe takes it, so S and PV have one issuer each; the exps run on
+// four warps, one per TMEM lane quarter (DESIGN.md §4 K2b, "What bounds the stream"):
+//   warp 1     TMA producer: Q once, then K(t), V(t) through the ring
+//   warp 2     S(t) issuer (one thread)          warp 3  PV(t) issuer (one thread)
+//   warps 4-7  softmax, warp 4 + q on lane quarter q / keys 32 q + [0, 32) of each
+//              tile, an online softmax of its own; the four merged in shared memory
+//   warp 0     idle
+// TMEM: S_0 [0,128) S_1 [128,256) P_0, P_1 [256,384) O [384,512).
 #pragma once
 #include "attn_fwd.cuh"
 #include "decode.cuh"
