@@ -259,14 +259,21 @@ def _attention_streamed(spec: AttentionSpec, inputs: dict, outer, mask_kind, out
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(comp)
     flops, launches, plans = 0.0, 0, []
-    for c in range(n):
-        mine = [p for p in pieces if p[0] == c]
-        with torch.cuda.stream(s_in):
-            for _, b0, b1, h0, h1 in mine:
+    # every chunk's host->device copy is enqueued first, each followed by an event: the
+    # copy engine then runs back to back while the host builds the plans and launches
+    # (enqueueing copy c after launch c-1 starved it: 8 chunks 3.19 ms vs 4 chunks 2.75)
+    landed = []
+    with torch.cuda.stream(s_in):
+        for c in range(n):
+            for _, b0, b1, h0, h1 in (p for p in pieces if p[0] == c):
                 q_d[b0:b1, h0 * g:h1 * g].copy_(q_h[b0:b1, h0 * g:h1 * g], non_blocking=True)
                 k_d[b0:b1, h0:h1].copy_(k_h[b0:b1, h0:h1], non_blocking=True)
                 v_d[b0:b1, h0:h1].copy_(v_h[b0:b1, h0:h1], non_blocking=True)
-        comp.wait_stream(s_in)
+            landed.append(torch.cuda.Event())
+            landed[-1].record(s_in)
+    for c in range(n):
+        mine = [p for p in pieces if p[0] == c]
+        comp.wait_event(landed[c])
         for _, b0, b1, h0, h1 in mine:
             qv, kv, vv = q_d[b0:b1, h0 * g:h1 * g], k_d[b0:b1, h0:h1], v_d[b0:b1, h0:h1]
             if cast:
@@ -330,12 +337,16 @@ def _causal_rows_streamed(spec, q_h, k_h, v_h, o_h, q_d, k_d, v_d, o_d, out, com
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(comp)
     plans, flops, kv_done = [], 0.0, 0
+    landed = []  # all host->device copies first (see _attention_streamed)
     for r0, r1 in zip(bounds[:-1], bounds[1:]):
         copy2d(q_d, q_h, r0, r1, N, B * Hq, esz, s_in)
         copy2d(k_d, k_h, kv_done, r1, N, B * Hkv, esz, s_in)
         copy2d(v_d, v_h, kv_done, r1, N, B * Hkv, esz, s_in)
         kv_done = r1
-        comp.wait_stream(s_in)
+        landed.append(torch.cuda.Event())
+        landed[-1].record(s_in)
+    for c, (r0, r1) in enumerate(zip(bounds[:-1], bounds[1:])):
+        comp.wait_event(landed[c])
         plan = AttentionPlan(q_d[:, :, r0:r1], k_d[:, :, :r1], v_d[:, :, :r1], o_d[:, :, r0:r1], spec.scale,
                              "causal", causal_offset=r0, err_flag=err, kv_stages=spec.stages,
                              item_rows=attn_item_rows(spec.block_m))
