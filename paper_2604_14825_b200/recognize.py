@@ -203,7 +203,7 @@ class AttentionSpec:
     @property
     def gpu_bm(self) -> int:
         """Rows per GPU work item for the single-head MA program (outer grid 1)."""
-        return attn_effective_rows(attn_item_rows(self.block_m), self.n, 1)
+        return attn_effective_rows(attn_item_rows(self.block_m), self.n, 1, d=self.d, m=self.m)
 
     def flops(self, causal: bool = False) -> float:
         """Megatron/FA convention: the two GEMMs only."""
@@ -240,11 +240,15 @@ def attn_item_rows(ma_block_rows: int) -> int:
     return 128 if 0 < ma_block_rows <= 32 else 0
 
 
-def attn_effective_rows(requested: int, n: int, batch_heads: int, sms: int = 148) -> int:
+def attn_effective_rows(requested: int, n: int, batch_heads: int, sms: int = 148, d: int = 128,
+                        m: Optional[int] = None) -> int:
     """The rows nt_attn_fwd uses (csrc/capi.cu attn_item_rows): an explicit 128/256,
-    else 128 when 256-row items would leave more than half of the SMs idle."""
+    else 128 when 256-row items would leave more than half of the SMs idle or at
+    head_dim 64 with <= 1024 keys (short items), else 256."""
     if requested in (128, 256):
         return requested
+    if d == 64 and m is not None and m <= 1024:
+        return 128
     return 128 if -(-n // 256) * batch_heads * 2 < sms else 256
 
 

@@ -108,7 +108,8 @@ class AttentionPlan:
         a.workspace = self.ws.data_ptr() if ws else None
         a.workspace_bytes = ws
         from .recognize import attn_effective_rows
-        self.item_rows = 256 if e4m3 else attn_effective_rows(int(item_rows), N, B * Hq, _lib.num_sms(q.device))
+        self.item_rows = 256 if e4m3 else attn_effective_rows(int(item_rows), N, B * Hq, _lib.num_sms(q.device),
+                                                              d=D, m=M)
         self.kv_slots = attn_kv_slots(64 if e4m3 else D, kv_stages, self.item_rows // 128)  # e4m3: D=64-sized tiles
         self.args = a
         self.shape = (B, Hq, Hkv, N, M, D)

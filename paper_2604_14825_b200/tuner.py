@@ -58,7 +58,7 @@ def realisation_key(spec, outer, mask_kind) -> tuple:
         from .recognize import attn_effective_rows
         from .runtime import attn_item_rows, attn_kv_slots
         bh = outer[0] * outer[1] if outer else 1
-        rows = attn_effective_rows(attn_item_rows(spec.block_m), spec.n, bh)
+        rows = attn_effective_rows(attn_item_rows(spec.block_m), spec.n, bh, d=spec.d, m=spec.m)
         return ("attn", spec.n, spec.m, spec.d, spec.scale, spec.mask is not None, mask_kind, outer,
                 rows, attn_kv_slots(spec.d, spec.stages, rows // 128))
     if isinstance(spec, GemmChainSpec):

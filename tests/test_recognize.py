@@ -183,8 +183,13 @@ def test_tile_tunables_select_distinct_realisations():
         for st in (1, 2, 3):
             keys.add(realisation_key(dc_replace(spec, block_m=bm, stages=st), None, "none"))
     assert len(keys) == 2  # one 256-row item -> always 128 rows here; {shallow, deep} ring at D=64
+    # short D=64 KV ranges (<= 1024 keys) always take 128-row items (capi.cu
+    # attn_item_rows); at 2048 keys the (4 x 32 x 8) items choose {128, 256} rows
     keys = {realisation_key(dc_replace(spec, block_m=bm, stages=st), (4, 32, 8), "none")
             for bm in (16, 32, 64, 128) for st in (1, 2, 3)}
-    assert len(keys) == 4  # (4 x 32) items: {128, 256} rows x {shallow, deep} ring
+    assert len(keys) == 2
+    keys = {realisation_key(dc_replace(spec, block_m=bm, stages=st, n=2048, m=2048), (4, 32, 8), "none")
+            for bm in (16, 32, 64, 128) for st in (1, 2, 3)}
+    assert len(keys) == 4  # {128, 256} rows x {shallow, deep} ring
     assert recognize(_load("attn256_t32x64.seed0.ma.json"))[0].gpu_bm == 128
     assert recognize(_load("bert512.seed0.ma.json"))[0].gpu_bm == 128  # 2 items of 256 < 148 / 2

@@ -24,8 +24,10 @@ def _args(B, Hq, Hkv, N, M, D, mask):
     return a
 
 
-def _rows(B, Hq, N):
+def _rows(B, Hq, N, D=128, M=None):
     """Library choice of query rows per work item (capi.cu attn_item_rows, item_rows = 0)."""
+    if D == 64 and M is not None and M <= 1024:
+        return 128
     return 128 if (N + 255) // 256 * B * Hq * 2 < SMS else 256
 
 
@@ -54,7 +56,7 @@ def _makespan(nk_lpt, BH, s, ctas):
 
 def _plan(B, Hq, N, M, D, causal):
     """Restatement of attn_split_plan: (kv_split, n_units, workspace bytes)."""
-    rows = _rows(B, Hq, N)
+    rows = _rows(B, Hq, N, D, M)
     nmb = (N + rows - 1) // rows
     BH = B * Hq
     nk = [_nkv(mb, N, M, causal, rows=rows) for mb in range(nmb)]
@@ -79,9 +81,9 @@ def _plan(B, Hq, N, M, D, causal):
     return S, units, prefix + ml + units * rows * D * 2  # bf16 partials
 
 
-def _units(B, Hq, N, M, causal, S):
+def _units(B, Hq, N, M, causal, S, D=128):
     """Restatement of the kernel's unit map: unit -> (b*Hq + hq, m-block, first tile, tiles)."""
-    rows = _rows(B, Hq, N)
+    rows = _rows(B, Hq, N, D, M)
     nmb = (N + rows - 1) // rows
     BH = B * Hq
     prefix = [0]
@@ -116,16 +118,16 @@ def test_split_plan_matches_library_and_covers_every_tile(B, Hq, Hkv, N, M, D, c
     if S == 0:
         return
     cover = {}
-    for bh, mb, lo, n in _units(B, Hq, N, M, causal, S):
+    for bh, mb, lo, n in _units(B, Hq, N, M, causal, S, D):
         assert 1 <= n <= S
         for j in range(lo, lo + n):
             cover[(bh, mb, j)] = cover.get((bh, mb, j), 0) + 1
-    rows = _rows(B, Hq, N)
+    rows = _rows(B, Hq, N, D, M)
     nmb = (N + rows - 1) // rows
     want = {(bh, mb, j) for bh in range(B * Hq) for mb in range(nmb)
             for j in range(_nkv(mb, N, M, causal, rows=rows))}
     assert set(cover) == want and all(v == 1 for v in cover.values())
-    assert len(_units(B, Hq, N, M, causal, S)) == units
+    assert len(_units(B, Hq, N, M, causal, S, D)) == units
 
 
 def test_tensor_masks_are_never_split():
