@@ -326,3 +326,29 @@ def test_e4m3_paged_decode_is_bitwise_the_dense_decode():
                     max_seq_kv=M, num_splits=6, **kw).launch()
     torch.cuda.synchronize()
     assert torch.equal(o1, o2)
+
+
+@pytest.mark.parametrize("e4m3", [False, True])
+def test_decode_with_an_empty_split(e4m3):
+    """129 keys over 3 splits of 128-key ranges: the third split has no keys (its four
+    quarter partials merge to weight 0) and the second holds one key."""
+    from paper_2604_14825_b200.runtime import DecodePlan
+
+    B, Hq, Hkv, M, D = 2, 8, 2, 129, 128
+    g = np.random.default_rng(129)
+    if e4m3:
+        (q, qd, qf), (k, kd, kf), (v, vd, vf) = (_quant_e4m3(g.standard_normal(s))
+                                                 for s in ((B, Hq, 1, D), (B, Hkv, M, D), (B, Hkv, M, D)))
+        kw, tol = dict(q_descale=qd, k_descale=kd, v_descale=vd), dict(max_abs=E4M3_MAX_ABS, rel=E4M3_REL_L2)
+    else:
+        qf, kf, vf = (round_bf16(g.standard_normal(s)) for s in ((B, Hq, 1, D), (B, Hkv, M, D), (B, Hkv, M, D)))
+        q, k, v = (torch.from_numpy(x).bfloat16() for x in (qf, kf, vf))
+        kw, tol = {}, {}
+    o = torch.empty((B, Hq, 1, D), dtype=torch.float32, device="cuda")
+    plan = DecodePlan(q.cuda(), k.cuda(), v.cuda(), o, 1 / np.sqrt(D), num_splits=3, **kw)
+    assert plan.splits == 3
+    plan.launch()
+    torch.cuda.synchronize()
+    plan.check_errors()
+    ref = reference_math.attention_batched_fp64(qf, kf, vf, 1 / np.sqrt(D), False)
+    _check(o.cpu().numpy(), ref, **tol)
