@@ -193,3 +193,17 @@ def test_tile_tunables_select_distinct_realisations():
     assert len(keys) == 4  # {128, 256} rows x {shallow, deep} ring
     assert recognize(_load("attn256_t32x64.seed0.ma.json"))[0].gpu_bm == 128
     assert recognize(_load("bert512.seed0.ma.json"))[0].gpu_bm == 128  # 2 items of 256 < 148 / 2
+
+
+def test_item_rows_rule_matches_the_library():
+    """recognize.attn_effective_rows restates csrc/capi.cu attn_item_rows: explicit 128 /
+    256 win; head_dim 64 with <= 1024 keys -> 128; else 128 only when 256-row items
+    would leave more than half of the SMs idle."""
+    from paper_2604_14825_b200.recognize import attn_effective_rows
+
+    assert attn_effective_rows(256, 512, 384, d=64, m=512) == 256
+    assert attn_effective_rows(0, 512, 384, d=64, m=512) == 128      # BERT-base
+    assert attn_effective_rows(0, 2048, 384, d=64, m=2048) == 256
+    assert attn_effective_rows(0, 512, 384, d=128, m=512) == 256
+    assert attn_effective_rows(0, 256, 1, d=128, m=256) == 128        # one item
+    assert attn_effective_rows(0, 8192, 32, d=128, m=8192) == 256     # Llama 8K
