@@ -9,10 +9,12 @@ for (M, N, K) in [(4096, 128, 4096), (4096, 64, 4096), (4096, 4096, 4096)]:
     a = torch.randn(M, K, device="cuda").bfloat16()
     b = (torch.randn(K, N, device="cuda") / K ** 0.5).bfloat16()
     c = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-    for force in (None, 1):
+    for force in (None, 1, 2, 4, 6, 8):
+        if M == 4096 and N == 4096 and force not in (None, 1):
+            continue
         p = GemmPlan(a, b, c)
         if force:
-            p.args.k_splits = 1
+            p.args.k_splits = min(force, p.args.k_splits) if force > 1 else 1
         for _ in range(3):
             p.launch()
         torch.cuda.synchronize()
