@@ -45,6 +45,29 @@ int choose_splits(int groups, int M, int requested) {
   return best;
 }
 
+#ifndef NT_DECODE_PDL
+#define NT_DECODE_PDL 1
+#endif
+// the repair-law combine as a programmatic dependent launch: its CTAs are scheduled
+// while the split kernel drains (K2b triggers launch_dependents at entry) and wait in
+// griddepcontrol.wait for its completion and memory
+int launch_combine(const DecodeParams& p, int R, cudaStream_t st) {
+  const int rows = p.B * p.Hkv * R;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((rows + 3) / 4);
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = NT_DECODE_PDL;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const int rc = check_cuda(cudaLaunchKernelEx(&cfg, decode_combine_kernel, p, R), "decode_combine launch");
+  g_launches++;
+  return rc;
+}
+
 template <int R, int PG>
 int launch(const CUtensorMap& mk, const CUtensorMap& mv, DecodeParams& p, cudaStream_t st) {
   int rc;
@@ -54,10 +77,7 @@ int launch(const CUtensorMap& mk, const CUtensorMap& mv, DecodeParams& p, cudaSt
   kern<<<grid, kDecodeCTAThreads, kDecodeSmem, st>>>(mk, mv, p);
   g_launches++;
   if ((rc = check_cuda(cudaGetLastError(), "decode_split launch"))) return rc;
-  const int rows = p.B * p.Hkv * R;
-  decode_combine_kernel<<<(rows + 3) / 4, 128, 0, st>>>(p, R);
-  g_launches++;
-  return check_cuda(cudaGetLastError(), "decode_combine launch");
+  return launch_combine(p, R, st);
 }
 template <int PG>
 int dispatch(int R, const CUtensorMap& mk, const CUtensorMap& mv, DecodeParams& p, cudaStream_t st) {
@@ -84,10 +104,7 @@ int launch_tc(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& m
   kern<<<grid, kDtcThreads, smem, st>>>(mq, mk, mv, p);
   g_launches++;
   if ((rc = check_cuda(cudaGetLastError(), "decode_tc launch"))) return rc;
-  const int rows = p.B * p.Hkv * R;
-  decode_combine_kernel<<<(rows + 3) / 4, 128, 0, st>>>(p, R);
-  g_launches++;
-  return check_cuda(cudaGetLastError(), "decode_combine launch");
+  return launch_combine(p, R, st);
 }
 
 template <int PG, bool FP8 = false>

@@ -337,6 +337,7 @@ __global__ void __launch_bounds__(kDecodeCTAThreads, 1)
 
 // combine the split partials of every (group, row); one warp per row
 __global__ void decode_combine_kernel(const DecodeParams p, int R) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // launched as a dependent of the split kernel
   const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   const int ngroups = p.B * p.Hkv;

@@ -124,6 +124,7 @@ __global__ void __launch_bounds__(kDtcThreads, 1)
   const int s = blockIdx.x;
   const int grp = blockIdx.y;  // b * Hkv + hkv
   const int b = grp / p.Hkv, hkv = grp % p.Hkv;
+  asm volatile("griddepcontrol.launch_dependents;");  // the combine may be scheduled now
   const int warp = __shfl_sync(0xffffffffu, threadIdx.x / 32, 0);
   const int lane = threadIdx.x & 31;
   const int j0 = s * p.keys_per_split;  // multiple of kDtcTile
