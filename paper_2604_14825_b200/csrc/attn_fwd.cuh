@@ -818,11 +818,25 @@ __global__ void __launch_bounds__(attn_threads<NQ>(), NQ == 2 ? 1 : 2)
         const int kv0 = (itm.kv_lo + j) * 128;
         if (MASK == MASK_TENSOR) {
           const float* mrow = p.mask + (long long)min(qi, p.N - 1) * p.mask_row_stride;
+          if (kv0 + 128 <= p.M && (reinterpret_cast<uintptr_t>(mrow) & 15) == 0) {
+            // a full tile of a 16-byte aligned row: 32 float4 loads instead of 128 scalar ones
+            const float4* m4 = reinterpret_cast<const float4*>(mrow + kv0);
 #pragma unroll
-          for (int c = 0; c < 128; ++c) {
-            const int kv = kv0 + c;
-            const float mk = (kv < p.M) ? __ldg(mrow + kv) : NINF;
-            s[c] = __float_as_uint(fmaf(__uint_as_float(s[c]), p.scale_log2, mk * 1.4426950408889634f));
+            for (int c4 = 0; c4 < 32; ++c4) {
+              const float4 mk = __ldg(m4 + c4);
+              const float mv[4] = {mk.x, mk.y, mk.z, mk.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                s[4 * c4 + e] = __float_as_uint(
+                    fmaf(__uint_as_float(s[4 * c4 + e]), p.scale_log2, mv[e] * 1.4426950408889634f));
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < 128; ++c) {
+              const int kv = kv0 + c;
+              const float mk = (kv < p.M) ? __ldg(mrow + kv) : NINF;
+              s[c] = __float_as_uint(fmaf(__uint_as_float(s[c]), p.scale_log2, mk * 1.4426950408889634f));
+            }
           }
         } else if (MASK == MASK_BITS) {
           // 128 visibility bits of this row's KV tile in one 16-byte load (bits past M are 0)
