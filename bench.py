@@ -64,8 +64,10 @@ CONFIGS = {
                              golden="causal4k", scale=LLAMA_SCALE, mask="tensor"),
     "bert512": dict(prog="scaled_0p125", B=32, Hq=12, Hkv=12, N=512, D=64, causal=False,
                     golden="bert512", scale=0.125),
+    # latency-bound (two CTAs): each step replays a CUDA graph of the launch, the way a
+    # serving loop issues it (the paper's GH200 ablation: 7.43 us)
     "attn256": dict(prog="attention", B=1, Hq=1, Hkv=1, N=256, D=64, causal=False,
-                    golden="attn256", scale=None),
+                    golden="attn256", scale=None, graph=True),
     # config 5: decode, the 4 q-heads of a GQA group packed as the MA's 4 rows
     "decode32k": dict(kind="decode", prog="llama", B=64, Hq=32, Hkv=8, N=1, M=32768, D=128, causal=False,
                       golden="decode4_32k", scale=LLAMA_SCALE),
@@ -530,6 +532,21 @@ def run_ours(args, cfg, rank, world, dist):
     torch.cuda.synchronize()
     if hasattr(plan, "check_errors") and not os.environ.get("NT_BENCH_NOCHECK"):
         plan.check_errors()
+    launch = plan.launch
+    if cfg.get("graph") and world == 1:
+        # one CUDA graph of the plan's launch (the persistent kernel's work counter resets
+        # itself, so replays are independent); each timed step is one replay
+        graph = torch.cuda.CUDAGraph()
+        c0 = _lib.launch_count()
+        with torch.cuda.graph(graph):
+            plan.launch(torch.cuda.current_stream())
+        graph_kernels = _lib.launch_count() - c0  # our kernels per replay
+        for _ in range(args.warmup):
+            graph.replay()
+        torch.cuda.synchronize()
+
+        def launch(_stream):
+            graph.replay()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     if world > 1:
@@ -540,13 +557,15 @@ def run_ours(args, cfg, rank, world, dist):
         for i in range(args.steps):
             flush.zero_()
             ev[i][0].record(stream)
-            plan.launch(stream)
+            launch(stream)
             ev[i][1].record(stream)
             if world > 1:
                 gather()
             ev[i][2].record(stream)
         torch.cuda.synchronize()
     launches = _lib.launch_count() - l0
+    if cfg.get("graph") and world == 1:
+        launches = graph_kernels * args.steps  # replays do not pass through the library's counter
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
