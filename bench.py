@@ -560,8 +560,10 @@ def run_ours(args, cfg, rank, world, dist):
             launch(stream)
             ev[i][1].record(stream)
             if world > 1:
+                # the step adds the all-gather; one process has nothing to add (a third
+                # back-to-back event record alone measured ~2.5 us on the device timeline)
                 gather()
-            ev[i][2].record(stream)
+                ev[i][2].record(stream)
         torch.cuda.synchronize()
     launches = _lib.launch_count() - l0
     if cfg.get("graph") and world == 1:
@@ -570,7 +572,7 @@ def run_ours(args, cfg, rank, world, dist):
         dist.barrier()
     torch.cuda.synchronize()
     kern_ms = [a.elapsed_time(b) for a, b, _ in ev]
-    step_ms = [a.elapsed_time(c) for a, _, c in ev]
+    step_ms = [a.elapsed_time(c) for a, _, c in ev] if world > 1 else kern_ms
     ms_kernel_local = statistics.mean(kern_ms)
     ms_kernel, ms_step = ms_kernel_local, statistics.mean(step_ms)
     if world > 1:
