@@ -281,7 +281,8 @@ def _paged_e4m3(k8, v8, page_size, layout, seed):
     return as8(kp), as8(vp), torch.from_numpy(bt).cuda()
 
 
-@pytest.mark.parametrize("page_size,layout", [(16, "NHD"), (64, "HND"), (128, "NHD"), (256, "HND")])
+@pytest.mark.parametrize("page_size,layout", [(16, "NHD"), (64, "HND"), (128, "NHD"), (256, "HND"), (8, "NHD"),
+                                              (32, "HND")])
 def test_e4m3_paged_decode_vs_fp64(page_size, layout):
     """FP8 paged cache, ragged sequence lengths, vs fp64 of the dequantised inputs."""
     from paper_2604_14825_b200.runtime import PagedDecodePlan
